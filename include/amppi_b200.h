@@ -1,0 +1,211 @@
+/* amppi_b200 — B200-native AERO-MPPI plan-cycle hot path, C ABI.
+ *
+ * Drop-in boundary for the reference planner's two hot-path entry points:
+ *
+ *   PerceptionSnapshot build_snapshot(const PointCloudBuffer&, const State& pose,
+ *                                     double r_max = 10.0);
+ *       proj/include/amppi/perception.hpp:142-143, proj/src/perception.cpp:237-246
+ *       -> amppi_snapshot() / amppi_snapshot_f64()
+ *
+ *   PlanResult plan_step(const State& x, const GoalSpec& goal,
+ *                        const PerceptionSnapshot& snap, const EnsembleConfig& cfg,
+ *                        const NominalSequence& previous,
+ *                        const ControlInput& last_applied, std::uint64_t cycle,
+ *                        std::uint64_t seed, PlanScratch& scratch);
+ *       proj/include/amppi/ensemble.hpp:59-69, proj/src/ensemble.cpp:29-179
+ *       -> amppi_plan()
+ *
+ * plus a batched-scene form of the same cycle (amppi_cycle_batch*, SURVEY.md
+ * §8 config C5).  Plain C types only: pointers, sizes, POD structs.  No
+ * exceptions cross the ABI; every call returns an amppi_status and the
+ * message of the last failure is available from amppi_last_error().  The C++
+ * shim include/amppi_b200.hpp re-creates the reference signatures and
+ * exceptions on top of this header.
+ *
+ * Threading: one context per host thread; calls on one context are
+ * serialised by the caller.  Host-pointer calls are synchronous (outputs are
+ * in caller memory on return); *_device calls are asynchronous on the
+ * context's stream.
+ */
+#ifndef AMPPI_B200_H
+#define AMPPI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMPPI_ABI_VERSION 1
+
+typedef enum {
+  AMPPI_OK = 0,
+  AMPPI_PLANNING_FAILED = 1,   /* every instance invalid: std::runtime_error("planning failed"), ensemble.cpp:158 */
+  AMPPI_INVALID_ARGUMENT = 2,  /* std::invalid_argument */
+  AMPPI_CUDA_ERROR = 3,
+  AMPPI_NCCL_ERROR = 4,
+  AMPPI_NO_SNAPSHOT = 5        /* amppi_plan before any amppi_snapshot */
+} amppi_status;
+
+/* Plain mirror of EnsembleConfig (ensemble.hpp:16-23) and its nested
+ * AnchorGrid (guidance.hpp:10-19), MppiConfig (mppi.hpp:14-21), CostWeights /
+ * CollisionParams (costs.hpp:13-29) and DynamicsParams (types.hpp:40-53).
+ * mppi_dt is MppiConfig::dt (guide horizon N*dt); dyn_dt is DynamicsParams::dt
+ * (RK4 step, tracking-cost time base) — they are distinct in the reference. */
+typedef struct {
+  int32_t m_h, m_v;
+  double lookahead, spacing_deg, terminal_speed, min_anchor_distance;
+  int32_t rollouts, horizon;
+  double lambda;
+  double sigma[4];
+  double mppi_dt;
+  int32_t iterations;
+  double q_track, q_vnorm, q_c, q_c_delta, q_p, q_v, q_q;
+  double col_scale, col_slope, col_d_min, col_d_max;
+  double mass;
+  double gravity[3];
+  double dyn_dt;
+  double thrust_min, thrust_max, omega_xy_max, omega_z_max;
+  double replan_hz, r_max;
+} amppi_config;
+
+/* State x = [p, q, v]; q scalar-first (w, x, y, z) as in types.hpp:13-26. */
+typedef struct {
+  double p[3];
+  double q[4];
+  double v[3];
+} amppi_state;
+
+/* ControlInput (types.hpp:29-38): collective thrust [N], body rates [rad/s]. */
+typedef struct {
+  double thrust;
+  double omega[3];
+} amppi_control;
+
+/* GoalSpec (costs.hpp:42-56). */
+typedef struct {
+  double p_goal[3];
+  double v_goal[3];
+  double q_goal[4];
+} amppi_goal;
+
+typedef struct {
+  int32_t device;          /* CUDA ordinal */
+  int32_t precision;       /* 32: FP32 stage-I screening + FP64 softmin support (default)
+                              64: FP64 stage I */
+  int32_t max_scenes;      /* batch capacity (>= 1) */
+  int64_t max_points;      /* total point capacity over a batch */
+  int32_t profile;         /* 1: time every kernel with CUDA events */
+  void* stream;            /* optional cudaStream_t to launch on; NULL: own stream */
+} amppi_options;
+
+/* PlanResult (ensemble.hpp:33-41) as caller-owned buffers; any pointer may be
+ * NULL.  Sizes: M = m_h*m_v, N = horizon, K = rollouts. */
+typedef struct {
+  int32_t winner;              /* out */
+  amppi_control control;       /* out: clamp(nominal_winner[0]) */
+  double breakdown[5];         /* out: track, vnorm, ctrl, goal, collision (costs.hpp:165-187) */
+  double* stage1;              /* [M] InstanceRecord::stage1 */
+  double* stage2;              /* [M] InstanceRecord::stage2 (+inf when invalid) */
+  double* ess;                 /* [M] */
+  uint8_t* valid;              /* [M] */
+  double* nominal;             /* [M*N*4] updated nominal per instance (NaN when invalid) */
+  double* winner_states;       /* [(N+1)*10] winner_rollout states p,q(wxyz),v */
+  double* winner_controls;     /* [N*4] winner_rollout controls */
+  double* anchor_initial;      /* [M*3] Anchor::initial_endpoint */
+  double* anchor_refined;      /* [M*3] */
+  double* anchor_safe_dir;     /* [M*3] */
+  double* anchor_safe_range;   /* [M] */
+  int32_t* anchor_ij;          /* [M*2] coarse (I, J) */
+  double* guide_coeffs;        /* [M*3*6] GuidingTrajectory::coeffs, [m][axis][power] */
+  double* sample_costs;        /* [M*K] stage-I cost of every sample, last iteration (verification) */
+} amppi_plan_result;
+
+/* Snapshot contents for verification (SphericalPartition / CoarsePartition /
+ * FilteredCloud, perception.hpp:60-94).  Cell arrays use flat(i,j)=i*60+j. */
+typedef struct {
+  double* ranges;              /* [7200] */
+  uint8_t* has_point;          /* [7200] */
+  double* nearest;             /* [7200*3] body frame (0 where empty) */
+  double* safe_range;          /* [200] flat(I,J)=I*10+J */
+  double* safe_dir;            /* [200*3] body frame */
+  double* safe_point;          /* [200*3] */
+  double* filtered;            /* [<=7200*3] world frame, flat-cell order */
+  int64_t n_filtered;          /* out */
+} amppi_snapshot_view;
+
+/* Batched scenes: scene s owns points [point_offsets[s], point_offsets[s+1]).
+ * Host-pointer form (amppi_cycle_batch) copies inputs in and results out;
+ * device form (amppi_cycle_batch_device) takes device pointers for every
+ * array and enqueues on the context stream. */
+typedef struct {
+  int32_t n_scenes;
+  const int64_t* point_offsets;     /* [n_scenes+1] */
+  const float* xyz;                 /* [total*3] world frame, float32 */
+  const amppi_state* poses;         /* [n_scenes] snapshot pose */
+  const amppi_state* states;        /* [n_scenes] plan state x */
+  const amppi_goal* goals;          /* [n_scenes] */
+  const double* previous;           /* [n_scenes*N*4] or NULL */
+  const int32_t* previous_len;      /* [n_scenes] (0 or N) or NULL */
+  const amppi_control* last_applied;/* [n_scenes] */
+  const uint64_t* cycles;           /* [n_scenes] */
+  const uint64_t* seeds;            /* [n_scenes] */
+  double r_max;
+} amppi_batch_input;
+
+typedef struct {
+  int32_t* status;                  /* [n_scenes] 0 ok, 1 planning failed */
+  int32_t* winner;                  /* [n_scenes] */
+  double* control;                  /* [n_scenes*4] */
+  double* winner_nominal;           /* [n_scenes*N*4] */
+  double* stage2;                   /* [n_scenes*M] */
+  double* breakdown;                /* [n_scenes*5] */
+} amppi_batch_output;
+
+typedef struct amppi_ctx amppi_ctx;
+
+void amppi_config_default(amppi_config* cfg);
+void amppi_options_default(amppi_options* opt);
+int amppi_abi_version(void);
+
+/* Context: device arenas sized from cfg/opt, one stream, cached CUDA graphs. */
+int amppi_create(const amppi_config* cfg, const amppi_options* opt, amppi_ctx** out);
+int amppi_destroy(amppi_ctx* ctx);
+const char* amppi_last_error(const amppi_ctx* ctx);
+int amppi_synchronize(amppi_ctx* ctx);
+
+/* == build_snapshot(buffer, pose, r_max): the buffer's frames concatenated
+ * oldest-first (PointCloudBuffer::body_points order, perception.cpp:55-62). */
+int amppi_snapshot(amppi_ctx* ctx, const float* world_xyz, int64_t n_points,
+                   const amppi_state* pose, double r_max);
+int amppi_snapshot_f64(amppi_ctx* ctx, const double* world_xyz, int64_t n_points,
+                       const amppi_state* pose, double r_max);
+int amppi_snapshot_download(amppi_ctx* ctx, amppi_snapshot_view* view);
+
+/* == plan_step(x, goal, snapshot, cfg, previous, last_applied, cycle, seed).
+ * previous: previous_len controls (N*4) or NULL/0 (hover warm start,
+ * ensemble.cpp:68-77).  injected_delta: NULL for the reference RNG stream, or
+ * [iterations*M*K*N*4] perturbations replacing the draws (verification).
+ * Returns AMPPI_PLANNING_FAILED when every instance is invalid. */
+int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal,
+               const double* previous, int32_t previous_len, const amppi_control* last_applied,
+               uint64_t cycle, uint64_t seed, const double* injected_delta,
+               amppi_plan_result* out);
+
+/* Snapshot + plan for a batch of independent scenes (one plan cycle each). */
+int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_output* out);
+int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in_device,
+                             amppi_batch_output* out_device);
+
+/* Profiling: per-kernel device time accumulated since the last reset
+ * (requires opt.profile = 1).  names/ms/launches are caller arrays of cap. */
+int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches,
+                       int32_t cap, int32_t* count);
+int amppi_kernel_times_reset(amppi_ctx* ctx);
+int amppi_set_stream(amppi_ctx* ctx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMPPI_B200_H */

@@ -1,0 +1,839 @@
+// Host runtime behind include/amppi_b200.h: context, device arenas, pinned
+// staging, kernel sequencing and the C-ABI entry points.  No CPU compute path:
+// every planning result comes from the CUDA kernels in k_*.cu; a context
+// cannot be created without a CUDA device.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "../../include/amppi_b200.h"
+#include "kernels.h"
+#include "layout.h"
+
+using namespace amppi_dev;
+
+namespace {
+
+constexpr double kPi = std::numbers::pi;
+
+struct Arena {
+  std::vector<void*> blocks;
+  cudaError_t alloc(void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) blocks.push_back(*p);
+    return e;
+  }
+  void release() {
+    for (void* p : blocks) cudaFree(p);
+    blocks.clear();
+  }
+};
+
+// Contiguous per-scene input block for one-copy uploads.
+struct InputBlock {
+  double* poses;
+  double* states;
+  double* goals;
+  double* last;
+  double* prev;
+  int64_t* offsets;
+  uint64_t* cycles;
+  uint64_t* seeds;
+  int32_t* prev_len;
+  size_t bytes;
+};
+
+template <typename T>
+T* carve(unsigned char*& cur, size_t count) {
+  const size_t align = 16;
+  uintptr_t p = reinterpret_cast<uintptr_t>(cur);
+  p = (p + align - 1) & ~(align - 1);
+  T* out = reinterpret_cast<T*>(p);
+  cur = reinterpret_cast<unsigned char*>(p + count * sizeof(T));
+  return out;
+}
+
+InputBlock layout_inputs(unsigned char* base, int S, int N) {
+  InputBlock b{};
+  unsigned char* cur = base;
+  b.poses = carve<double>(cur, static_cast<size_t>(S) * 10);
+  b.states = carve<double>(cur, static_cast<size_t>(S) * 10);
+  b.goals = carve<double>(cur, static_cast<size_t>(S) * 10);
+  b.last = carve<double>(cur, static_cast<size_t>(S) * 4);
+  b.prev = carve<double>(cur, static_cast<size_t>(S) * N * 4);
+  b.offsets = carve<int64_t>(cur, static_cast<size_t>(S) + 1);
+  b.cycles = carve<uint64_t>(cur, S);
+  b.seeds = carve<uint64_t>(cur, S);
+  b.prev_len = carve<int32_t>(cur, S);
+  b.bytes = static_cast<size_t>(cur - base) + 16;
+  return b;
+}
+
+// Contiguous single-scene result block for one-copy downloads.
+struct ResultBlock {
+  int32_t* winner;
+  int32_t* status;
+  uint8_t* valid;
+  uint8_t* alive;
+  double* control;
+  double* stage1;
+  double* stage2;
+  double* ess;
+  double* breakdown;
+  double* nominal;
+  double* anchor_init;
+  double* anchor_ref;
+  double* anchor_dir;
+  double* anchor_range;
+  int32_t* anchor_ij;
+  double* guide_coef;
+  uint32_t* n_support;
+  size_t bytes;
+};
+
+ResultBlock layout_results(unsigned char* base, int S, int M, int N) {
+  ResultBlock r{};
+  unsigned char* cur = base;
+  const size_t SM = static_cast<size_t>(S) * M;
+  r.winner = carve<int32_t>(cur, S);
+  r.status = carve<int32_t>(cur, S);
+  r.valid = carve<uint8_t>(cur, SM);
+  r.alive = carve<uint8_t>(cur, SM);
+  r.control = carve<double>(cur, static_cast<size_t>(S) * 4);
+  r.stage1 = carve<double>(cur, SM);
+  r.stage2 = carve<double>(cur, SM);
+  r.ess = carve<double>(cur, SM);
+  r.breakdown = carve<double>(cur, SM * 5);
+  r.nominal = carve<double>(cur, SM * N * 4);
+  r.anchor_init = carve<double>(cur, SM * 3);
+  r.anchor_ref = carve<double>(cur, SM * 3);
+  r.anchor_dir = carve<double>(cur, SM * 3);
+  r.anchor_range = carve<double>(cur, SM);
+  r.anchor_ij = carve<int32_t>(cur, SM * 2);
+  r.guide_coef = carve<double>(cur, SM * 18);
+  r.n_support = carve<uint32_t>(cur, SM);
+  r.bytes = static_cast<size_t>(cur - base) + 16;
+  return r;
+}
+
+}  // namespace
+
+struct amppi_ctx {
+  amppi_config cfg{};
+  amppi_options opt{};
+  DevConfig dc{};
+  cudaStream_t stream{nullptr};
+  bool own_stream{false};
+  std::string err;
+  int S_cap{1};
+  int64_t P_cap{0};
+  Arena arena;
+  // inputs
+  unsigned char* d_in{nullptr};
+  unsigned char* h_in{nullptr};  // pinned mirror
+  InputBlock din{}, hin{};
+  float* d_xyz{nullptr};
+  double* d_xyz64{nullptr};
+  float* h_xyz{nullptr};  // pinned staging
+  size_t h_xyz_bytes{0};
+  double* d_injected{nullptr};
+  size_t injected_bytes{0};
+  // results
+  unsigned char* d_res{nullptr};
+  unsigned char* h_res{nullptr};
+  ResultBlock dres{}, hres{};
+  // device state
+  Perception P{};
+  Plan pl{};
+  uint32_t* cand_k{nullptr};
+  double* cand_s{nullptr};
+  double* cand_w{nullptr};
+  unsigned char* d_gather{nullptr};
+  // single-scene snapshot bookkeeping
+  bool have_snapshot{false};
+  double snap_r_max{10.0};
+  double snap_pose[10]{};
+  int64_t snap_points{0};
+  KernelTimer timer;
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* where) {
+    err = std::string(where) + ": " + cudaGetErrorString(e);
+    return AMPPI_CUDA_ERROR;
+  }
+};
+
+#define CK(expr)                                              \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ctx->cuda_fail(_e, #expr);  \
+  } while (0)
+
+namespace {
+
+DevConfig to_dev(const amppi_config& c) {
+  DevConfig d{};
+  d.m_h = c.m_h;
+  d.m_v = c.m_v;
+  d.M = c.m_h * c.m_v;
+  d.K = c.rollouts;
+  d.N = c.horizon;
+  d.iterations = c.iterations;
+  d.lookahead = c.lookahead;
+  d.spacing_deg = c.spacing_deg;
+  d.terminal_speed = c.terminal_speed;
+  d.min_anchor_distance = c.min_anchor_distance;
+  d.lambda = c.lambda;
+  for (int i = 0; i < 4; ++i) d.sigma[i] = c.sigma[i];
+  d.mppi_dt = c.mppi_dt;
+  d.q_track = c.q_track;
+  d.q_vnorm = c.q_vnorm;
+  d.q_c = c.q_c;
+  d.q_c_delta = c.q_c_delta;
+  d.q_p = c.q_p;
+  d.q_v = c.q_v;
+  d.q_q = c.q_q;
+  d.col_scale = c.col_scale;
+  d.col_slope = c.col_slope;
+  d.col_d_min = c.col_d_min;
+  d.col_d_max = c.col_d_max;
+  d.mass = c.mass;
+  for (int i = 0; i < 3; ++i) d.gravity[i] = c.gravity[i];
+  d.dyn_dt = c.dyn_dt;
+  d.thrust_min = c.thrust_min;
+  d.thrust_max = c.thrust_max;
+  d.omega_xy_max = c.omega_xy_max;
+  d.omega_z_max = c.omega_z_max;
+  d.r_max = c.r_max;
+  return d;
+}
+
+std::string validate(const amppi_config& c) {
+  if (c.m_h < 1 || c.m_v < 1) return "anchor grid must be at least 1x1";
+  if (c.m_h * c.m_v > 1024) return "at most 1024 anchors";
+  if (c.rollouts < 1) return "rollouts must be positive";
+  if (c.horizon < 1 || c.horizon > 64) return "horizon must be in [1, 64]";
+  if (c.iterations < 1) return "iterations must be positive";
+  if (!(c.lambda > 0.0)) return "lambda must be positive";
+  if (!(c.mass > 0.0)) return "mass must be positive";
+  if (!(c.dyn_dt > 0.0) || !(c.mppi_dt > 0.0)) return "dt must be positive";
+  if (!(c.col_d_max > 0.0)) return "d_obs_max must be positive";
+  if (!(c.r_max > 0.0)) return "r_max must be positive";
+  return "";
+}
+
+// cell_direction(i, j) for every fine cell (perception.cpp:36-42), host libm.
+std::vector<double> cell_direction_table() {
+  std::vector<double> t(static_cast<size_t>(kCells) * 3);
+  const double az_step = 2.0 * kPi / kAz, el_step = kPi / kEl;
+  for (int i = 0; i < kAz; ++i)
+    for (int j = 0; j < kEl; ++j) {
+      const double az = -kPi + (i + 0.5) * az_step;
+      const double el = -0.5 * kPi + (j + 0.5) * el_step;
+      const double ce = std::cos(el);
+      double* o = t.data() + 3 * (i * kEl + j);
+      o[0] = ce * std::cos(az);
+      o[1] = ce * std::sin(az);
+      o[2] = std::sin(el);
+    }
+  return t;
+}
+
+int alloc_points(amppi_ctx* ctx, int64_t P) {
+  if (P <= ctx->P_cap && ctx->d_xyz) return AMPPI_OK;
+  const int64_t cap = std::max<int64_t>(P, 1024);
+  if (ctx->d_xyz) cudaFree(ctx->d_xyz);
+  if (ctx->d_xyz64) cudaFree(ctx->d_xyz64);
+  if (ctx->P.cand) cudaFree(ctx->P.cand);
+  if (ctx->h_xyz) cudaFreeHost(ctx->h_xyz);
+  ctx->d_xyz = nullptr;
+  ctx->d_xyz64 = nullptr;
+  ctx->P.cand = nullptr;
+  ctx->h_xyz = nullptr;
+  CK(cudaMalloc(&ctx->d_xyz, static_cast<size_t>(cap) * 3 * sizeof(float)));
+  CK(cudaMalloc(&ctx->d_xyz64, static_cast<size_t>(cap) * 3 * sizeof(double)));
+  CK(cudaMalloc(&ctx->P.cand, static_cast<size_t>(cap) * sizeof(Candidate)));
+  ctx->h_xyz_bytes = static_cast<size_t>(cap) * 3 * sizeof(double);
+  CK(cudaMallocHost(&ctx->h_xyz, ctx->h_xyz_bytes));
+  ctx->P.cand_cap = cap;
+  ctx->P_cap = cap;
+  return AMPPI_OK;
+}
+
+int create_impl(amppi_ctx* ctx) {
+  const int S = ctx->S_cap;
+  const DevConfig& dc = ctx->dc;
+  const int M = dc.M, K = dc.K, N = dc.N;
+  const size_t SM = static_cast<size_t>(S) * M;
+  CK(cudaSetDevice(ctx->opt.device));
+  if (ctx->opt.stream) {
+    ctx->stream = static_cast<cudaStream_t>(ctx->opt.stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  CK(init_kernel_attributes());
+  Arena& A = ctx->arena;
+  // inputs (device + pinned mirror with identical layout)
+  {
+    const InputBlock probe = layout_inputs(nullptr, S, N);
+    void* p = nullptr;
+    CK(A.alloc(&p, probe.bytes));
+    ctx->d_in = static_cast<unsigned char*>(p);
+    CK(cudaMallocHost(&p, probe.bytes));
+    ctx->h_in = static_cast<unsigned char*>(p);
+    ctx->din = layout_inputs(ctx->d_in, S, N);
+    ctx->hin = layout_inputs(ctx->h_in, S, N);
+  }
+  {
+    const ResultBlock probe = layout_results(nullptr, S, M, N);
+    void* p = nullptr;
+    CK(A.alloc(&p, probe.bytes));
+    ctx->d_res = static_cast<unsigned char*>(p);
+    CK(cudaMemset(ctx->d_res, 0, probe.bytes));
+    CK(cudaMallocHost(&p, probe.bytes));
+    ctx->h_res = static_cast<unsigned char*>(p);
+    ctx->dres = layout_results(ctx->d_res, S, M, N);
+    ctx->hres = layout_results(ctx->h_res, S, M, N);
+  }
+  if (int rc = alloc_points(ctx, std::max<int64_t>(ctx->opt.max_points, 1024)); rc != AMPPI_OK) return rc;
+
+  Perception& P = ctx->P;
+  void* p = nullptr;
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCells * sizeof(uint64_t)));
+  P.cell_r = static_cast<uint64_t*>(p);
+  CK(cudaMemset(P.cell_r, 0xFF, static_cast<size_t>(S) * kCells * sizeof(uint64_t)));
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCells * sizeof(uint32_t)));
+  P.cell_idx = static_cast<uint32_t*>(p);
+  CK(cudaMemset(P.cell_idx, 0xFF, static_cast<size_t>(S) * kCells * sizeof(uint32_t)));
+  CK(A.alloc(&p, sizeof(unsigned long long)));
+  P.cand_count = static_cast<unsigned long long*>(p);
+  {
+    const std::vector<double> dirs = cell_direction_table();
+    CK(A.alloc(&p, dirs.size() * sizeof(double)));
+    CK(cudaMemcpy(p, dirs.data(), dirs.size() * sizeof(double), cudaMemcpyHostToDevice));
+    P.cell_dir = static_cast<const double*>(p);
+  }
+  if (S <= 64) {  // verification views (single-scene API)
+    CK(A.alloc(&p, static_cast<size_t>(S) * kCells * sizeof(double)));
+    P.ranges = static_cast<double*>(p);
+    CK(A.alloc(&p, static_cast<size_t>(S) * kCells));
+    P.has_point = static_cast<uint8_t*>(p);
+    CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 3 * sizeof(double)));
+    P.nearest = static_cast<double*>(p);
+  }
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 3 * sizeof(double)));
+  P.filtered = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCoarse * sizeof(double)));
+  P.safe_range = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCoarse * 3 * sizeof(double)));
+  P.safe_dir = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCoarse * 3 * sizeof(double)));
+  P.safe_point = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(int32_t)));
+  P.n_filtered = static_cast<int32_t*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(GridMeta)));
+  P.grid = static_cast<GridMeta*>(p);
+  CK(cudaMemset(P.grid, 0, static_cast<size_t>(S) * sizeof(GridMeta)));
+  CK(A.alloc(&p, static_cast<size_t>(S) * (kGridCells + 1) * sizeof(uint32_t)));
+  P.grid_start = static_cast<uint32_t*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kOccWords * sizeof(uint32_t)));
+  P.grid_occ = static_cast<uint32_t*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 3 * sizeof(double)));
+  P.grid_pts64 = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCells * sizeof(float4)));
+  P.grid_pts32 = static_cast<float4*>(p);
+
+  Plan& pl = ctx->pl;
+  const ResultBlock& r = ctx->dres;
+  pl.anchor_init = r.anchor_init;
+  pl.anchor_ref = r.anchor_ref;
+  pl.anchor_dir = r.anchor_dir;
+  pl.anchor_range = r.anchor_range;
+  pl.anchor_ij = r.anchor_ij;
+  pl.guide_coef = r.guide_coef;
+  pl.nominal = r.nominal;
+  pl.alive = r.alive;
+  pl.stage1 = r.stage1;
+  pl.stage2 = r.stage2;
+  pl.ess = r.ess;
+  pl.valid = r.valid;
+  pl.breakdown = r.breakdown;
+  pl.n_support = r.n_support;
+  pl.winner = r.winner;
+  pl.status = r.status;
+  pl.control = r.control;
+  CK(A.alloc(&p, SM * N * 3 * sizeof(double)));
+  pl.guide64 = static_cast<double*>(p);
+  CK(A.alloc(&p, SM * N * sizeof(float4)));
+  pl.guide32 = static_cast<float4*>(p);
+  CK(A.alloc(&p, SM * K * sizeof(float)));
+  pl.cost32 = static_cast<float*>(p);
+  CK(A.alloc(&p, SM * K * sizeof(double)));
+  pl.cost64 = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(int32_t)));
+  pl.done = static_cast<int32_t*>(p);
+  CK(cudaMemset(pl.done, 0, static_cast<size_t>(S) * sizeof(int32_t)));
+  CK(A.alloc(&p, static_cast<size_t>(S) * (N + 1) * 10 * sizeof(double)));
+  pl.winner_states = static_cast<double*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * N * 4 * sizeof(double)));
+  pl.winner_controls = static_cast<double*>(p);
+  CK(A.alloc(&p, SM * K * sizeof(uint32_t)));
+  ctx->cand_k = static_cast<uint32_t*>(p);
+  CK(A.alloc(&p, SM * K * sizeof(double)));
+  ctx->cand_s = static_cast<double*>(p);
+  CK(A.alloc(&p, SM * K * sizeof(double)));
+  ctx->cand_w = static_cast<double*>(p);
+  ctx->timer.enabled = ctx->opt.profile != 0;
+  return AMPPI_OK;
+}
+
+BatchIn batch_from_block(amppi_ctx* ctx, int S, double r_max, bool f64_points) {
+  BatchIn in{};
+  in.xyz = ctx->d_xyz;
+  in.xyz64 = f64_points ? ctx->d_xyz64 : nullptr;
+  in.offsets = ctx->din.offsets;
+  in.poses = ctx->din.poses;
+  in.states = ctx->din.states;
+  in.goals = ctx->din.goals;
+  in.prev = ctx->din.prev;
+  in.prev_len = ctx->din.prev_len;
+  in.last_applied = ctx->din.last;
+  in.cycles = ctx->din.cycles;
+  in.seeds = ctx->din.seeds;
+  in.injected = nullptr;
+  in.S = S;
+  in.r_max = r_max;
+  return in;
+}
+
+int run_cycle(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, bool do_snapshot, bool do_plan,
+              bool winner_rollout) {
+  if (do_snapshot) {
+    cudaError_t e = launch_snapshot(in, ctx->P, ctx->dc, max_pts_scene, ctx->stream, &ctx->timer);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_snapshot");
+  }
+  if (do_plan) {
+    cudaError_t e = launch_plan_impl(in, ctx->P, ctx->pl, ctx->dc, ctx->opt.precision, winner_rollout, ctx->cand_k,
+                                     ctx->cand_s, ctx->cand_w, ctx->stream, &ctx->timer);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_plan");
+  }
+  return AMPPI_OK;
+}
+
+int sync_and_collect(amppi_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->timer.enabled) ctx->timer.collect();
+  return AMPPI_OK;
+}
+
+void put_pose(double* o, const amppi_state* s) {
+  std::memcpy(o, s, 10 * sizeof(double));
+}
+
+}  // namespace
+
+extern "C" {
+
+int amppi_abi_version(void) { return AMPPI_ABI_VERSION; }
+
+void amppi_config_default(amppi_config* c) {
+  // Table I defaults, i.e. the reference's EnsembleConfig{} (ensemble.hpp:16-23)
+  c->m_h = 5;
+  c->m_v = 3;
+  c->lookahead = 5.0;
+  c->spacing_deg = 18.0;
+  c->terminal_speed = 3.0;
+  c->min_anchor_distance = 0.5;
+  c->rollouts = 128;
+  c->horizon = 25;
+  c->lambda = 0.1;
+  c->sigma[0] = 1.0;
+  c->sigma[1] = 1.0;
+  c->sigma[2] = 1.0;
+  c->sigma[3] = 0.5;
+  c->mppi_dt = 0.05;
+  c->iterations = 1;
+  c->q_track = 15.0;
+  c->q_vnorm = 0.15;
+  c->q_c = 0.5;
+  c->q_c_delta = 0.5;
+  c->q_p = 3.0;
+  c->q_v = 0.25;
+  c->q_q = 1.0;
+  c->col_scale = 1.0e6;
+  c->col_slope = 5.0;
+  c->col_d_min = 0.4;
+  c->col_d_max = 1.0;
+  c->mass = 1.0;
+  c->gravity[0] = 0.0;
+  c->gravity[1] = 0.0;
+  c->gravity[2] = -9.81;
+  c->dyn_dt = 0.05;
+  c->thrust_min = 0.3;
+  c->thrust_max = 16.35;
+  c->omega_xy_max = 3.0;
+  c->omega_z_max = 2.0;
+  c->replan_hz = 50.0;
+  c->r_max = 10.0;
+}
+
+void amppi_options_default(amppi_options* o) {
+  o->device = 0;
+  o->precision = 32;
+  o->max_scenes = 1;
+  o->max_points = 1 << 20;
+  o->profile = 0;
+  o->stream = nullptr;
+}
+
+int amppi_create(const amppi_config* cfg, const amppi_options* opt, amppi_ctx** out) {
+  if (!cfg || !out) return AMPPI_INVALID_ARGUMENT;
+  *out = nullptr;
+  const std::string bad = validate(*cfg);
+  if (!bad.empty()) return AMPPI_INVALID_ARGUMENT;
+  auto* ctx = new (std::nothrow) amppi_ctx();
+  if (!ctx) return AMPPI_CUDA_ERROR;
+  ctx->cfg = *cfg;
+  if (opt)
+    ctx->opt = *opt;
+  else
+    amppi_options_default(&ctx->opt);
+  if (ctx->opt.precision != 32 && ctx->opt.precision != 64) ctx->opt.precision = 32;
+  ctx->S_cap = std::max(1, ctx->opt.max_scenes);
+  ctx->dc = to_dev(*cfg);
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+    delete ctx;
+    return AMPPI_CUDA_ERROR;
+  }
+  const int rc = create_impl(ctx);
+  if (rc != AMPPI_OK) {
+    std::fprintf(stderr, "amppi_create: %s\n", ctx->err.c_str());
+    amppi_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return AMPPI_OK;
+}
+
+int amppi_destroy(amppi_ctx* ctx) {
+  if (!ctx) return AMPPI_OK;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->arena.release();
+  if (ctx->d_xyz) cudaFree(ctx->d_xyz);
+  if (ctx->d_xyz64) cudaFree(ctx->d_xyz64);
+  if (ctx->P.cand) cudaFree(ctx->P.cand);
+  if (ctx->d_injected) cudaFree(ctx->d_injected);
+  if (ctx->h_xyz) cudaFreeHost(ctx->h_xyz);
+  if (ctx->h_in) cudaFreeHost(ctx->h_in);
+  if (ctx->h_res) cudaFreeHost(ctx->h_res);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return AMPPI_OK;
+}
+
+const char* amppi_last_error(const amppi_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int amppi_synchronize(amppi_ctx* ctx) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  return sync_and_collect(ctx);
+}
+
+int amppi_set_stream(amppi_ctx* ctx, void* stream) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->own_stream = false;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return AMPPI_OK;
+}
+
+static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n, const amppi_state* pose,
+                           double r_max) {
+  if (!ctx || (!pts && n > 0) || !pose || n < 0) return ctx ? ctx->fail(AMPPI_INVALID_ARGUMENT, "bad arguments")
+                                                            : AMPPI_INVALID_ARGUMENT;
+  if (!(r_max > 0.0)) return ctx->fail(AMPPI_INVALID_ARGUMENT, "r_max must be positive");
+  if (n > 0xFFFFFFFFll) return ctx->fail(AMPPI_INVALID_ARGUMENT, "at most 2^32-1 points per scene");
+  if (int rc = alloc_points(ctx, n); rc != AMPPI_OK) return rc;
+  const size_t bytes = static_cast<size_t>(n) * 3 * (f64 ? sizeof(double) : sizeof(float));
+  if (n > 0) {
+    std::memcpy(ctx->h_xyz, pts, bytes);
+    CK(cudaMemcpyAsync(f64 ? static_cast<void*>(ctx->d_xyz64) : static_cast<void*>(ctx->d_xyz), ctx->h_xyz, bytes,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  }
+  put_pose(ctx->hin.poses, pose);
+  ctx->hin.offsets[0] = 0;
+  ctx->hin.offsets[1] = n;
+  // upload pose + offsets (the start of the input block)
+  CK(cudaMemcpyAsync(ctx->din.poses, ctx->hin.poses, 10 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->din.offsets, ctx->hin.offsets, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  BatchIn in = batch_from_block(ctx, 1, r_max, f64);
+  if (int rc = run_cycle(ctx, in, n, true, false, false); rc != AMPPI_OK) return rc;
+  ctx->have_snapshot = true;
+  ctx->snap_r_max = r_max;
+  ctx->snap_points = n;
+  std::memcpy(ctx->snap_pose, pose, sizeof(ctx->snap_pose));
+  // cudaMemcpyAsync from pinned staging: the staging buffer is reused by the
+  // next call, so finish the copy before returning.
+  return sync_and_collect(ctx);
+}
+
+int amppi_snapshot(amppi_ctx* ctx, const float* xyz, int64_t n, const amppi_state* pose, double r_max) {
+  return snapshot_common(ctx, xyz, false, n, pose, r_max);
+}
+
+int amppi_snapshot_f64(amppi_ctx* ctx, const double* xyz, int64_t n, const amppi_state* pose, double r_max) {
+  return snapshot_common(ctx, xyz, true, n, pose, r_max);
+}
+
+int amppi_snapshot_download(amppi_ctx* ctx, amppi_snapshot_view* v) {
+  if (!ctx || !v) return AMPPI_INVALID_ARGUMENT;
+  if (!ctx->have_snapshot) return ctx->fail(AMPPI_NO_SNAPSHOT, "no snapshot");
+  const Perception& P = ctx->P;
+  if ((v->ranges || v->has_point || v->nearest) && !P.ranges)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "verification views need max_scenes <= 64");
+  if (v->ranges) CK(cudaMemcpy(v->ranges, P.ranges, kCells * sizeof(double), cudaMemcpyDeviceToHost));
+  if (v->has_point) CK(cudaMemcpy(v->has_point, P.has_point, kCells, cudaMemcpyDeviceToHost));
+  if (v->nearest) CK(cudaMemcpy(v->nearest, P.nearest, kCells * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (v->safe_range) CK(cudaMemcpy(v->safe_range, P.safe_range, kCoarse * sizeof(double), cudaMemcpyDeviceToHost));
+  if (v->safe_dir) CK(cudaMemcpy(v->safe_dir, P.safe_dir, kCoarse * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (v->safe_point) CK(cudaMemcpy(v->safe_point, P.safe_point, kCoarse * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  int32_t nf = 0;
+  CK(cudaMemcpy(&nf, P.n_filtered, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  v->n_filtered = nf;
+  if (v->filtered && nf > 0)
+    CK(cudaMemcpy(v->filtered, P.filtered, static_cast<size_t>(nf) * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  return AMPPI_OK;
+}
+
+int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
+               int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
+               const double* injected, amppi_plan_result* out) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (!x || !goal || !last_applied) return ctx->fail(AMPPI_INVALID_ARGUMENT, "null argument");
+  if (!ctx->have_snapshot) return ctx->fail(AMPPI_NO_SNAPSHOT, "amppi_plan before amppi_snapshot");
+  const DevConfig& dc = ctx->dc;
+  const int M = dc.M, K = dc.K, N = dc.N;
+  InputBlock& h = ctx->hin;
+  put_pose(h.states, x);
+  std::memcpy(h.goals, goal, 10 * sizeof(double));
+  std::memcpy(h.last, last_applied, 4 * sizeof(double));
+  const bool has_prev = previous && previous_len == N;
+  if (has_prev) std::memcpy(h.prev, previous, static_cast<size_t>(N) * 4 * sizeof(double));
+  h.prev_len[0] = has_prev ? N : 0;
+  h.cycles[0] = cycle;
+  h.seeds[0] = seed;
+  // one upload of the whole single-scene input block (poses..prev_len)
+  const size_t span = static_cast<size_t>(reinterpret_cast<unsigned char*>(h.prev_len + 1) -
+                                          reinterpret_cast<unsigned char*>(h.poses));
+  CK(cudaMemcpyAsync(ctx->din.poses, h.poses, span, cudaMemcpyHostToDevice, ctx->stream));
+  BatchIn in = batch_from_block(ctx, 1, ctx->snap_r_max, false);
+  if (injected) {
+    const size_t bytes = static_cast<size_t>(dc.iterations) * M * K * N * 4 * sizeof(double);
+    if (bytes > ctx->injected_bytes) {
+      if (ctx->d_injected) cudaFree(ctx->d_injected);
+      ctx->d_injected = nullptr;
+      CK(cudaMalloc(&ctx->d_injected, bytes));
+      ctx->injected_bytes = bytes;
+    }
+    CK(cudaMemcpyAsync(ctx->d_injected, injected, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    in.injected = ctx->d_injected;
+  }
+  const bool want_states = out && (out->winner_states || out->winner_controls);
+  if (int rc = run_cycle(ctx, in, ctx->snap_points, false, true, want_states); rc != AMPPI_OK) return rc;
+  CK(cudaMemcpyAsync(ctx->h_res, ctx->d_res, ctx->dres.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<float> c32;
+  std::vector<double> c64;
+  if (out && out->sample_costs) {
+    if (ctx->opt.precision == 32) {
+      c32.resize(static_cast<size_t>(M) * K);
+      CK(cudaMemcpyAsync(c32.data(), ctx->pl.cost32, c32.size() * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+      CK(cudaMemcpyAsync(out->sample_costs, ctx->pl.cost64, static_cast<size_t>(M) * K * sizeof(double),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  }
+  if (want_states && out->winner_states)
+    CK(cudaMemcpyAsync(out->winner_states, ctx->pl.winner_states, static_cast<size_t>(N + 1) * 10 * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (want_states && out->winner_controls)
+    CK(cudaMemcpyAsync(out->winner_controls, ctx->pl.winner_controls, static_cast<size_t>(N) * 4 * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (int rc = sync_and_collect(ctx); rc != AMPPI_OK) return rc;
+  const ResultBlock& r = ctx->hres;
+  const int status = r.status[0];
+  if (out) {
+    if (!c32.empty())
+      for (size_t i = 0; i < c32.size(); ++i) out->sample_costs[i] = c32[i];
+    out->winner = r.winner[0];
+    if (status == 0) {
+      out->control.thrust = r.control[0];
+      for (int i = 0; i < 3; ++i) out->control.omega[i] = r.control[1 + i];
+      for (int i = 0; i < 5; ++i) out->breakdown[i] = r.breakdown[static_cast<size_t>(r.winner[0]) * 5 + i];
+    }
+    for (int m = 0; m < M; ++m) {
+      if (out->stage1) out->stage1[m] = r.stage1[m];
+      if (out->stage2) out->stage2[m] = r.stage2[m];
+      if (out->ess) out->ess[m] = r.ess[m];
+      if (out->valid) out->valid[m] = r.valid[m];
+      if (out->nominal)
+        for (int i = 0; i < N * 4; ++i)
+          out->nominal[static_cast<size_t>(m) * N * 4 + i] =
+              r.valid[m] ? r.nominal[static_cast<size_t>(m) * N * 4 + i] : std::numeric_limits<double>::quiet_NaN();
+      for (int a = 0; a < 3; ++a) {
+        if (out->anchor_initial) out->anchor_initial[3 * m + a] = r.anchor_init[3 * m + a];
+        if (out->anchor_refined) out->anchor_refined[3 * m + a] = r.anchor_ref[3 * m + a];
+        if (out->anchor_safe_dir) out->anchor_safe_dir[3 * m + a] = r.anchor_dir[3 * m + a];
+      }
+      if (out->anchor_safe_range) out->anchor_safe_range[m] = r.anchor_range[m];
+      if (out->anchor_ij) {
+        out->anchor_ij[2 * m] = r.anchor_ij[2 * m];
+        out->anchor_ij[2 * m + 1] = r.anchor_ij[2 * m + 1];
+      }
+      if (out->guide_coeffs)
+        for (int i = 0; i < 18; ++i) out->guide_coeffs[18 * m + i] = r.guide_coef[18 * m + i];
+    }
+  }
+  if (status != 0) return ctx->fail(AMPPI_PLANNING_FAILED, "planning failed");
+  return AMPPI_OK;
+}
+
+static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, bool device_out);
+
+int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_output* out) {
+  if (!ctx || !in) return AMPPI_INVALID_ARGUMENT;
+  const int S = in->n_scenes;
+  if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
+  const int N = ctx->dc.N;
+  const int64_t total = in->point_offsets[S];
+  if (int rc = alloc_points(ctx, total); rc != AMPPI_OK) return rc;
+  int64_t max_scene = 0;
+  for (int s = 0; s < S; ++s) max_scene = std::max(max_scene, in->point_offsets[s + 1] - in->point_offsets[s]);
+  // inputs: points straight from the caller's buffer, per-scene arrays via the
+  // pinned block
+  if (total > 0)
+    CK(cudaMemcpyAsync(ctx->d_xyz, in->xyz, static_cast<size_t>(total) * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                       ctx->stream));
+  InputBlock& h = ctx->hin;
+  std::memcpy(h.poses, in->poses, static_cast<size_t>(S) * 10 * sizeof(double));
+  std::memcpy(h.states, in->states, static_cast<size_t>(S) * 10 * sizeof(double));
+  std::memcpy(h.goals, in->goals, static_cast<size_t>(S) * 10 * sizeof(double));
+  std::memcpy(h.last, in->last_applied, static_cast<size_t>(S) * 4 * sizeof(double));
+  if (in->previous) std::memcpy(h.prev, in->previous, static_cast<size_t>(S) * N * 4 * sizeof(double));
+  std::memcpy(h.offsets, in->point_offsets, static_cast<size_t>(S + 1) * sizeof(int64_t));
+  std::memcpy(h.cycles, in->cycles, static_cast<size_t>(S) * sizeof(uint64_t));
+  std::memcpy(h.seeds, in->seeds, static_cast<size_t>(S) * sizeof(uint64_t));
+  for (int s = 0; s < S; ++s) h.prev_len[s] = in->previous ? (in->previous_len ? in->previous_len[s] : N) : 0;
+  const size_t span = static_cast<size_t>(reinterpret_cast<unsigned char*>(h.prev_len + ctx->S_cap) -
+                                          reinterpret_cast<unsigned char*>(h.poses));
+  CK(cudaMemcpyAsync(ctx->din.poses, h.poses, span, cudaMemcpyHostToDevice, ctx->stream));
+  BatchIn bin = batch_from_block(ctx, S, in->r_max, false);
+  if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
+  return batch_outputs_gather(ctx, S, out, false);
+}
+
+int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_output* out) {
+  if (!ctx || !in) return AMPPI_INVALID_ARGUMENT;
+  const int S = in->n_scenes;
+  if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
+  BatchIn bin{};
+  bin.xyz = in->xyz;
+  bin.xyz64 = nullptr;
+  bin.offsets = in->point_offsets;
+  bin.poses = reinterpret_cast<const double*>(in->poses);
+  bin.states = reinterpret_cast<const double*>(in->states);
+  bin.goals = reinterpret_cast<const double*>(in->goals);
+  bin.prev = in->previous;
+  bin.prev_len = in->previous_len;
+  bin.last_applied = reinterpret_cast<const double*>(in->last_applied);
+  bin.cycles = in->cycles;
+  bin.seeds = in->seeds;
+  bin.injected = nullptr;
+  bin.S = S;
+  bin.r_max = in->r_max;
+  // per-scene point counts are device-resident: size the keying grid from the
+  // context's capacity (blocks beyond a scene's end exit immediately)
+  const int64_t max_scene = std::max<int64_t>(1, ctx->P_cap / S);
+  if (ctx->P.cand_cap < ctx->P_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point capacity");
+  if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
+  return batch_outputs_gather(ctx, S, out, true);
+}
+
+int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches, int32_t cap,
+                       int32_t* count) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  int i = 0;
+  for (const auto& kv : ctx->timer.totals) {
+    if (i < cap) {
+      if (names) names[i] = kv.first.c_str();
+      if (ms) ms[i] = kv.second.first;
+      if (launches) launches[i] = kv.second.second;
+    }
+    ++i;
+  }
+  if (count) *count = i;
+  return AMPPI_OK;
+}
+
+int amppi_kernel_times_reset(amppi_ctx* ctx) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  ctx->timer.totals.clear();
+  return AMPPI_OK;
+}
+
+}  // extern "C"
+
+// Gather the per-scene winner outputs on the device; copy them out for the
+// host-pointer API.
+static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, bool device_out) {
+  if (!out) return device_out ? AMPPI_OK : sync_and_collect(ctx);
+  const int M = ctx->dc.M, N = ctx->dc.N;
+  if (device_out) {
+    GatherOut g{out->status, out->winner, out->control, out->winner_nominal, out->stage2, out->breakdown};
+    cudaError_t e = launch_gather(ctx->pl, ctx->dc, S, g, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_gather");
+    return AMPPI_OK;
+  }
+  if (!ctx->d_gather) {
+    const size_t Sc = static_cast<size_t>(ctx->S_cap);
+    const size_t bytes = Sc * (2 * sizeof(int32_t) + (4 + 5 + static_cast<size_t>(N) * 4 + M) * sizeof(double)) + 256;
+    void* p = nullptr;
+    CK(ctx->arena.alloc(&p, bytes));
+    ctx->d_gather = static_cast<unsigned char*>(p);
+  }
+  unsigned char* cur = ctx->d_gather;
+  const size_t Sc = static_cast<size_t>(ctx->S_cap);
+  GatherOut g{};
+  g.status = carve<int32_t>(cur, Sc);
+  g.winner = carve<int32_t>(cur, Sc);
+  g.control = carve<double>(cur, Sc * 4);
+  g.breakdown = carve<double>(cur, Sc * 5);
+  g.winner_nominal = carve<double>(cur, Sc * N * 4);
+  g.stage2 = carve<double>(cur, Sc * M);
+  cudaError_t e = launch_gather(ctx->pl, ctx->dc, S, g, ctx->stream);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_gather");
+  const cudaStream_t st = ctx->stream;
+  if (out->status) CK(cudaMemcpyAsync(out->status, g.status, S * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (out->winner) CK(cudaMemcpyAsync(out->winner, g.winner, S * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (out->control) CK(cudaMemcpyAsync(out->control, g.control, S * 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out->breakdown)
+    CK(cudaMemcpyAsync(out->breakdown, g.breakdown, S * 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out->winner_nominal)
+    CK(cudaMemcpyAsync(out->winner_nominal, g.winner_nominal, static_cast<size_t>(S) * N * 4 * sizeof(double),
+                       cudaMemcpyDeviceToHost, st));
+  if (out->stage2)
+    CK(cudaMemcpyAsync(out->stage2, g.stage2, static_cast<size_t>(S) * M * sizeof(double), cudaMemcpyDeviceToHost, st));
+  return sync_and_collect(ctx);
+}

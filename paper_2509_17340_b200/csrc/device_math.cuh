@@ -1,0 +1,383 @@
+// Device math for the plan-cycle kernels, templated on the arithmetic type.
+//
+// Real = double is compiled in translation units built with -fmad=false and
+// follows the reference's Eigen operation order exactly (SURVEY.md Appendix
+// A.1; the same convention the CPU oracle fixes), so FP64 results differ from
+// the oracle only through libm last-ulp differences (exp/log/sin/cos).
+// Real = float is the throughput path (FMA contraction on, fast forms for the
+// attitude term and quaternion normalisation); it is used for stage-I
+// screening only, never for a returned value.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+#include "layout.h"
+
+namespace amppi_dev {
+
+template <typename R>
+struct V3 {
+  R x, y, z;
+};
+template <typename R>
+struct Q4 {
+  R w, x, y, z;
+};
+
+template <typename R>
+__device__ __forceinline__ V3<R> operator+(V3<R> a, V3<R> b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+template <typename R>
+__device__ __forceinline__ V3<R> operator-(V3<R> a, V3<R> b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+template <typename R>
+__device__ __forceinline__ V3<R> operator*(R s, V3<R> a) { return {s * a.x, s * a.y, s * a.z}; }
+
+template <typename R>
+__device__ __forceinline__ R sqnorm(V3<R> a) { return (a.x * a.x + a.y * a.y) + a.z * a.z; }
+
+template <typename R>
+__device__ __forceinline__ R dsqrt(R x) {
+  if constexpr (std::is_same_v<R, double>) return sqrt(x); else return sqrtf(x);
+}
+
+template <typename R>
+__device__ __forceinline__ R norm3(V3<R> a) { return dsqrt(sqnorm(a)); }
+
+template <typename R>
+__device__ __forceinline__ V3<R> cross(V3<R> a, V3<R> b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+// std::clamp semantics (NaN passes through), ensemble of types.hpp:70-78.
+template <typename R>
+__device__ __forceinline__ R clampv(R v, R lo, R hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+template <typename R>
+__device__ __forceinline__ bool finite3(V3<R> a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+
+template <typename R>
+__device__ __forceinline__ Q4<R> qmul(Q4<R> a, Q4<R> b) {  // Hamilton, left to right
+  return {a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+          a.w * b.y + a.y * b.w + a.z * b.x - a.x * b.z, a.w * b.z + a.z * b.w + a.x * b.y - a.y * b.x};
+}
+
+template <typename R>
+__device__ __forceinline__ R qsqnorm(Q4<R> q) { return ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w; }
+
+// Eigen normalized(): divide by sqrt(squaredNorm) when positive.
+template <typename R>
+__device__ __forceinline__ Q4<R> qnormalized(Q4<R> q) {
+  const R n2 = qsqnorm(q);
+  if constexpr (std::is_same_v<R, double>) {
+    if (!(n2 > 0.0)) return q;
+    const double n = sqrt(n2);
+    return {q.w / n, q.x / n, q.y / n, q.z / n};
+  } else {
+    if (!(n2 > 0.0f)) return q;
+    const float r = rsqrtf(n2);
+    return {q.w * r, q.x * r, q.y * r, q.z * r};
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ bool qfinite(Q4<R> q) {
+  return isfinite(q.w) && isfinite(q.x) && isfinite(q.y) && isfinite(q.z);
+}
+
+// Eigen _transformVector: uv = 2 (q.vec x v); v + w uv + q.vec x uv.
+template <typename R>
+__device__ __forceinline__ V3<R> qrot(Q4<R> q, V3<R> v) {
+  const V3<R> qv{q.x, q.y, q.z};
+  V3<R> uv = cross(qv, v);
+  uv = uv + uv;
+  return (v + q.w * uv) + cross(qv, uv);
+}
+
+// Third column of R(q) for a unit q == q * e_z; FP32 shortcut only.
+__device__ __forceinline__ V3<float> qrot_ez_fast(Q4<float> q) {
+  return {2.f * (q.w * q.y + q.x * q.z), 2.f * (q.y * q.z - q.w * q.x), 1.f - 2.f * (q.x * q.x + q.y * q.y)};
+}
+
+struct M3 {
+  double m[3][3];
+};
+
+// Eigen QuaternionBase::toRotationMatrix.
+__device__ __forceinline__ M3 rotmat(Q4<double> q) {
+  const double tx = 2.0 * q.x, ty = 2.0 * q.y, tz = 2.0 * q.z;
+  const double twx = tx * q.w, twy = ty * q.w, twz = tz * q.w;
+  const double txx = tx * q.x, txy = ty * q.x, txz = tz * q.x;
+  const double tyy = ty * q.y, tyz = tz * q.y, tzz = tz * q.z;
+  M3 r;
+  r.m[0][0] = 1.0 - (tyy + tzz);
+  r.m[0][1] = txy - twz;
+  r.m[0][2] = txz + twy;
+  r.m[1][0] = txy + twz;
+  r.m[1][1] = 1.0 - (txx + tzz);
+  r.m[1][2] = tyz - twx;
+  r.m[2][0] = txz - twy;
+  r.m[2][1] = tyz + twx;
+  r.m[2][2] = 1.0 - (txx + tyy);
+  return r;
+}
+
+__device__ __forceinline__ V3<double> mat_vec(const M3& a, V3<double> v) {
+  return {(a.m[0][0] * v.x + a.m[0][1] * v.y) + a.m[0][2] * v.z,
+          (a.m[1][0] * v.x + a.m[1][1] * v.y) + a.m[1][2] * v.z,
+          (a.m[2][0] * v.x + a.m[2][1] * v.y) + a.m[2][2] * v.z};
+}
+
+__device__ __forceinline__ V3<double> mat_t_vec(const M3& a, V3<double> v) {  // a^T v
+  return {(a.m[0][0] * v.x + a.m[1][0] * v.y) + a.m[2][0] * v.z,
+          (a.m[0][1] * v.x + a.m[1][1] * v.y) + a.m[2][1] * v.z,
+          (a.m[0][2] * v.x + a.m[1][2] * v.y) + a.m[2][2] * v.z};
+}
+
+// ||R(q) G^T - I||_F with the oracle's column-major summation (costs.hpp:100-104).
+// gt = R(q_goal)^T.
+__device__ __forceinline__ double attitude_err_exact(Q4<double> q, const M3& gt) {
+  const M3 r = rotmat(q);
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double e = (r.m[i][0] * gt.m[0][j] + r.m[i][1] * gt.m[1][j]) + r.m[i][2] * gt.m[2][j];
+      e = e - (i == j ? 1.0 : 0.0);
+      s = s + e * e;
+    }
+  return sqrt(s);
+}
+
+// Closed form for unit quaternions: ||R(q)R(g)^T - I||_F = 2 sqrt(2) |vec(q (x) g*)|.
+__device__ __forceinline__ float attitude_err_fast(Q4<float> q, Q4<float> g) {
+  const float ex = g.w * q.x - q.w * g.x - (q.y * g.z - q.z * g.y);
+  const float ey = g.w * q.y - q.w * g.y - (q.z * g.x - q.x * g.z);
+  const float ez = g.w * q.z - q.w * g.z - (q.x * g.y - q.y * g.x);
+  return 2.8284271247461903f * sqrtf(ex * ex + ey * ey + ez * ez);
+}
+
+// ---------------------------------------------------------------------------
+// SplitMix64 counter RNG (rng.hpp:10-66)
+// ---------------------------------------------------------------------------
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// RandomStream::derive(seed, a, b, c) followed by the constructor's mix.
+__device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t k = mix64(seed + kGamma);
+  k = mix64(k ^ (a + kGamma));
+  k = mix64(k ^ (b + kGamma));
+  k = mix64(k ^ (c + kGamma));
+  return mix64(k ^ kGamma);
+}
+
+// Normal pair p of the stream (normals 2p -> cos, 2p+1 -> sin) drawn from
+// counters 2p+1 (u1 = 1 - U) and 2p+2 (u2), Box-Muller as rng.hpp:43-55.
+__device__ __forceinline__ void normal_pair(uint64_t key, uint32_t p, double& n0, double& n1) {
+  const uint64_t a = mix64(key + (2ull * p + 1ull) * kGamma);
+  const uint64_t b = mix64(key + (2ull * p + 2ull) * kGamma);
+  const double u1 = 1.0 - static_cast<double>(a >> 11) * 0x1.0p-53;
+  const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;
+  const double r = sqrt(-2.0 * log(u1));
+  const double ang = 6.283185307179586 * u2;  // (2.0 * pi) * u2, 2.0*pi exact
+  double s, c;
+  sincos(ang, &s, &c);
+  n0 = r * c;
+  n1 = r * s;
+}
+
+// FP32 screening draw: same integers, float arithmetic with full-range tails
+// (1 - U kept exact via the integer complement; small U via log1p).
+__device__ __forceinline__ void normal_pair_f(uint64_t key, uint32_t p, float& n0, float& n1) {
+  const uint64_t a = mix64(key + (2ull * p + 1ull) * kGamma);
+  const uint64_t b = mix64(key + (2ull * p + 2ull) * kGamma);
+  const uint64_t ma = a >> 11;
+  float lg;
+  if (ma < (1ull << 52)) {  // U < 0.5: log(1-U) = log1p(-U)
+    lg = log1pf(-static_cast<float>(ma) * 0x1.0p-53f);
+  } else {
+    lg = logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
+  }
+  const float r = sqrtf(-2.0f * lg);
+  const float u2x2 = static_cast<float>(b >> 11) * 0x1.0p-52f;  // 2*u2
+  float s, c;
+  sincospif(u2x2, &s, &c);
+  n0 = r * c;
+  n1 = r * s;
+}
+
+// ---------------------------------------------------------------------------
+// dynamics (dynamics.hpp:13-78)
+// ---------------------------------------------------------------------------
+template <typename R>
+struct Dyn {
+  R mass, inv_mass, gx, gy, gz, dt, half_dt, dt6;
+  R tmin, tmax, wxy, wz;
+};
+
+template <typename R>
+__device__ __forceinline__ Dyn<R> make_dyn(const DevConfig& c) {
+  Dyn<R> d;
+  d.mass = static_cast<R>(c.mass);
+  d.inv_mass = static_cast<R>(1.0 / c.mass);
+  d.gx = static_cast<R>(c.gravity[0]);
+  d.gy = static_cast<R>(c.gravity[1]);
+  d.gz = static_cast<R>(c.gravity[2]);
+  d.dt = static_cast<R>(c.dyn_dt);
+  d.half_dt = static_cast<R>(0.5 * c.dyn_dt);
+  d.dt6 = static_cast<R>(c.dyn_dt / 6.0);
+  d.tmin = static_cast<R>(c.thrust_min);
+  d.tmax = static_cast<R>(c.thrust_max);
+  d.wxy = static_cast<R>(c.omega_xy_max);
+  d.wz = static_cast<R>(c.omega_z_max);
+  return d;
+}
+
+template <typename R>
+struct St {
+  V3<R> p;
+  Q4<R> q;
+  V3<R> v;
+};
+
+template <typename R>
+struct Deriv {
+  V3<R> dp;
+  Q4<R> dq;
+  V3<R> dv;
+};
+
+template <typename R>
+__device__ __forceinline__ Deriv<R> derivative(const St<R>& x, R thrust, V3<R> om, const Dyn<R>& d) {
+  Deriv<R> k;
+  k.dp = x.v;
+  const Q4<R> qd = qmul(x.q, Q4<R>{R(0), om.x, om.y, om.z});
+  k.dq = {R(0.5) * qd.w, R(0.5) * qd.x, R(0.5) * qd.y, R(0.5) * qd.z};
+  if constexpr (std::is_same_v<R, double>) {
+    const V3<double> dir = qrot(qnormalized(x.q), V3<double>{0.0, 0.0, 1.0});
+    const double a = thrust / d.mass;
+    k.dv = V3<double>{a * dir.x, a * dir.y, a * dir.z} + V3<double>{d.gx, d.gy, d.gz};
+  } else {
+    const V3<float> dir = qrot_ez_fast(qnormalized(x.q));
+    const float a = thrust * d.inv_mass;
+    k.dv = {a * dir.x + d.gx, a * dir.y + d.gy, a * dir.z + d.gz};
+  }
+  return k;
+}
+
+template <typename R>
+__device__ __forceinline__ St<R> advance(const St<R>& s, const Deriv<R>& k, R h) {
+  St<R> o;
+  o.p = s.p + h * k.dp;
+  o.v = s.v + h * k.dv;
+  o.q = {s.q.w + h * k.dq.w, s.q.x + h * k.dq.x, s.q.y + h * k.dq.y, s.q.z + h * k.dq.z};
+  return o;
+}
+
+template <typename R>
+__device__ __forceinline__ R rk_comb(R a, R b, R c, R e) { return ((a + R(2) * b) + R(2) * c) + e; }
+
+// rk4_step_raw followed by q.normalize() (mppi.cpp:48-49).
+template <typename R>
+__device__ __forceinline__ St<R> rk4_normalized(const St<R>& x, R thrust, V3<R> om, const Dyn<R>& d) {
+  const Deriv<R> k1 = derivative(x, thrust, om, d);
+  const Deriv<R> k2 = derivative(advance(x, k1, d.half_dt), thrust, om, d);
+  const Deriv<R> k3 = derivative(advance(x, k2, d.half_dt), thrust, om, d);
+  const Deriv<R> k4 = derivative(advance(x, k3, d.dt), thrust, om, d);
+  const R h6 = d.dt6;
+  St<R> n;
+  n.p = {x.p.x + h6 * rk_comb(k1.dp.x, k2.dp.x, k3.dp.x, k4.dp.x),
+         x.p.y + h6 * rk_comb(k1.dp.y, k2.dp.y, k3.dp.y, k4.dp.y),
+         x.p.z + h6 * rk_comb(k1.dp.z, k2.dp.z, k3.dp.z, k4.dp.z)};
+  n.v = {x.v.x + h6 * rk_comb(k1.dv.x, k2.dv.x, k3.dv.x, k4.dv.x),
+         x.v.y + h6 * rk_comb(k1.dv.y, k2.dv.y, k3.dv.y, k4.dv.y),
+         x.v.z + h6 * rk_comb(k1.dv.z, k2.dv.z, k3.dv.z, k4.dv.z)};
+  n.q = {x.q.w + h6 * rk_comb(k1.dq.w, k2.dq.w, k3.dq.w, k4.dq.w),
+         x.q.x + h6 * rk_comb(k1.dq.x, k2.dq.x, k3.dq.x, k4.dq.x),
+         x.q.y + h6 * rk_comb(k1.dq.y, k2.dq.y, k3.dq.y, k4.dq.y),
+         x.q.z + h6 * rk_comb(k1.dq.z, k2.dq.z, k3.dq.z, k4.dq.z)};
+  n.q = qnormalized(n.q);
+  return n;
+}
+
+template <typename R>
+__device__ __forceinline__ bool state_finite(const St<R>& s) {
+  return finite3(s.p) && finite3(s.v) && qfinite(s.q);
+}
+
+// ---------------------------------------------------------------------------
+// collision (costs.hpp:113-118, perception.cpp:191-235)
+// ---------------------------------------------------------------------------
+template <typename R>
+__device__ __forceinline__ R collision_term(R d, R scale, R slope, R dmin, R dmax) {
+  if (d < dmin) return scale;
+  if (d < dmax) {
+    if constexpr (std::is_same_v<R, double>) return scale * exp(-slope * (d - dmin));
+    else return scale * __expf(-slope * (d - dmin));
+  }
+  return R(0);
+}
+
+// Squared distance to the nearest filtered point among the 27 grid cells
+// around p; returns +inf when none.  Exact whenever the true nearest distance
+// is below the grid cell size h >= d_max.
+__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint32_t* __restrict__ start,
+                                                   const double* __restrict__ pts, V3<double> p) {
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  if (g.dims[0] == 0) return best;
+  const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
+  const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
+  const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
+  const int x0 = max(cx - 1, 0), x1 = min(cx + 1, g.dims[0] - 1);
+  const int y0 = max(cy - 1, 0), y1 = min(cy + 1, g.dims[1] - 1);
+  const int z0 = max(cz - 1, 0), z1 = min(cz + 1, g.dims[2] - 1);
+  for (int x = x0; x <= x1; ++x)
+    for (int y = y0; y <= y1; ++y) {
+      const int row = (x * g.dims[1] + y) * g.dims[2];
+      const uint32_t b = start[row + z0], e = start[row + z1 + 1];
+      for (uint32_t k = b; k < e; ++k) {
+        const V3<double> q{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]};
+        const double d2 = sqnorm(p - q);
+        best = d2 < best ? d2 : best;
+      }
+    }
+  return best;
+}
+
+__device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint32_t* __restrict__ start,
+                                                 const uint32_t* __restrict__ occ, const float4* __restrict__ pts,
+                                                 V3<float> p) {
+  float best = __int_as_float(0x7f800000);
+  if (g.dims[0] == 0) return best;
+  const float fx = (p.x - g.origin_f[0]) * g.inv_h_f;
+  const float fy = (p.y - g.origin_f[1]) * g.inv_h_f;
+  const float fz = (p.z - g.origin_f[2]) * g.inv_h_f;
+  const int cx = __float2int_rd(fx), cy = __float2int_rd(fy), cz = __float2int_rd(fz);
+  if (cx < -1 || cy < -1 || cz < -1 || cx > g.dims[0] || cy > g.dims[1] || cz > g.dims[2]) return best;
+  // dilated occupancy (cells -1..dims padded by one): skip empty neighbourhoods
+  const int ox = cx + 1, oy = cy + 1, oz = cz + 1;
+  const int oc = (ox * (g.dims[1] + 2) + oy) * (g.dims[2] + 2) + oz;
+  if (!((__ldg(occ + (oc >> 5)) >> (oc & 31)) & 1u)) return best;
+  const int x0 = max(cx - 1, 0), x1 = min(cx + 1, g.dims[0] - 1);
+  const int y0 = max(cy - 1, 0), y1 = min(cy + 1, g.dims[1] - 1);
+  const int z0 = max(cz - 1, 0), z1 = min(cz + 1, g.dims[2] - 1);
+  for (int x = x0; x <= x1; ++x)
+    for (int y = y0; y <= y1; ++y) {
+      const int row = (x * g.dims[1] + y) * g.dims[2];
+      const uint32_t b = __ldg(start + row + z0), e = __ldg(start + row + z1 + 1);
+      for (uint32_t k = b; k < e; ++k) {
+        const float4 q = __ldg(pts + k);
+        const float dx = p.x - q.x, dy = p.y - q.y, dz = p.z - q.z;
+        best = fminf(best, dx * dx + dy * dy + dz * dz);
+      }
+    }
+  return best;
+}
+
+}  // namespace amppi_dev

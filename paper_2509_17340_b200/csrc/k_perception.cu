@@ -1,0 +1,406 @@
+// Snapshot kernels: LiDAR ingest + 3°/18° multi-resolution partition +
+// filtered cloud + collision grid.  Replaces build_snapshot
+// (proj/src/perception.cpp:237-246) and everything under it.
+//
+// Built with -fmad=false: every FP64 value that feeds an integer decision
+// (cell keys, per-cell argmin, pooled argmax) is computed with the oracle's
+// operation order and IEEE rounding, so keys and ranges are bit-exact.
+//
+//   K1 k_key_points      one thread per point: world->body (FP64), range,
+//                        (i, j) cell key, 64-bit atomicMin of the range bits
+//                        per cell + candidate log for the (r, index) tie-break
+//   K1b k_resolve_ties   candidates whose range equals the cell minimum take
+//                        atomicMin of their point index (lexicographic
+//                        (r, idx) minimum == "strict <, first point wins",
+//                        perception.cpp:80-86)
+//   K2 k_finalize_scene  one CTA per scene: ranges/has_point, 6x6 argmax
+//                        pooling, flat-order compaction + world transform,
+//                        collision grid (counting sort) + dilated occupancy
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "cr_math.cuh"
+#include "device_math.cuh"
+#include "kernels.h"
+
+namespace amppi_dev {
+
+namespace {
+
+constexpr double kPiD = 0x1.921fb54442d18p+1;      // std::numbers::pi
+constexpr double kHalfPi = 0x1.921fb54442d18p+0;   // 0.5 * pi
+constexpr double kAzStep = 0x1.acee9f37bebd5p-5;   // 2*pi/120 == pi/60
+constexpr double kElStep = 0x1.acee9f37bebd5p-5;
+constexpr double kGuard = 1e-9;  // cells; CUDA atan2 error is < 1e-13 cells
+
+__device__ __forceinline__ bool near_integer(double v) {
+  const double fl = floor(v);
+  return (v - fl) < kGuard || ((fl + 1.0) - v) < kGuard;
+}
+
+}  // namespace
+
+// azimuth_cell(atan2(y, x)) (perception.cpp:17-21) with glibc-equal keys.
+__device__ int az_cell_of(double y, double x) {
+  double az = atan2(y, x);
+  double v = (az + kPiD) / kAzStep;
+  if (near_integer(v)) {
+    az = crm::atan2_cr(y, x);
+    v = (az + kPiD) / kAzStep;
+  }
+  int i = static_cast<int>(floor(v));
+  if (i >= kAz) i -= kAz;
+  return i < 0 ? 0 : (i > kAz - 1 ? kAz - 1 : i);
+}
+
+// elevation_cell(atan2(z, rho)) (perception.cpp:23-26).
+__device__ int el_cell_of(double z, double rho) {
+  double el = atan2(z, rho);
+  double v = (el + kHalfPi) / kElStep;
+  if (near_integer(v)) {
+    el = crm::atan2_cr(z, rho);
+    v = (el + kHalfPi) / kElStep;
+  }
+  const int j = static_cast<int>(floor(v));
+  return j < 0 ? 0 : (j > kEl - 1 ? kEl - 1 : j);
+}
+
+namespace {
+
+struct PoseFrame {
+  V3<double> p;
+  M3 r;  // body -> world
+};
+
+__device__ __forceinline__ PoseFrame load_pose(const double* s10) {
+  PoseFrame f;
+  f.p = {s10[0], s10[1], s10[2]};
+  f.r = rotmat(Q4<double>{s10[3], s10[4], s10[5], s10[6]});
+  return f;
+}
+
+__device__ __forceinline__ V3<double> load_point(const BatchIn& in, int64_t g) {
+  if (in.xyz64) return {in.xyz64[3 * g], in.xyz64[3 * g + 1], in.xyz64[3 * g + 2]};
+  return {static_cast<double>(in.xyz[3 * g]), static_cast<double>(in.xyz[3 * g + 1]),
+          static_cast<double>(in.xyz[3 * g + 2])};
+}
+
+// PointCloudBuffer::body_points: R^T (p - pose.p) (perception.cpp:58-61).
+__device__ __forceinline__ V3<double> to_body(const PoseFrame& f, V3<double> w) {
+  return mat_t_vec(f.r, w - f.p);
+}
+
+__global__ void __launch_bounds__(256) k_key_points(BatchIn in, Perception P) {
+  const int s = blockIdx.y;
+  __shared__ PoseFrame pose;
+  if (threadIdx.x == 0) pose = load_pose(in.poses + 10 * s);
+  __syncthreads();
+  const int64_t b = in.offsets[s], e = in.offsets[s + 1];
+  const double r_max = in.r_max;
+  uint64_t* __restrict__ cell_r = P.cell_r + static_cast<int64_t>(s) * kCells;
+  for (int64_t g = b + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < e;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const V3<double> p = to_body(pose, load_point(in, g));
+    const double r = sqrt(sqnorm(p));
+    if (!(r > kMinPointRange) || r > r_max) continue;  // perception.cpp:74
+    const int i = az_cell_of(p.y, p.x);
+    const int j = el_cell_of(p.z, sqrt(p.x * p.x + p.y * p.y));
+    const int f = i * kEl + j;
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(r));
+    const uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(cell_r + f), bits);
+    if (old >= bits) {  // may be the cell minimum: log for the index tie-break
+      const unsigned long long slot = atomicAdd(P.cand_count, 1ull);
+      if (slot < static_cast<unsigned long long>(P.cand_cap))
+        P.cand[slot] = Candidate{static_cast<uint32_t>(s * kCells + f), static_cast<uint32_t>(g - b), bits};
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
+  const unsigned long long n = *P.cand_count;
+  for (unsigned long long c = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+       c += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const Candidate cd = P.cand[c];
+    if (P.cell_r[cd.cell] == cd.bits) atomicMin(P.cell_idx + cd.cell, cd.idx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2
+// ---------------------------------------------------------------------------
+constexpr int kFinalizeThreads = 512;
+constexpr int kChunk = (kCells + kFinalizeThreads - 1) / kFinalizeThreads;  // 15
+
+struct FinalizeSmem {
+  double rng[kCells];
+  uint32_t idx[kCells];
+  uint32_t counts[kGridCells + 1];
+  uint32_t occ[kOccWords];
+  uint32_t warp_sums[kFinalizeThreads / 32];
+  double bbox_lo[kFinalizeThreads / 32][3];
+  double bbox_hi[kFinalizeThreads / 32][3];
+  GridMeta meta;
+  PoseFrame pose;
+  uint32_t total;
+};
+
+// Block-wide exclusive scan of one value per thread; returns the prefix and
+// writes the total to *total (all threads see it after the call).
+__device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t w = lane < nw ? warp_sums[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_sums[lane] = w;  // inclusive
+    if (lane == nw - 1) *total = w;
+  }
+  __syncthreads();
+  const uint32_t base = warp > 0 ? warp_sums[warp - 1] : 0u;
+  const uint32_t out = base + x - v;
+  __syncthreads();
+  return out;
+}
+
+__global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x;
+  const double r_max = in.r_max;
+  const int64_t cell_base = static_cast<int64_t>(s) * kCells;
+  const int64_t pt_base = in.offsets[s];
+  if (tid == 0) sm.pose = load_pose(in.poses + 10 * s);
+
+  // 1. per-cell range / argmin; reset the atomics tables for the next cycle
+  for (int f = tid; f < kCells; f += blockDim.x) {
+    const uint64_t bits = P.cell_r[cell_base + f];
+    const bool has = bits != kEmptyCell;
+    sm.rng[f] = has ? __longlong_as_double(static_cast<long long>(bits)) : r_max;
+    sm.idx[f] = has ? P.cell_idx[cell_base + f] : 0xFFFFFFFFu;
+    P.cell_r[cell_base + f] = kEmptyCell;
+    P.cell_idx[cell_base + f] = 0xFFFFFFFFu;
+    if (P.ranges) P.ranges[cell_base + f] = sm.rng[f];
+    if (P.has_point) P.has_point[cell_base + f] = has ? 1 : 0;
+  }
+  for (int w = tid; w < kOccWords; w += blockDim.x) sm.occ[w] = 0u;
+  __syncthreads();
+
+  // 2. 6x6 argmax pooling, i outer / j inner, strict > (perception.cpp:99-121)
+  if (tid < kCoarse) {
+    const int I = tid / kCEl, J = tid % kCEl;
+    int bi = I * kPool, bj = J * kPool;
+    double best = -1.0;
+    for (int i = I * kPool; i < (I + 1) * kPool; ++i)
+      for (int j = J * kPool; j < (J + 1) * kPool; ++j) {
+        const double r = sm.rng[i * kEl + j];
+        if (r > best) {
+          best = r;
+          bi = i;
+          bj = j;
+        }
+      }
+    const int c = bi * kEl + bj;
+    const double dx = P.cell_dir[3 * c], dy = P.cell_dir[3 * c + 1], dz = P.cell_dir[3 * c + 2];
+    const int64_t o = static_cast<int64_t>(s) * kCoarse + tid;
+    P.safe_range[o] = best;
+    P.safe_dir[3 * o] = dx;
+    P.safe_dir[3 * o + 1] = dy;
+    P.safe_dir[3 * o + 2] = dz;
+    P.safe_point[3 * o] = best * dx;
+    P.safe_point[3 * o + 1] = best * dy;
+    P.safe_point[3 * o + 2] = best * dz;
+  }
+
+  // 3. filtered cloud in flat order (perception.cpp:124-144): compaction
+  const int f0 = tid * kChunk;
+  const int f1 = min(f0 + kChunk, kCells);
+  uint32_t mine = 0;
+  for (int f = f0; f < f1; ++f) mine += sm.idx[f] != 0xFFFFFFFFu;
+  const uint32_t pos0 = block_exclusive_scan(mine, sm.warp_sums, &sm.total);
+  const uint32_t n_pts = sm.total;
+  double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+  double* __restrict__ filt = P.filtered + cell_base * 3;
+  uint32_t pos = pos0;
+  for (int f = f0; f < f1; ++f) {
+    const uint32_t k = sm.idx[f];
+    if (k == 0xFFFFFFFFu) {
+      if (P.nearest) {
+        P.nearest[(cell_base + f) * 3] = 0.0;
+        P.nearest[(cell_base + f) * 3 + 1] = 0.0;
+        P.nearest[(cell_base + f) * 3 + 2] = 0.0;
+      }
+      continue;
+    }
+    const V3<double> pb = to_body(sm.pose, load_point(in, pt_base + k));
+    const V3<double> pw = sm.pose.p + mat_vec(sm.pose.r, pb);  // to_world_frame
+    if (P.nearest) {
+      P.nearest[(cell_base + f) * 3] = pb.x;
+      P.nearest[(cell_base + f) * 3 + 1] = pb.y;
+      P.nearest[(cell_base + f) * 3 + 2] = pb.z;
+    }
+    filt[3 * pos] = pw.x;
+    filt[3 * pos + 1] = pw.y;
+    filt[3 * pos + 2] = pw.z;
+    lo[0] = fmin(lo[0], pw.x); lo[1] = fmin(lo[1], pw.y); lo[2] = fmin(lo[2], pw.z);
+    hi[0] = fmax(hi[0], pw.x); hi[1] = fmax(hi[1], pw.y); hi[2] = fmax(hi[2], pw.z);
+    ++pos;
+  }
+  // bbox reduction
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if (lane == 0) {
+      sm.bbox_lo[warp][a] = lo[a];
+      sm.bbox_hi[warp][a] = hi[a];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    GridMeta m{};
+    m.n_points = static_cast<int>(n_pts);
+    if (n_pts > 0) {
+      double L[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, H[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+        for (int a = 0; a < 3; ++a) {
+          L[a] = fmin(L[a], sm.bbox_lo[w][a]);
+          H[a] = fmax(H[a], sm.bbox_hi[w][a]);
+        }
+      const double ext = fmax(fmax(H[0] - L[0], H[1] - L[1]), H[2] - L[2]);
+      // cell >= d_max (with margin) so the 27-cell neighbourhood contains every
+      // point closer than d_max; at most kGridAxis cells per axis
+      double h = cfg.col_d_max * (1.0 + 1e-3) + 1e-6;
+      const double h_cap = ext / (kGridAxis - 1) * (1.0 + 1e-9);
+      if (h_cap > h) h = h_cap;
+      m.h = h;
+      m.inv_h = 1.0 / h;
+      for (int a = 0; a < 3; ++a) {
+        m.origin[a] = L[a];
+        m.origin_f[a] = static_cast<float>(L[a]);
+        int d = static_cast<int>(floor((H[a] - L[a]) * m.inv_h)) + 1;
+        m.dims[a] = d < 1 ? 1 : (d > kGridAxis ? kGridAxis : d);
+      }
+      m.inv_h_f = static_cast<float>(m.inv_h);
+    }
+    sm.meta = m;
+    P.grid[s] = m;
+    P.n_filtered[s] = static_cast<int32_t>(n_pts);
+  }
+  __syncthreads();
+  const GridMeta meta = sm.meta;
+  const int ncell = meta.dims[0] * meta.dims[1] * meta.dims[2];
+  uint32_t* __restrict__ gstart = P.grid_start + static_cast<int64_t>(s) * (kGridCells + 1);
+  uint32_t* __restrict__ gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
+  if (n_pts == 0) {
+    for (int w = tid; w < kOccWords; w += blockDim.x) gocc[w] = 0u;
+    if (tid == 0) gstart[0] = 0u;
+    return;
+  }
+
+  // 4. counting sort into the grid
+  for (int c = tid; c <= ncell; c += blockDim.x) sm.counts[c] = 0u;
+  __syncthreads();
+  auto cell_of = [&](const V3<double>& p, int* c3) {
+    const double rel[3] = {p.x - meta.origin[0], p.y - meta.origin[1], p.z - meta.origin[2]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int c = static_cast<int>(floor(rel[a] * meta.inv_h));
+      c3[a] = c < 0 ? 0 : (c > meta.dims[a] - 1 ? meta.dims[a] - 1 : c);
+    }
+    return (c3[0] * meta.dims[1] + c3[1]) * meta.dims[2] + c3[2];
+  };
+  for (uint32_t k = pos0; k < pos; ++k) {
+    const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
+    int c3[3];
+    const int c = cell_of(pw, c3);
+    atomicAdd(&sm.counts[c], 1u);
+    // dilated occupancy over the padded (dims+2)^3 lattice
+    const int py = meta.dims[1] + 2, pz = meta.dims[2] + 2;
+    for (int dx = 0; dx < 3; ++dx)
+      for (int dy = 0; dy < 3; ++dy)
+        for (int dz = 0; dz < 3; ++dz) {
+          const int oc = ((c3[0] + dx) * py + (c3[1] + dy)) * pz + (c3[2] + dz);
+          atomicOr(&sm.occ[oc >> 5], 1u << (oc & 31));
+        }
+  }
+  __syncthreads();
+  // exclusive scan of counts (each thread a contiguous chunk of cells)
+  const int cchunk = (ncell + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(tid * cchunk, ncell), c1 = min(c0 + cchunk, ncell);
+  uint32_t local = 0;
+  for (int c = c0; c < c1; ++c) local += sm.counts[c];
+  uint32_t run = block_exclusive_scan(local, sm.warp_sums, &sm.total);
+  for (int c = c0; c < c1; ++c) {
+    const uint32_t cnt = sm.counts[c];
+    gstart[c] = run;
+    sm.counts[c] = run;  // becomes the scatter cursor
+    run += cnt;
+  }
+  if (tid == 0) gstart[ncell] = n_pts;
+  for (int w = tid; w < kOccWords; w += blockDim.x) gocc[w] = sm.occ[w];
+  __syncthreads();
+  double* __restrict__ gp64 = P.grid_pts64 + cell_base * 3;
+  float4* __restrict__ gp32 = P.grid_pts32 + cell_base;
+  for (uint32_t k = pos0; k < pos; ++k) {
+    const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
+    int c3[3];
+    const int c = cell_of(pw, c3);
+    const uint32_t slot = atomicAdd(&sm.counts[c], 1u);
+    gp64[3 * slot] = pw.x;
+    gp64[3 * slot + 1] = pw.y;
+    gp64[3 * slot + 2] = pw.z;
+    gp32[slot] = make_float4(static_cast<float>(pw.x), static_cast<float>(pw.y), static_cast<float>(pw.z), 0.f);
+  }
+}
+
+}  // namespace
+
+size_t finalize_smem_bytes() { return sizeof(FinalizeSmem); }
+
+cudaError_t init_kernel_attributes() {
+  return cudaFuncSetAttribute(k_finalize_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(sizeof(FinalizeSmem)));
+}
+
+cudaError_t launch_snapshot(const BatchIn& in, const Perception& P, const DevConfig& cfg, int64_t max_points_per_scene,
+                            cudaStream_t st, KernelTimer* timer) {
+  cudaError_t err = cudaMemsetAsync(P.cand_count, 0, sizeof(unsigned long long), st);
+  if (err != cudaSuccess) return err;
+  const int threads = 256;
+  int64_t blocks_x = (max_points_per_scene + threads - 1) / threads;
+  if (blocks_x < 1) blocks_x = 1;
+  if (blocks_x > 4096) blocks_x = 4096;
+  {
+    TimedRegion t(timer, "k_key_points", st);
+    k_key_points<<<dim3(static_cast<unsigned>(blocks_x), in.S), threads, 0, st>>>(in, P);
+  }
+  {
+    TimedRegion t(timer, "k_resolve_ties", st);
+    k_resolve_ties<<<148 * 4, 256, 0, st>>>(P);
+  }
+  {
+    TimedRegion t(timer, "k_finalize_scene", st);
+    k_finalize_scene<<<in.S, kFinalizeThreads, sizeof(FinalizeSmem), st>>>(in, P, cfg);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace amppi_dev

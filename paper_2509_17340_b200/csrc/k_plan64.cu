@@ -1,0 +1,580 @@
+// Plan kernels in FP64 (built with -fmad=false): anchors + guides, the FP64
+// stage-I rollouts (precision 64), the per-instance MPPI update with exact
+// softmin support, stage II and the per-scene winner selection.  Replaces
+// plan_step (proj/src/ensemble.cpp:29-169) end to end together with the FP32
+// screening kernel in k_plan32.cu.
+//
+//   K4  k_anchors       one thread per (scene, anchor): near-goal logic
+//                       (ensemble.cpp:42-66), sample_initial_endpoints /
+//                       refine_endpoints (guidance.cpp:16-72) with
+//                       correctly-rounded atan2/sin/cos, quintic guide
+//                       (guidance.cpp:74-140), guide table g(t*dt), warm
+//                       start (ensemble.cpp:68-77)
+//   K3d k_stage1_f64    one thread per (scene, anchor, sample), FP64 stage I
+//   K4b k_update        one CTA per (scene, anchor): min / softmin support,
+//                       FP64 re-evaluation of the support (after FP32
+//                       screening), weights, weighted perturbation sum and
+//                       clamp (mppi.cpp:70-101), stage-II re-rollout
+//                       (ensemble.cpp:132-149); the last CTA of a scene picks
+//                       the winner (ensemble.cpp:151-168)
+#include <cuda_runtime.h>
+
+#include "cr_math.cuh"
+#include "kernels.h"
+#include "rollout.cuh"
+
+namespace amppi_dev {
+
+namespace {
+
+constexpr double kPiD = 0x1.921fb54442d18p+1;
+constexpr double kHalfPi = 0x1.921fb54442d18p+0;
+constexpr double kAzStep = 0x1.acee9f37bebd5p-5;
+constexpr double kMaxElevation = 0x1.8da7e39bae2a4p+0;  // 89*pi/180
+
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
+
+__device__ __forceinline__ St<double> load_state(const double* s) {
+  St<double> x;
+  x.p = {s[0], s[1], s[2]};
+  x.q = {s[3], s[4], s[5], s[6]};
+  x.v = {s[7], s[8], s[9]};
+  return x;
+}
+
+// cell of an exactly computed angle (atan2 already correctly rounded)
+__device__ __forceinline__ int az_cell_exact(double az) {
+  int i = static_cast<int>(floor((az + kPiD) / kAzStep));
+  if (i >= kAz) i -= kAz;
+  return i < 0 ? 0 : (i > kAz - 1 ? kAz - 1 : i);
+}
+__device__ __forceinline__ int el_cell_exact(double el) {
+  const int j = static_cast<int>(floor((el + kHalfPi) / kAzStep));
+  return j < 0 ? 0 : (j > kEl - 1 ? kEl - 1 : j);
+}
+
+__device__ __forceinline__ V3<double> direction_from_angles(double az, double el) {
+  const double ce = crm::cos_cr(el);
+  return {ce * crm::cos_cr(az), ce * crm::sin_cr(az), crm::sin_cr(el)};
+}
+
+// ---------------------------------------------------------------------------
+// K4: anchors, guides, warm start
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int M = cfg.M, N = cfg.N;
+  if (gid >= in.S * M) return;
+  const int s = gid / M, m = gid % M;
+  const St<double> x = load_state(in.states + 10 * s);
+  const double* gl = in.goals + 10 * s;
+  const V3<double> goal_p{gl[0], gl[1], gl[2]};
+  const double* ps = in.poses + 10 * s;
+  const V3<double> pose_p{ps[0], ps[1], ps[2]};
+  const M3 body_to_world = rotmat(Q4<double>{ps[3], ps[4], ps[5], ps[6]});
+  const double horizon_s = static_cast<double>(N) * cfg.mppi_dt;
+
+  V3<double> initial, refined, safe_dir;
+  double safe_range, terminal_speed;
+  int ci = 0, cj = 0;
+  const double goal_dist = norm3(goal_p - x.p);
+  if (goal_dist > cfg.min_anchor_distance) {
+    const double lookahead = dmin(cfg.lookahead, goal_dist);
+    terminal_speed = dmin(cfg.terminal_speed, goal_dist / horizon_s);
+    // sample_initial_endpoints, index m = v*m_h + h
+    const int v = m / cfg.m_h, h = m % cfg.m_h;
+    const V3<double> tg = goal_p - x.p;
+    const double az0 = crm::atan2_cr(tg.y, tg.x);
+    const double el0 = crm::atan2_cr(tg.z, sqrt(tg.x * tg.x + tg.y * tg.y));
+    const double spacing = cfg.spacing_deg * kPiD / 180.0;
+    const double el_off = (static_cast<double>(v) - 0.5 * static_cast<double>(cfg.m_v - 1)) * spacing;
+    const double el = clampv(el0 + el_off, -kMaxElevation, kMaxElevation);
+    const double az = az0 + (static_cast<double>(h) - 0.5 * static_cast<double>(cfg.m_h - 1)) * spacing;
+    initial = x.p + lookahead * direction_from_angles(az, el);
+    // refine_endpoints
+    V3<double> dir_world = initial - pose_p;
+    if (sqnorm(dir_world) < 1e-18) dir_world = {1.0, 0.0, 0.0};
+    const double n2 = sqnorm(dir_world);
+    if (n2 > 0.0) {
+      const double n = sqrt(n2);
+      dir_world = {dir_world.x / n, dir_world.y / n, dir_world.z / n};
+    }
+    const V3<double> db = mat_t_vec(body_to_world, dir_world);
+    const double azb = crm::atan2_cr(db.y, db.x);
+    const double elb = crm::atan2_cr(db.z, sqrt(db.x * db.x + db.y * db.y));
+    ci = az_cell_exact(azb) / kPool;
+    cj = el_cell_exact(elb) / kPool;
+    const int64_t f = static_cast<int64_t>(s) * kCoarse + ci * kCEl + cj;
+    safe_range = P.safe_range[f];
+    safe_dir = mat_vec(body_to_world, V3<double>{P.safe_dir[3 * f], P.safe_dir[3 * f + 1], P.safe_dir[3 * f + 2]});
+    const double reach = dmin(lookahead, dmax(safe_range - cfg.col_d_max, cfg.min_anchor_distance));
+    refined = pose_p + reach * safe_dir;
+  } else {
+    // inside the anchor floor every guide settles on the goal at rest
+    initial = goal_p;
+    refined = goal_p;
+    safe_dir = qrot(x.q, V3<double>{1.0, 0.0, 0.0});
+    safe_range = in.r_max;
+    terminal_speed = 0.0;
+  }
+  const int64_t sm = static_cast<int64_t>(s) * M + m;
+  double* ai = pl.anchor_init + 3 * sm;
+  double* ar = pl.anchor_ref + 3 * sm;
+  double* ad = pl.anchor_dir + 3 * sm;
+  ai[0] = initial.x; ai[1] = initial.y; ai[2] = initial.z;
+  ar[0] = refined.x; ar[1] = refined.y; ar[2] = refined.z;
+  ad[0] = safe_dir.x; ad[1] = safe_dir.y; ad[2] = safe_dir.z;
+  pl.anchor_range[sm] = safe_range;
+  pl.anchor_ij[2 * sm] = ci;
+  pl.anchor_ij[2 * sm + 1] = cj;
+
+  // build_guides: start acceleration from the clamped last control
+  const Dyn<double> dy = make_dyn<double>(cfg);
+  const double* la = in.last_applied + 4 * s;
+  const double lt = clampv(la[0], dy.tmin, dy.tmax);
+  const V3<double> lw{clampv(la[1], -dy.wxy, dy.wxy), clampv(la[2], -dy.wxy, dy.wxy), clampv(la[3], -dy.wz, dy.wz)};
+  const V3<double> a0 = derivative(x, lt, lw, dy).dv;
+  const V3<double> end_v = terminal_speed * safe_dir;
+  // solve_quintic (guidance.cpp:74-94)
+  const double T = horizon_s;
+  const double T2 = T * T, T3 = T2 * T, T4 = T3 * T, T5 = T4 * T;
+  const V3<double> half_a = 0.5 * a0;
+  const V3<double> dp = refined - ((x.p + T * x.v) + T2 * half_a);
+  const V3<double> dv = end_v - (x.v + T * a0);
+  const V3<double> da = V3<double>{0.0, 0.0, 0.0} - a0;
+  V3<double> c[6];
+  c[0] = x.p;
+  c[1] = x.v;
+  c[2] = half_a;
+  const double e3 = 2.0 * T3, e4 = 2.0 * T4, e5 = 2.0 * T5;
+  const double t8 = 8.0 * T, t14 = 14.0 * T, t6 = 6.0 * T, t2 = 2.0 * T2;
+  {
+    const V3<double> num = ((20.0 * dp - t8 * dv) + T2 * da);
+    c[3] = {num.x / e3, num.y / e3, num.z / e3};
+  }
+  {
+    const V3<double> num = ((-30.0 * dp + t14 * dv) - t2 * da);
+    c[4] = {num.x / e4, num.y / e4, num.z / e4};
+  }
+  {
+    const V3<double> num = ((12.0 * dp - t6 * dv) + T2 * da);
+    c[5] = {num.x / e5, num.y / e5, num.z / e5};
+  }
+  double* gc = pl.guide_coef + 18 * sm;
+  for (int k = 0; k < 6; ++k) {
+    gc[k] = c[k].x;
+    gc[6 + k] = c[k].y;
+    gc[12 + k] = c[k].z;
+  }
+  // guide table g(t * dt) for t < N (tracking cost, costs.hpp:59-66)
+  for (int t = 0; t < N; ++t) {
+    double tt = static_cast<double>(t) * cfg.dyn_dt;
+    tt = clampv(tt, 0.0, T);
+    V3<double> o = c[5];
+    for (int k = 4; k >= 0; --k) o = V3<double>{o.x * tt, o.y * tt, o.z * tt} + c[k];
+    const int64_t gi = sm * N + t;
+    pl.guide64[3 * gi] = o.x;
+    pl.guide64[3 * gi + 1] = o.y;
+    pl.guide64[3 * gi + 2] = o.z;
+    pl.guide32[gi] = make_float4(static_cast<float>(o.x), static_cast<float>(o.y), static_cast<float>(o.z), 0.f);
+  }
+  // warm start: shifted previous winner, or hover (ensemble.cpp:68-77)
+  const int plen = in.prev ? (in.prev_len ? in.prev_len[s] : N) : 0;
+  double* nom = pl.nominal + sm * N * 4;
+  if (plen == N) {
+    const double* pv = in.prev + static_cast<int64_t>(s) * N * 4;
+    for (int j = 0; j < N; ++j) {
+      const int src = j + 1 < N ? j + 1 : N - 1;
+      for (int cc = 0; cc < 4; ++cc) nom[4 * j + cc] = pv[4 * src + cc];
+    }
+  } else {
+    const double hover = cfg.mass * sqrt((cfg.gravity[0] * cfg.gravity[0] + cfg.gravity[1] * cfg.gravity[1]) +
+                                         cfg.gravity[2] * cfg.gravity[2]);
+    for (int j = 0; j < N; ++j) {
+      nom[4 * j] = hover;
+      nom[4 * j + 1] = 0.0;
+      nom[4 * j + 2] = 0.0;
+      nom[4 * j + 3] = 0.0;
+    }
+  }
+  pl.alive[sm] = 1;
+  pl.stage1[sm] = 0.0;
+  pl.ess[sm] = 0.0;
+}
+
+// Fill an FP64 rollout environment for (scene, instance); unom may point to
+// shared or global memory.
+__device__ __forceinline__ RolloutEnv<double> make_env64(const BatchIn& in, const Perception& P, const Plan& pl,
+                                                        const DevConfig& cfg, int s, int m, const double* unom) {
+  RolloutEnv<double> e;
+  const int64_t sm = static_cast<int64_t>(s) * cfg.M + m;
+  e.unom = unom;
+  e.guide = pl.guide64 + sm * cfg.N * 3;
+  e.N = cfg.N;
+  e.dyn = make_dyn<double>(cfg);
+  const double* gl = in.goals + 10 * s;
+  e.pg = {gl[0], gl[1], gl[2]};
+  e.vg = {gl[3], gl[4], gl[5]};
+  const M3 g = rotmat(Q4<double>{gl[6], gl[7], gl[8], gl[9]});
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) e.gt.m[i][j] = g.m[j][i];
+  e.q_p = cfg.q_p;
+  e.q_v = cfg.q_v;
+  e.q_q = cfg.q_q;
+  e.cs = cfg.col_scale;
+  e.ca = cfg.col_slope;
+  e.cdmin = cfg.col_d_min;
+  e.cdmax = cfg.col_d_max;
+  e.grid = P.grid[s];
+  e.gstart = P.grid_start + static_cast<int64_t>(s) * (kGridCells + 1);
+  e.gpts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
+  e.has_guide = true;
+  return e;
+}
+
+__device__ __forceinline__ const double* injected_row(const BatchIn& in, const DevConfig& cfg, int s, int iter, int m,
+                                                      int k) {
+  const int64_t row = (((static_cast<int64_t>(s) * cfg.iterations + iter) * cfg.M + m) * cfg.K + k);
+  return in.injected + row * cfg.N * 4;
+}
+
+// ---------------------------------------------------------------------------
+// K3d: FP64 stage I (precision 64)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_stage1_f64(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter) {
+  extern __shared__ double sm_unom[];
+  const int tiles = (cfg.K + blockDim.x - 1) / blockDim.x;
+  int b = blockIdx.x;
+  const int tile = b % tiles;
+  b /= tiles;
+  const int m = b % cfg.M;
+  const int s = b / cfg.M;
+  const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
+  const int N = cfg.N;
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) sm_unom[i] = pl.nominal[smi * N * 4 + i];
+  __syncthreads();
+  const int k = tile * blockDim.x + threadIdx.x;
+  if (k >= cfg.K) return;
+  double* out = pl.cost64 + smi * cfg.K + k;
+  if (!pl.alive[smi]) {
+    *out = __longlong_as_double(0x7ff0000000000000ll);
+    return;
+  }
+  const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, sm_unom);
+  const St<double> x0 = load_state(in.states + 10 * s);
+  CostSums<double> cs;
+  if (in.injected) {
+    cs = rollout_costs(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)});
+  } else {
+    const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+    const PertRngD pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                      cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+    cs = rollout_costs(x0, env, pr);
+  }
+  *out = cs.valid ? stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta)
+                  : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// ---------------------------------------------------------------------------
+// K4b: update + stage II + selection
+// ---------------------------------------------------------------------------
+constexpr int kUpdateThreads = 256;
+
+struct UpdateScratch {  // global, per (scene, instance): [K] each
+  uint32_t* cand_k;
+  double* cand_s;
+  double* cand_w;
+};
+
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(kUpdateThreads) k_update(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                           UpdateScratch us, int iter, int precision, int last_iter) {
+  __shared__ double s_unom[4 * 64];
+  __shared__ double s_red[kUpdateThreads / 32];
+  __shared__ uint32_t s_cnt[kUpdateThreads / 32 + 1];
+  __shared__ double s_rho_screen, s_rho, s_eta;
+  __shared__ uint32_t s_ncand;
+  __shared__ int s_dead;
+  __shared__ bool s_last;
+
+  const int m = blockIdx.x % cfg.M;
+  const int s = blockIdx.x / cfg.M;
+  const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
+  const int K = cfg.K, N = cfg.N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  uint32_t* cand_k = us.cand_k + smi * K;
+  double* cand_s = us.cand_s + smi * K;
+  double* cand_w = us.cand_w + smi * K;
+
+  for (int i = tid; i < 4 * N; i += blockDim.x) s_unom[i] = pl.nominal[smi * N * 4 + i];
+  const bool alive = pl.alive[smi] != 0;
+
+  if (alive) {
+    // 1. screening minimum over finite costs
+    double lmin = kInf;
+    for (int k = tid; k < K; k += blockDim.x) {
+      const double c = precision == 32 ? static_cast<double>(pl.cost32[smi * K + k]) : pl.cost64[smi * K + k];
+      if (isfinite(c)) lmin = fmin(lmin, c);
+    }
+    lmin = warp_min(lmin);
+    if (lane == 0) s_red[warp] = lmin;
+    __syncthreads();
+    if (tid == 0) {
+      double r = kInf;
+      for (int w = 0; w < kUpdateThreads / 32; ++w) r = fmin(r, s_red[w]);
+      s_rho_screen = r;
+      s_dead = !isfinite(r);
+    }
+    __syncthreads();
+  } else {
+    if (tid == 0) s_dead = 1;
+    __syncthreads();
+  }
+
+  if (!s_dead) {
+    // 2. softmin support in k order: every sample whose weight can exceed
+    //    e^-64 relative to the minimum (FP32 screening adds a safety margin)
+    const double rho_s = s_rho_screen;
+    const double window = precision == 32 ? 64.0 * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
+    const int per = (K + blockDim.x - 1) / blockDim.x;
+    const int k0 = min(tid * per, K), k1 = min(k0 + per, K);
+    uint32_t mine = 0;
+    for (int k = k0; k < k1; ++k) {
+      const double c = precision == 32 ? static_cast<double>(pl.cost32[smi * K + k]) : pl.cost64[smi * K + k];
+      mine += (isfinite(c) && c - rho_s <= window);
+    }
+    // block exclusive scan
+    uint32_t x = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_cnt[warp] = x;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+      for (int w = 0; w < kUpdateThreads / 32; ++w) {
+        const uint32_t t = s_cnt[w];
+        s_cnt[w] = run;
+        run += t;
+      }
+      s_ncand = run;
+    }
+    __syncthreads();
+    uint32_t pos = s_cnt[warp] + x - mine;
+    for (int k = k0; k < k1; ++k) {
+      const double c = precision == 32 ? static_cast<double>(pl.cost32[smi * K + k]) : pl.cost64[smi * K + k];
+      if (isfinite(c) && c - rho_s <= window) {
+        cand_k[pos] = static_cast<uint32_t>(k);
+        cand_s[pos] = c;
+        ++pos;
+      }
+    }
+    __syncthreads();
+    const uint32_t ncand = s_ncand;
+    const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+
+    // 3. exact FP64 stage-I cost of the support (FP32 screening only)
+    if (precision == 32) {
+      const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, s_unom);
+      const St<double> x0 = load_state(in.states + 10 * s);
+      for (uint32_t c = tid; c < ncand; c += blockDim.x) {
+        const int k = static_cast<int>(cand_k[c]);
+        CostSums<double> cs;
+        if (in.injected) {
+          cs = rollout_costs(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)});
+        } else {
+          const PertRngD pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                            cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+          cs = rollout_costs(x0, env, pr);
+        }
+        cand_s[c] = cs.valid ? stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta) : kInf;
+      }
+      __syncthreads();
+    }
+
+    // 4. rho, weights, eta, ess in k order (compute_weights, mppi.cpp:70-87)
+    if (tid == 0) {
+      double rho = kInf;
+      for (uint32_t c = 0; c < ncand; ++c)
+        if (isfinite(cand_s[c])) rho = dmin(rho, cand_s[c]);
+      double eta = 0.0;
+      for (uint32_t c = 0; c < ncand; ++c) {
+        const double e = isfinite(cand_s[c]) ? exp(-(cand_s[c] - rho) / cfg.lambda) : 0.0;
+        cand_w[c] = e;
+        eta += e;
+      }
+      double w2 = 0.0;
+      for (uint32_t c = 0; c < ncand; ++c) {
+        const double w = cand_w[c] / eta;
+        cand_w[c] = w;
+        w2 += w * w;
+      }
+      s_rho = rho;
+      s_eta = eta;
+      if (isfinite(rho)) {
+        pl.stage1[smi] = rho;
+        pl.ess[smi] = w2 > 0.0 ? 1.0 / w2 : 0.0;
+      } else {
+        s_dead = 1;  // "no valid rollout" after exact re-evaluation
+        pl.alive[smi] = 0;
+      }
+      pl.n_support[smi] = ncand;
+    }
+    __syncthreads();
+
+    // 5. u_j <- clamp(u_j + sum_k w_k delta_k[j]) (update_nominal, mppi.cpp:89-101),
+    //    deltas regenerated from the counter RNG and clamped against u_j
+    const Dyn<double> dy = make_dyn<double>(cfg);
+    for (int jc = tid; jc < 4 * N && !s_dead; jc += blockDim.x) {
+      const int j = jc >> 2, c = jc & 3;
+      const double u = s_unom[jc];
+      const double lo = c == 0 ? dy.tmin : (c == 3 ? -dy.wz : -dy.wxy);
+      const double hi = c == 0 ? dy.tmax : (c == 3 ? dy.wz : dy.wxy);
+      double du = 0.0;
+      for (uint32_t ci = 0; ci < ncand; ++ci) {
+        const double w = cand_w[ci];
+        if (w == 0.0) continue;
+        const int k = static_cast<int>(cand_k[ci]);
+        double draw;
+        if (in.injected) {
+          draw = injected_row(in, cfg, s, iter, m, k)[jc];
+        } else {
+          const uint64_t key = stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
+          double n0, n1;
+          normal_pair(key, static_cast<uint32_t>(jc >> 1), n0, n1);
+          draw = cfg.sigma[c] * ((jc & 1) ? n1 : n0);
+        }
+        const double applied = clampv(u + draw, lo, hi) - u;
+        du = du + w * applied;
+      }
+      pl.nominal[smi * N * 4 + jc] = clampv(u + du, lo, hi);
+    }
+  } else if (alive) {
+    if (tid == 0) pl.alive[smi] = 0;  // no valid rollout: the instance dies
+  }
+  __syncthreads();
+
+  if (!last_iter) return;
+
+  // 6. stage II (ensemble.cpp:132-149): noise-free re-rollout, goal + collision
+  if (tid == 0) {
+    double st2 = kInf;
+    bool valid = false;
+    double bd[5] = {0, 0, 0, 0, 0};
+    if (!s_dead) {
+      const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * N * 4);
+      const CostSums<double> cs = rollout_costs(load_state(in.states + 10 * s), env, PertZero<double>{});
+      if (cs.valid) {
+        st2 = cs.goal + cs.col;
+        valid = isfinite(st2);
+        bd[0] = cfg.q_track * cs.trk;
+        bd[1] = cfg.q_vnorm * cs.vn;
+        bd[2] = cfg.q_c * cs.mag + cfg.q_c_delta * cs.rate;
+        bd[3] = cs.goal;
+        bd[4] = cs.col;
+      }
+    }
+    pl.stage2[smi] = st2;
+    pl.valid[smi] = valid ? 1 : 0;
+    for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
+    __threadfence();
+    const int arrived = atomicAdd(pl.done + s, 1);
+    s_last = arrived == cfg.M - 1;
+  }
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence();
+  // 7. selection: first minimum stage-2 among valid instances
+  int winner = -1;
+  const int64_t base = static_cast<int64_t>(s) * cfg.M;
+  for (int mm = 0; mm < cfg.M; ++mm) {
+    if (!pl.valid[base + mm]) continue;
+    if (winner < 0 || pl.stage2[base + mm] < pl.stage2[base + winner]) winner = mm;
+  }
+  pl.winner[s] = winner;
+  pl.status[s] = winner < 0 ? 1 : 0;
+  if (winner >= 0) {
+    const Dyn<double> dy = make_dyn<double>(cfg);
+    const double* u = pl.nominal + (base + winner) * N * 4;
+    pl.control[4 * s] = clampv(u[0], dy.tmin, dy.tmax);
+    pl.control[4 * s + 1] = clampv(u[1], -dy.wxy, dy.wxy);
+    pl.control[4 * s + 2] = clampv(u[2], -dy.wxy, dy.wxy);
+    pl.control[4 * s + 3] = clampv(u[3], -dy.wz, dy.wz);
+  }
+  pl.done[s] = 0;
+}
+
+// Winner re-rollout states/controls (PlanResult::winner_rollout) on request.
+__global__ void k_winner_rollout(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= in.S) return;
+  const int w = pl.winner[s];
+  if (w < 0) return;
+  const int64_t smi = static_cast<int64_t>(s) * cfg.M + w;
+  const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, w, pl.nominal + smi * cfg.N * 4);
+  rollout_costs(load_state(in.states + 10 * s), env, PertZero<double>{}, pl.winner_states + static_cast<int64_t>(s) * (cfg.N + 1) * 10,
+                pl.winner_controls + static_cast<int64_t>(s) * cfg.N * 4);
+}
+
+__global__ void k_gather(Plan pl, DevConfig cfg, int S, GatherOut g) {
+  const int s = blockIdx.x;
+  if (s >= S) return;
+  const int w = pl.winner[s];
+  const int M = cfg.M, N = cfg.N;
+  const int64_t base = static_cast<int64_t>(s) * M;
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x)
+    if (g.winner_nominal) g.winner_nominal[static_cast<int64_t>(s) * N * 4 + i] = w >= 0 ? pl.nominal[(base + w) * N * 4 + i] : 0.0;
+  for (int m = threadIdx.x; m < M; m += blockDim.x)
+    if (g.stage2) g.stage2[base + m] = pl.stage2[base + m];
+  if (threadIdx.x < 5 && g.breakdown) g.breakdown[5 * s + threadIdx.x] = w >= 0 ? pl.breakdown[(base + w) * 5 + threadIdx.x] : 0.0;
+  if (threadIdx.x < 4 && g.control) g.control[4 * s + threadIdx.x] = w >= 0 ? pl.control[4 * s + threadIdx.x] : 0.0;
+  if (threadIdx.x == 0) {
+    if (g.status) g.status[s] = pl.status[s];
+    if (g.winner) g.winner[s] = w;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gather(const Plan& pl, const DevConfig& cfg, int S, const GatherOut& g, cudaStream_t st) {
+  k_gather<<<S, 128, 0, st>>>(pl, cfg, S, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                             int precision, bool want_winner_rollout, uint32_t* cand_k, double* cand_s, double* cand_w,
+                             cudaStream_t st, KernelTimer* timer) {
+  const int SM = in.S * cfg.M;
+  {
+    TimedRegion t(timer, "k_anchors", st);
+    k_anchors<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+  }
+  const UpdateScratch us{cand_k, cand_s, cand_w};
+  for (int iter = 0; iter < cfg.iterations; ++iter) {
+    if (precision == 32) {
+      cudaError_t e = launch_stage1_f32(in, P, pl, cfg, iter, st, timer);
+      if (e != cudaSuccess) return e;
+    } else {
+      const int threads = 128;
+      const int tiles = (cfg.K + threads - 1) / threads;
+      TimedRegion t(timer, "k_stage1_f64", st);
+      k_stage1_f64<<<SM * tiles, threads, 4 * cfg.N * sizeof(double), st>>>(in, P, pl, cfg, iter);
+    }
+    TimedRegion t(timer, "k_update", st);
+    k_update<<<SM, kUpdateThreads, 0, st>>>(in, P, pl, cfg, us, iter, precision, iter + 1 == cfg.iterations);
+  }
+  if (want_winner_rollout) {
+    TimedRegion t(timer, "k_winner_rollout", st);
+    k_winner_rollout<<<(in.S + 31) / 32, 32, 0, st>>>(in, P, pl, cfg);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace amppi_dev

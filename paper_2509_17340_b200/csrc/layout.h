@@ -1,0 +1,127 @@
+// Device-side data layout shared by the host runtime and the kernels.
+// Everything here is POD; see DESIGN.md "Data layout in HBM".
+#pragma once
+
+#include <cstdint>
+
+namespace amppi_dev {
+
+// Partition geometry (perception.hpp:12-22).
+constexpr int kAz = 120;
+constexpr int kEl = 60;
+constexpr int kPool = 6;
+constexpr int kCAz = kAz / kPool;
+constexpr int kCEl = kEl / kPool;
+constexpr int kCells = kAz * kEl;       // 7200, flat(i,j) = i*60 + j
+constexpr int kCoarse = kCAz * kCEl;    // 200, flat(I,J) = I*10 + J
+constexpr double kMinPointRange = 0.05;
+constexpr double kHorizonReach = 25.0;
+
+// Collision grid: at most kGridAxis cells per axis, cell size >= d_max.
+constexpr int kGridAxis = 24;
+constexpr int kGridCells = kGridAxis * kGridAxis * kGridAxis;
+constexpr int kOccAxis = kGridAxis + 2;
+constexpr int kOccWords = (kOccAxis * kOccAxis * kOccAxis + 31) / 32;
+
+constexpr uint64_t kEmptyCell = 0xFFFFFFFFFFFFFFFFull;  // > bits of any finite positive double
+
+// Flat copy of amppi_config plus derived sizes.
+struct DevConfig {
+  int m_h, m_v, M, K, N, iterations;
+  double lookahead, spacing_deg, terminal_speed, min_anchor_distance;
+  double lambda, sigma[4], mppi_dt;
+  double q_track, q_vnorm, q_c, q_c_delta, q_p, q_v, q_q;
+  double col_scale, col_slope, col_d_min, col_d_max;
+  double mass, gravity[3], dyn_dt, thrust_min, thrust_max, omega_xy_max, omega_z_max;
+  double r_max;
+};
+
+struct GridMeta {
+  double origin[3];
+  double h, inv_h;
+  float origin_f[3];
+  float inv_h_f;
+  int dims[3];
+  int n_points;
+};
+
+// Per-batch input arrays (device pointers).  States/goals are 10 doubles:
+// p(3) q(w,x,y,z) v(3) and p_goal(3) v_goal(3) q_goal(4).
+struct BatchIn {
+  const float* xyz;
+  const double* xyz64;        // alternative FP64 input (single-scene API), or null
+  const int64_t* offsets;     // [S+1]
+  const double* poses;        // [S*10]
+  const double* states;       // [S*10]
+  const double* goals;        // [S*10]
+  const double* prev;         // [S*N*4] or null
+  const int32_t* prev_len;    // [S] or null
+  const double* last_applied; // [S*4]
+  const uint64_t* cycles;     // [S]
+  const uint64_t* seeds;      // [S]
+  const double* injected;     // [S*iters*M*K*N*4] or null
+  int S;
+  double r_max;
+};
+
+struct Candidate {
+  uint32_t cell;   // scene*kCells + f
+  uint32_t idx;    // point index within the scene
+  uint64_t bits;   // range as IEEE bits
+};
+
+struct Perception {
+  uint64_t* cell_r;            // [S*7200] min range bits (kEmptyCell when empty)
+  uint32_t* cell_idx;          // [S*7200] argmin point index
+  Candidate* cand;             // [cap]
+  unsigned long long* cand_count;
+  int64_t cand_cap;
+  const double* cell_dir;      // [7200*3] cell-centre directions (host libm)
+  // outputs
+  double* ranges;              // [S*7200] or null (verification)
+  uint8_t* has_point;          // [S*7200] or null
+  double* nearest;             // [S*7200*3] or null
+  double* filtered;            // [S*7200*3] or null (flat-cell order)
+  double* safe_range;          // [S*200]
+  double* safe_dir;            // [S*600]
+  double* safe_point;          // [S*600]
+  int32_t* n_filtered;         // [S]
+  GridMeta* grid;              // [S]
+  uint32_t* grid_start;        // [S*(kGridCells+1)]
+  uint32_t* grid_occ;          // [S*kOccWords]
+  double* grid_pts64;          // [S*7200*3] sorted by grid cell
+  float4* grid_pts32;          // [S*7200]
+};
+
+struct Plan {
+  // anchors / guides (FP64)
+  double* anchor_init;         // [S*M*3]
+  double* anchor_ref;          // [S*M*3]
+  double* anchor_dir;          // [S*M*3]
+  double* anchor_range;        // [S*M]
+  int32_t* anchor_ij;          // [S*M*2]
+  double* guide_coef;          // [S*M*18] [axis][power]
+  double* guide64;             // [S*M*N*3]
+  float4* guide32;             // [S*M*N]
+  double* nominal;             // [S*M*N*4] current nominal (FP64 always)
+  // stage I
+  float* cost32;               // [S*M*K]
+  double* cost64;              // [S*M*K]
+  uint8_t* alive;              // [S*M]
+  // per instance
+  double* stage1;              // [S*M]
+  double* stage2;              // [S*M]
+  double* ess;                 // [S*M]
+  uint8_t* valid;              // [S*M]
+  double* breakdown;           // [S*M*5]
+  uint32_t* n_support;         // [S*M] softmin support size (diagnostics)
+  // per scene
+  int32_t* done;               // [S] arrival counter (self-resetting)
+  int32_t* winner;             // [S]
+  int32_t* status;             // [S]
+  double* control;             // [S*4]
+  double* winner_states;       // [S*(N+1)*10] or null
+  double* winner_controls;     // [S*N*4] or null
+};
+
+}  // namespace amppi_dev
