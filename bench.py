@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""AERO-MPPI plan-cycle benchmark (BASELINE.json metric: rollout-steps/s and
+p50 plan-cycle latency).
+
+Default workload = config C5 (the largest single-GPU config): 4096
+independent synthetic scenes (forest / verticals / inclines, 20k LiDAR points
+each), every scene planned with 4x2 anchors x 256 samples x 30 steps.  A
+"step" is one full plan cycle (build_snapshot + plan_step) for every scene.
+Scenes are sharded across ranks (strong scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+value  : rollout-steps/s with inputs resident in HBM (amppi_cycle_batch_device)
+e2e    : same metric through the host-pointer API amppi_cycle_batch (pinned
+         host inputs copied in and results copied out every step)
+latency: p50 / p99 of host-to-host amppi_snapshot + amppi_plan on a C1 cycle
+roofline / cpu_baseline / clocks / gpu_launches: see DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rollout-steps/s (anchors×samples×horizon); p50 plan-cycle latency ms"
+FLOPS_PER_STEP = 440  # algorithmic FP32 flops per rollout-step (FMA = 2)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scenes", type=int, default=4096)
+    ap.add_argument("--points", type=int, default=20000)
+    ap.add_argument("--latency-cycles", type=int, default=1000)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(data: dict, cfg, scene_ids, seconds: float) -> dict:
+    """Oracle restatement (oracle/, the reference's parallel_for threading with
+    hardware_concurrency workers) on a time-bounded sample of the workload."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    from oracle_py import Oracle
+
+    orc = Oracle()
+    cores = os.cpu_count() or 1
+    orc.set_workers(cores)
+    ocfg = orc.config(cfg)
+    off = data["offsets"]
+    done, t0 = 0, time.perf_counter()
+    for s in scene_ids:
+        pts = data["xyz"][off[s]:off[s + 1]].astype(np.float64)
+        snap = orc.snapshot(pts, data["poses"][s], cfg.r_max)
+        g = data["goals"][s]
+        orc.plan(snap, ocfg, data["states"][s], g[0:3], g[3:6], g[6:10], None, data["last"][s],
+                 int(data["cycles"][s]), int(data["seeds"][s]))
+        done += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    steps = done * cfg.grid.count() * cfg.mppi.rollouts * cfg.mppi.horizon * cfg.mppi.iterations
+    return {"value": steps / dt, "unit": "rollout-steps/s", "cores": cores, "kind": "port",
+            "sample": f"{done} scenes of the workload (build_snapshot + plan_step each), {dt:.1f} s, "
+                      f"oracle/ restatement, parallel_for over {cores} threads"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path (the
+    oracle restatement; the reference itself cannot be built here, SURVEY.md
+    §0) on this box's host cores, same config / metric, bounded samples."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    from oracle_py import Oracle
+
+    from paper_2509_17340_b200.workloads import plan_config, rollout_steps
+
+    cfg = plan_config()
+    orc = Oracle()
+    cores = os.cpu_count() or 1
+    orc.set_workers(cores)
+    ocfg = orc.config(cfg)
+    # inputs from the oracle's own simulator: C5 scene family, 20k points each
+    n_sample = 3
+    scenes = []
+    for s in range(n_sample):
+        sc = orc.scene(1 + s % 3, s + 1)
+        rng = np.random.default_rng(12345 + s)
+        start = np.array([rng.uniform(1.0, 30.0), rng.uniform(-8.0, 8.0), 2.0])
+        frames, pose = [], None
+        for f in range(20):
+            pose = np.concatenate([start + [0.06 * f, 0, 0], [1, 0, 0, 0], [3.0, 0, 0]])
+            frames.append(sc.lidar(pose, 1000 * s + f))
+        pts = np.concatenate(frames)[: args.points]
+        scenes.append((pts, pose))
+    goal_q = np.array([1.0, 0, 0, 0])
+
+    def step(i):
+        for pts, pose in scenes:
+            snap = orc.snapshot(pts, pose, cfg.r_max)
+            orc.plan(snap, ocfg, pose, [45.0, 0, 2.0], [0, 0, 0], goal_q, None, [9.81, 0, 0, 0], 100 + i, 1)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    value = rollout_steps(cfg, n_sample) * args.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": "rollout-steps/s", "impl": "reference", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 sample: forest/verticals/inclines scenes x (4x2 anchors x 256 samples x 30 "
+                                   "steps), 20k points each", "scenes_per_step": n_sample,
+                       "anchors": cfg.grid.count(), "samples": cfg.mppi.rollouts, "horizon": cfg.mppi.horizon},
+            "cpu_baseline": {"value": value, "unit": "rollout-steps/s", "cores": cores, "kind": "port",
+                             "sample": f"{n_sample} scenes per step, oracle/ restatement of build_snapshot + "
+                                       f"plan_step (reference not buildable: Eigen/vendor absent)"},
+            "e2e": {"value": value, "unit": "rollout-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_2509_17340_b200 import ControlInput, GoalSpec, Planner, State, load
+    from paper_2509_17340_b200.workloads import plan_config, rollout_steps, scenes
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    # a dedicated (non-default) stream: the planner launches on it and the
+    # timing events are recorded on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    cfg = plan_config()
+    S_total = args.scenes
+    per = [S_total // ws + (1 if r < S_total % ws else 0) for r in range(ws)]
+    first = sum(per[:rank])
+    S = per[rank]
+    data = scenes(S, points=args.points, frames=20, first=first, device=local)
+    P = int(data["offsets"][-1])
+    planner = Planner(cfg, device=local, precision=32, max_scenes=S, max_points=max(P, 1 << 16), profile=True,
+                      stream=stream.cuda_stream)
+
+    def tens(a, dt):
+        return torch.from_numpy(np.ascontiguousarray(a).view(dt) if a.dtype != dt else np.ascontiguousarray(a))
+
+    dvals = {
+        "xyz": torch.from_numpy(data["xyz"]).to(dev),
+        "offsets": torch.from_numpy(data["offsets"]).to(dev),
+        "poses": torch.from_numpy(data["poses"]).to(dev),
+        "states": torch.from_numpy(data["states"]).to(dev),
+        "goals": torch.from_numpy(data["goals"]).to(dev),
+        "last": torch.from_numpy(data["last"]).to(dev),
+        "cycles": torch.from_numpy(data["cycles"].view(np.int64)).to(dev),
+        "seeds": torch.from_numpy(data["seeds"].view(np.int64)).to(dev),
+    }
+    N, M = cfg.mppi.horizon, cfg.grid.count()
+    dout = {"status": torch.zeros(S, dtype=torch.int32, device=dev), "winner": torch.zeros(S, dtype=torch.int32, device=dev),
+            "control": torch.zeros(S, 4, dtype=torch.float64, device=dev),
+            "winner_nominal": torch.zeros(S, N, 4, dtype=torch.float64, device=dev),
+            "stage2": torch.zeros(S, M, dtype=torch.float64, device=dev),
+            "breakdown": torch.zeros(S, 5, dtype=torch.float64, device=dev)}
+    dptr = {k: v.data_ptr() for k, v in dvals.items()}
+    optr = {k: v.data_ptr() for k, v in dout.items()}
+
+    def step():
+        dvals["cycles"].add_(1)  # fresh perturbation streams every cycle
+        planner.cycle_batch_device(dptr, optr, S, cfg.r_max)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    planner.kernel_times_reset()
+    sampler = ClockSampler(local)
+    sampler.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    planner.synchronize()
+    ktimes = planner.kernel_times()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_steps = rollout_steps(cfg, S_total) * args.steps
+    value = total_steps / (ms_max / 1e3)
+    n_ok = int((dout["status"] == 0).sum().item())
+    launches = sum(v[1] for v in ktimes.values())
+
+    # roofline of the dominant kernel (FP32 stage-I rollouts)
+    lib = load()
+    import ctypes
+
+    peak = ctypes.c_double()
+    pms = ctypes.c_double()
+    lib.amppi_probe_fp32_peak(local, ctypes.byref(peak), ctypes.byref(pms))
+    k_ms, k_n = ktimes.get("k_stage1_f32", (float("nan"), 1))
+    per_launch_flops = FLOPS_PER_STEP * rollout_steps(cfg, S) / cfg.mppi.iterations
+    achieved = per_launch_flops / (k_ms / k_n / 1e3) / 1e12
+    share = k_ms / sum(v[0] for v in ktimes.values())
+
+    # e2e through the host-pointer API
+    e2e = None
+    if not args.no_e2e:
+        pinned_xyz = torch.from_numpy(data["xyz"]).pin_memory()  # keep alive while in use
+        host = {k: data[k] for k in ("offsets", "poses", "states", "goals", "last", "cycles", "seeds")}
+        host["xyz"] = pinned_xyz.numpy()
+        planner.kernel_times_reset()
+        for i in range(max(1, args.warmup)):
+            planner.cycle_batch(host["offsets"], host["xyz"], host["poses"], host["states"], host["goals"],
+                                host["last"], host["cycles"] + i, host["seeds"])
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            planner.cycle_batch(host["offsets"], host["xyz"], host["poses"], host["states"], host["goals"],
+                                host["last"], host["cycles"] + 1000 + i, host["seeds"])
+        el = time.perf_counter() - t0
+        t = torch.tensor([el], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+        h2d = (data["xyz"].nbytes + data["offsets"].nbytes + data["poses"].nbytes + data["states"].nbytes +
+               data["goals"].nbytes + data["last"].nbytes + data["cycles"].nbytes + data["seeds"].nbytes)
+        d2h = S * (4 + 4 + 8 * 4 + 8 * N * 4 + 8 * M + 8 * 5)
+        e2e = {"value": total_steps / el, "unit": "rollout-steps/s", "h2d_bytes_per_step": int(h2d) * ws,
+               "d2h_bytes_per_step": int(d2h) * ws, "ms_per_step": 1000 * el / args.steps}
+
+    latency = None
+    cpu = None
+    if rank == 0:
+        # p50 plan-cycle latency: C1 single scene, host-to-host through the C-ABI
+        one = scenes(1, points=args.points, frames=20, first=0, kinds=1, device=local)
+        lp = Planner(cfg, device=local, precision=32, max_scenes=1, max_points=1 << 16)
+        pts = one["xyz"]
+        x = State.from_array(one["states"][0])
+        goal = GoalSpec((45.0, 0.0, 2.0), (0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0))
+        la = ControlInput(one["last"][0][0], (0.0, 0.0, 0.0))
+        prev = None
+        lat = []
+        for i in range(100 + args.latency_cycles):
+            t0 = time.perf_counter()
+            snap = lp.build_snapshot(pts, x, cfg.r_max)
+            r = lp.plan_step(x, goal, snap, prev, la, 100 + i, 1, want_rollout=False)
+            t1 = time.perf_counter()
+            prev = r.per_instance[r.winner].nominal
+            if i >= 100:
+                lat.append(1000 * (t1 - t0))
+        lp.close()
+        lat.sort()
+        latency = {"workload": "C1: one forest scene, 20k float32 points, 4x2 anchors x 256 x 30, host-to-host "
+                               "amppi_snapshot + amppi_plan (pinned staging, warm nominal)",
+                   "p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(0.99 * len(lat))], "cycles": len(lat),
+                   "rollout_steps_per_s_at_p50": rollout_steps(cfg, 1) / (lat[len(lat) // 2] / 1e3)}
+        cpu = cpu_baseline(data, cfg, range(min(S, 64)), args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rollout-steps/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 stage-I screening / f64 keys, anchors, update, "
+                                                             "stage II", "data": "synthetic",
+            "config": {"workload": "C5: independent synthetic scenes (forest/verticals/inclines, GPU LiDAR, "
+                                   f"{args.points} points each) x (4x2 anchors x 256 samples x 30 steps), one full "
+                                   "plan cycle (snapshot + plan) per scene per step",
+                       "scenes": S_total, "anchors": M, "samples": cfg.mppi.rollouts, "horizon": N,
+                       "iterations": cfg.mppi.iterations, "points_total": int(P) * ws,
+                       "parallelism": f"scene-sharded x{ws}",
+                       "l2": "inputs larger than L2 (points alone %.0f MB vs 126 MB)" % (data["xyz"].nbytes / 1e6),
+                       "planned_ok": n_ok},
+            "latency": latency,
+            "e2e": e2e,
+            "roofline": {"bound": "fp32", "kernel": "k_stage1_f32", "achieved": achieved, "peak": peak.value,
+                         "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": None,
+                         "peak_source": "measured FFMA probe (amppi_probe_fp32_peak) in this run",
+                         "algorithmic_flops_per_launch": per_launch_flops,
+                         "kernel_ms_per_launch": k_ms / k_n, "kernel_share_of_step": share},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+            "kernels": {k: {"ms_total": v[0], "launches": v[1]} for k, v in sorted(ktimes.items())},
+        }
+        print(json.dumps(line), flush=True)
+    planner.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

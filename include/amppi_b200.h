@@ -205,6 +205,21 @@ int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* 
 int amppi_kernel_times_reset(amppi_ctx* ctx);
 int amppi_set_stream(amppi_ctx* ctx, void* stream);
 
+/* Synthetic input generator (not on the plan path):
+ * scenario families of sim_world.cpp:174-246 (kind 0 empty, 1 forest,
+ * 2 verticals, 3 inclines, 4 two_gap) and the per-cell jittered LiDAR of
+ * sim_world.cpp:248-328 ray-cast on the GPU in FP32.  Frame f of scene s uses
+ * poses[s*frames+f] / frame_seeds[s*frames+f]; hits are packed per scene in
+ * frame-then-ray order, at most cap_per_scene points per scene;
+ * xyz_out holds n_scenes*cap_per_scene*3 floats. */
+int amppi_sim_scan(int32_t n_scenes, const int32_t* kinds, const uint64_t* scene_seeds, int32_t frames,
+                   const amppi_state* poses, const uint64_t* frame_seeds, double r_max, int64_t cap_per_scene,
+                   float* xyz_out, int64_t* offsets_out, int32_t device);
+
+/* Measured FP32 FMA-pipe throughput of the device (TFLOP/s, FMA = 2 flops):
+ * the roofline denominator for the CUDA-core rollout kernel. */
+int amppi_probe_fp32_peak(int32_t device, double* tflops, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -129,6 +129,10 @@ EXPORTS = {
                                           ctypes.c_int32, c_int32_p]),
     "amppi_kernel_times_reset": (ctypes.c_int, [ctypes.c_void_p]),
     "amppi_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "amppi_sim_scan": (ctypes.c_int, [ctypes.c_int32, c_int32_p, c_uint64_p, ctypes.c_int32, ctypes.c_void_p,
+                                      c_uint64_p, ctypes.c_double, ctypes.c_int64, c_float_p, c_int64_p,
+                                      ctypes.c_int32]),
+    "amppi_probe_fp32_peak": (ctypes.c_int, [ctypes.c_int32, c_double_p, c_double_p]),
 }
 
 _lib = None

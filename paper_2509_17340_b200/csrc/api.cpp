@@ -348,6 +348,8 @@ int create_impl(amppi_ctx* ctx) {
   CK(cudaMemset(P.grid, 0, static_cast<size_t>(S) * sizeof(GridMeta)));
   CK(A.alloc(&p, static_cast<size_t>(S) * (kGridCells + 1) * sizeof(uint32_t)));
   P.grid_start = static_cast<uint32_t*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kGridCells * sizeof(uint4)));
+  P.grid_cell = static_cast<uint4*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kOccWords * sizeof(uint32_t)));
   P.grid_occ = static_cast<uint32_t*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 3 * sizeof(double)));
@@ -789,6 +791,7 @@ int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* 
 
 int amppi_kernel_times_reset(amppi_ctx* ctx) {
   if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (int rc = sync_and_collect(ctx); rc != AMPPI_OK) return rc;  // drop in-flight events too
   ctx->timer.totals.clear();
   return AMPPI_OK;
 }

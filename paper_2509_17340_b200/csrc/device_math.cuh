@@ -324,59 +324,101 @@ __device__ __forceinline__ R collision_term(R d, R scale, R slope, R dmin, R dma
   return R(0);
 }
 
-// Squared distance to the nearest filtered point among the 27 grid cells
-// around p; returns +inf when none.  Exact whenever the true nearest distance
-// is below the grid cell size h >= d_max.
-__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint32_t* __restrict__ start,
-                                                   const double* __restrict__ pts, V3<double> p) {
+// Collision-grid neighbourhood order: the query's own cell, then the 6 face,
+// 12 edge and 8 corner neighbours (closest first, so the branch-and-bound
+// below prunes early).
+__constant__ __device__ signed char kNbrOrder[27][3] = {
+    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
+    {-1, -1, 0}, {-1, 1, 0},  {1, -1, 0},  {1, 1, 0},   {-1, 0, -1}, {-1, 0, 1},  {1, 0, -1},
+    {1, 0, 1},   {0, -1, -1}, {0, -1, 1},  {0, 1, -1},  {0, 1, 1},   {-1, -1, -1}, {-1, -1, 1},
+    {-1, 1, -1}, {-1, 1, 1},  {1, -1, -1}, {1, -1, 1},  {1, 1, -1},  {1, 1, 1}};
+
+__device__ __forceinline__ bool occupancy_maybe_near(const GridMeta& g, const uint32_t* __restrict__ occ, int cx,
+                                                     int cy, int cz) {
+  if (cx < -1 || cy < -1 || cz < -1 || cx > g.dims[0] || cy > g.dims[1] || cz > g.dims[2]) return false;
+  const int oc = ((cx + 1) * (g.dims[1] + 2) + (cy + 1)) * (g.dims[2] + 2) + (cz + 1);
+  return (__ldg(occ + (oc >> 5)) >> (oc & 31)) & 1u;
+}
+
+// Squared distance to the nearest filtered point, exact whenever the true
+// nearest distance is below d_max (every such point lies in the 27 cells of
+// size h >= d_max around p).  Branch and bound over the cells' outward-
+// quantised point boxes: a cell is skipped when its box is farther than the
+// best distance so far or than d_max (its points cannot change the cost);
+// the scan stops once a point is closer than d_min (cost = C for any such d).
+// Returns +inf when no point is within reach.
+__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ cells,
+                                                   const uint32_t* __restrict__ occ, const double* __restrict__ pts,
+                                                   V3<double> p, double lim2, double stop2) {
   double best = __longlong_as_double(0x7ff0000000000000ll);
   if (g.dims[0] == 0) return best;
   const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
   const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
   const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
-  const int x0 = max(cx - 1, 0), x1 = min(cx + 1, g.dims[0] - 1);
-  const int y0 = max(cy - 1, 0), y1 = min(cy + 1, g.dims[1] - 1);
-  const int z0 = max(cz - 1, 0), z1 = min(cz + 1, g.dims[2] - 1);
-  for (int x = x0; x <= x1; ++x)
-    for (int y = y0; y <= y1; ++y) {
-      const int row = (x * g.dims[1] + y) * g.dims[2];
-      const uint32_t b = start[row + z0], e = start[row + z1 + 1];
-      for (uint32_t k = b; k < e; ++k) {
-        const V3<double> q{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]};
-        const double d2 = sqnorm(p - q);
-        best = d2 < best ? d2 : best;
-      }
+  if (!occupancy_maybe_near(g, occ, cx, cy, cz)) return best;
+  const double q = g.h * (1.0 / 255.0);
+  for (int o = 0; o < 27; ++o) {
+    const int x = cx + kNbrOrder[o][0], y = cy + kNbrOrder[o][1], z = cz + kNbrOrder[o][2];
+    if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
+    const uint4 rec = cells[(x * g.dims[1] + y) * g.dims[2] + z];
+    if (rec.y == 0) continue;
+    const double c0x = g.origin[0] + x * g.h, c0y = g.origin[1] + y * g.h, c0z = g.origin[2] + z * g.h;
+    const double gx = fmax(fmax(c0x + (rec.z & 255u) * q - p.x, p.x - (c0x + (rec.w & 255u) * q)), 0.0);
+    const double gy = fmax(fmax(c0y + ((rec.z >> 8) & 255u) * q - p.y, p.y - (c0y + ((rec.w >> 8) & 255u) * q)), 0.0);
+    const double gz =
+        fmax(fmax(c0z + ((rec.z >> 16) & 255u) * q - p.z, p.z - (c0z + ((rec.w >> 16) & 255u) * q)), 0.0);
+    const double bd2 = gx * gx + gy * gy + gz * gz;
+    if (bd2 > fmin(best, lim2) * (1.0 + 1e-12)) continue;
+    for (uint32_t k = rec.x; k < rec.x + rec.y; ++k) {
+      const V3<double> qq{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]};
+      const double d2 = sqnorm(p - qq);
+      best = d2 < best ? d2 : best;
     }
+    if (best < stop2) break;
+  }
   return best;
 }
 
-__device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint32_t* __restrict__ start,
+__device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4* __restrict__ cells,
                                                  const uint32_t* __restrict__ occ, const float4* __restrict__ pts,
-                                                 V3<float> p) {
+                                                 V3<float> p, float lim2, float stop2) {
   float best = __int_as_float(0x7f800000);
   if (g.dims[0] == 0) return best;
   const float fx = (p.x - g.origin_f[0]) * g.inv_h_f;
   const float fy = (p.y - g.origin_f[1]) * g.inv_h_f;
   const float fz = (p.z - g.origin_f[2]) * g.inv_h_f;
   const int cx = __float2int_rd(fx), cy = __float2int_rd(fy), cz = __float2int_rd(fz);
-  if (cx < -1 || cy < -1 || cz < -1 || cx > g.dims[0] || cy > g.dims[1] || cz > g.dims[2]) return best;
-  // dilated occupancy (cells -1..dims padded by one): skip empty neighbourhoods
-  const int ox = cx + 1, oy = cy + 1, oz = cz + 1;
-  const int oc = (ox * (g.dims[1] + 2) + oy) * (g.dims[2] + 2) + oz;
-  if (!((__ldg(occ + (oc >> 5)) >> (oc & 31)) & 1u)) return best;
-  const int x0 = max(cx - 1, 0), x1 = min(cx + 1, g.dims[0] - 1);
-  const int y0 = max(cy - 1, 0), y1 = min(cy + 1, g.dims[1] - 1);
-  const int z0 = max(cz - 1, 0), z1 = min(cz + 1, g.dims[2] - 1);
-  for (int x = x0; x <= x1; ++x)
-    for (int y = y0; y <= y1; ++y) {
-      const int row = (x * g.dims[1] + y) * g.dims[2];
-      const uint32_t b = __ldg(start + row + z0), e = __ldg(start + row + z1 + 1);
-      for (uint32_t k = b; k < e; ++k) {
-        const float4 q = __ldg(pts + k);
-        const float dx = p.x - q.x, dy = p.y - q.y, dz = p.z - q.z;
-        best = fminf(best, dx * dx + dy * dy + dz * dz);
-      }
+  if (!occupancy_maybe_near(g, occ, cx, cy, cz)) return best;
+  // p relative to the query cell's corner, in cells (box quanta: 1/255 cell)
+  const float rx = (fx - static_cast<float>(cx)) * 255.f, ry = (fy - static_cast<float>(cy)) * 255.f,
+              rz = (fz - static_cast<float>(cz)) * 255.f;
+  const float q2 = g.h_f * g.h_f * (1.f / (255.f * 255.f));
+  const float lim = lim2 / q2;  // thresholds in quanta^2
+  for (int o = 0; o < 27; ++o) {
+    const int ox = kNbrOrder[o][0], oy = kNbrOrder[o][1], oz = kNbrOrder[o][2];
+    const int x = cx + ox, y = cy + oy, z = cz + oz;
+    if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
+    const uint4 rec = __ldg(cells + (x * g.dims[1] + y) * g.dims[2] + z);
+    if (rec.y == 0) continue;
+    // box in quanta relative to the query cell's corner
+    const float bx0 = static_cast<float>(ox * 255 + static_cast<int>(rec.z & 255u)) - 1.f;
+    const float bx1 = static_cast<float>(ox * 255 + static_cast<int>(rec.w & 255u)) + 1.f;
+    const float by0 = static_cast<float>(oy * 255 + static_cast<int>((rec.z >> 8) & 255u)) - 1.f;
+    const float by1 = static_cast<float>(oy * 255 + static_cast<int>((rec.w >> 8) & 255u)) + 1.f;
+    const float bz0 = static_cast<float>(oz * 255 + static_cast<int>((rec.z >> 16) & 255u)) - 1.f;
+    const float bz1 = static_cast<float>(oz * 255 + static_cast<int>((rec.w >> 16) & 255u)) + 1.f;
+    const float gx = fmaxf(fmaxf(bx0 - rx, rx - bx1), 0.f);
+    const float gy = fmaxf(fmaxf(by0 - ry, ry - by1), 0.f);
+    const float gz = fmaxf(fmaxf(bz0 - rz, rz - bz1), 0.f);
+    const float bd2 = gx * gx + gy * gy + gz * gz;
+    if (bd2 >= fminf(best / q2, lim)) continue;
+    for (uint32_t k = rec.x; k < rec.x + rec.y; ++k) {
+      const float4 qq = __ldg(pts + k);
+      const float dx = p.x - qq.x, dy = p.y - qq.y, dz = p.z - qq.z;
+      best = fminf(best, dx * dx + dy * dy + dz * dz);
     }
+    if (best < stop2) break;
+  }
   return best;
 }
 

@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
         m.dims[a] = d < 1 ? 1 : (d > kGridAxis ? kGridAxis : d);
       }
       m.inv_h_f = static_cast<float>(m.inv_h);
+      m.h_f = static_cast<float>(m.h);
     }
     sm.meta = m;
     P.grid[s] = m;
@@ -368,6 +369,37 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
     gp64[3 * slot + 1] = pw.y;
     gp64[3 * slot + 2] = pw.z;
     gp32[slot] = make_float4(static_cast<float>(pw.x), static_cast<float>(pw.y), static_cast<float>(pw.z), 0.f);
+  }
+  __syncthreads();
+  // 5. per-cell records: point range + point bounding box relative to the
+  //    cell corner, quantised outward to h/255 (one extra quantum of slack)
+  uint4* __restrict__ gcell = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  const double quanta = 255.0 * meta.inv_h;
+  for (int c = tid; c < ncell; c += blockDim.x) {
+    const uint32_t b = gstart[c], e = gstart[c + 1];
+    if (b == e) {
+      gcell[c] = make_uint4(b, 0u, 0u, 0u);
+      continue;
+    }
+    const int cz = c % meta.dims[2], cy = (c / meta.dims[2]) % meta.dims[1], cx = c / (meta.dims[2] * meta.dims[1]);
+    const int cc[3] = {cx, cy, cz};
+    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (uint32_t k = b; k < e; ++k)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = fmin(lo[a], gp64[3 * k + a]);
+        hi[a] = fmax(hi[a], gp64[3 * k + a]);
+      }
+    uint32_t ql = 0u, qh = 0u;
+    for (int a = 0; a < 3; ++a) {
+      const double corner = meta.origin[a] + cc[a] * meta.h;
+      double fl = floor((lo[a] - corner) * quanta) - 1.0;
+      double fh = ceil((hi[a] - corner) * quanta) + 1.0;
+      fl = fl < 0.0 ? 0.0 : (fl > 255.0 ? 255.0 : fl);
+      fh = fh < 0.0 ? 0.0 : (fh > 255.0 ? 255.0 : fh);
+      ql |= static_cast<uint32_t>(fl) << (8 * a);
+      qh |= static_cast<uint32_t>(fh) << (8 * a);
+    }
+    gcell[c] = make_uint4(b, e - b, ql, qh);
   }
 }
 

@@ -5,9 +5,10 @@
 // (sample_rollout_perturbations + rollout_into + stage1_cost,
 // mppi.cpp:16-61, costs.hpp:150-162).  The instance's nominal sequence and
 // guide table are staged once per CTA in shared memory; the collision query
-// reads the scene's grid (dilated occupancy bit first, then <= 9 contiguous
-// cell ranges).  Its FP32 costs only select the softmin support; k_update
-// re-evaluates that support in FP64.
+// reads the scene's grid (dilated occupancy bit, then branch and bound over
+// the 27 neighbour cells' point boxes).  Its FP32 costs only select the
+// softmin support; k_refine re-evaluates that support in FP64 (DESIGN.md
+// "Precision").
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -19,10 +20,19 @@ namespace {
 
 constexpr int kMaxN = 64;
 
-__global__ void __launch_bounds__(128) k_stage1_f32(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter) {
+// mode 0: every sample, no bound.  mode 1: samples [0, k1) without bound.
+// mode 2: samples [k1, K) aborted once their partial cost exceeds
+// U + 2 window, U = min cost of samples [0, k1) -- an actual sample cost, so
+// the instance minimum rho <= U and no softmin-support member (cost <= rho +
+// 64 lambda) can abort.  Aborted samples report FLT_MAX.
+__global__ void __launch_bounds__(128) k_stage1_f32(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter,
+                                                    int mode, int k1) {
   __shared__ float s_unom[4 * kMaxN];
   __shared__ float4 s_guide[kMaxN];
-  const int tiles = (cfg.K + blockDim.x - 1) / blockDim.x;
+  __shared__ float s_bound;
+  const int k_lo = mode == 2 ? k1 : 0;
+  const int k_n = mode == 0 ? cfg.K : (mode == 1 ? k1 : cfg.K - k1);
+  const int tiles = (k_n + blockDim.x - 1) / blockDim.x;
   int b = blockIdx.x;
   const int tile = b % tiles;
   b /= tiles;
@@ -32,9 +42,19 @@ __global__ void __launch_bounds__(128) k_stage1_f32(BatchIn in, Perception P, Pl
   const int N = cfg.N;
   for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
   for (int i = threadIdx.x; i < N; i += blockDim.x) s_guide[i] = pl.guide32[smi * N + i];
+  if (threadIdx.x < 32) {
+    float u = __int_as_float(0x7f800000);
+    if (mode == 2)
+      for (int k = threadIdx.x; k < k1; k += 32) u = fminf(u, pl.cost32[smi * cfg.K + k]);
+    for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
+    if (threadIdx.x == 0) {
+      const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
+      s_bound = (mode == 2 && u < 3.0e38f) ? u + 2.0f * window : __int_as_float(0x7f800000);
+    }
+  }
   __syncthreads();
-  const int k = tile * blockDim.x + threadIdx.x;
-  if (k >= cfg.K) return;
+  const int k = k_lo + tile * blockDim.x + threadIdx.x;
+  if (k >= k_lo + k_n) return;
   float* out = pl.cost32 + smi * cfg.K + k;
   if (!pl.alive[smi]) {
     *out = __int_as_float(0x7f800000);
@@ -57,10 +77,15 @@ __global__ void __launch_bounds__(128) k_stage1_f32(BatchIn in, Perception P, Pl
   env.cdmin = static_cast<float>(cfg.col_d_min);
   env.cdmax = static_cast<float>(cfg.col_d_max);
   env.grid = P.grid[s];
-  env.gstart = P.grid_start + static_cast<int64_t>(s) * (kGridCells + 1);
+  env.gcells = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
   env.gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
   env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   env.has_guide = true;
+  env.abort_above = s_bound;
+  env.wq_track = static_cast<float>(cfg.q_track);
+  env.wq_vnorm = static_cast<float>(cfg.q_vnorm);
+  env.wq_c = static_cast<float>(cfg.q_c);
+  env.wq_cd = static_cast<float>(cfg.q_c_delta);
 
   const double* xs = in.states + 10 * s;
   St<float> x0;
@@ -79,9 +104,9 @@ __global__ void __launch_bounds__(128) k_stage1_f32(BatchIn in, Perception P, Pl
                       static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
     cs = rollout_costs(x0, env, pr);
   }
-  *out = cs.valid ? stage1_total(cs, static_cast<float>(cfg.q_track), static_cast<float>(cfg.q_vnorm),
-                                 static_cast<float>(cfg.q_c), static_cast<float>(cfg.q_c_delta))
-                  : __int_as_float(0x7f800000);
+  *out = cs.aborted ? 3.4028234663852886e38f
+                    : cs.valid ? stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd)
+                               : __int_as_float(0x7f800000);
 }
 
 }  // namespace
@@ -89,12 +114,23 @@ __global__ void __launch_bounds__(128) k_stage1_f32(BatchIn in, Perception P, Pl
 cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
                               cudaStream_t st, KernelTimer* timer) {
   const int64_t total = static_cast<int64_t>(in.S) * cfg.M * cfg.K;
-  // latency mode (few rollouts): spread warps over SMs; throughput mode: 128
-  const int threads = total < 148 * 128 ? 32 : 128;
-  const int tiles = (cfg.K + threads - 1) / threads;
+  const int64_t SM = static_cast<int64_t>(in.S) * cfg.M;
+  if (total < 148 * 128 * 4 || cfg.K <= 64) {
+    // latency mode (few rollouts): one pass, warps spread over the SMs
+    const int threads = total < 148 * 128 ? 32 : 128;
+    const int tiles = (cfg.K + threads - 1) / threads;
+    TimedRegion t(timer, "k_stage1_f32", st);
+    k_stage1_f32<<<static_cast<unsigned>(SM * tiles), threads, 0, st>>>(in, P, pl, cfg, iter, 0, 0);
+    return cudaGetLastError();
+  }
+  const int k1 = 32;
+  {
+    TimedRegion t(timer, "k_stage1_f32_bound", st);
+    k_stage1_f32<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
+  }
+  const int tiles = (cfg.K - k1 + 127) / 128;
   TimedRegion t(timer, "k_stage1_f32", st);
-  k_stage1_f32<<<static_cast<unsigned>(static_cast<int64_t>(in.S) * cfg.M * tiles), threads, 0, st>>>(in, P, pl, cfg,
-                                                                                                       iter);
+  k_stage1_f32<<<static_cast<unsigned>(SM * tiles), 128, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
   return cudaGetLastError();
 }
 

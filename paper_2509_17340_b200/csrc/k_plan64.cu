@@ -54,9 +54,18 @@ __device__ __forceinline__ int el_cell_exact(double el) {
   return j < 0 ? 0 : (j > kEl - 1 ? kEl - 1 : j);
 }
 
-__device__ __forceinline__ V3<double> direction_from_angles(double az, double el) {
-  const double ce = crm::cos_cr(el);
-  return {ce * crm::cos_cr(az), ce * crm::sin_cr(az), crm::sin_cr(el)};
+__device__ __forceinline__ V3<double> direction_from_angles(double az, double el, bool cr) {
+  if (cr) {
+    const double ce = crm::cos_cr(el);
+    return {ce * crm::cos_cr(az), ce * crm::sin_cr(az), crm::sin_cr(el)};
+  }
+  const double ce = cos(el);
+  return {ce * cos(az), ce * sin(az), sin(el)};
+}
+
+__device__ __forceinline__ bool near_integer(double v) {
+  const double fl = floor(v);
+  return (v - fl) < 1e-9 || ((fl + 1.0) - v) < 1e-9;
 }
 
 // ---------------------------------------------------------------------------
@@ -82,29 +91,39 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
   if (goal_dist > cfg.min_anchor_distance) {
     const double lookahead = dmin(cfg.lookahead, goal_dist);
     terminal_speed = dmin(cfg.terminal_speed, goal_dist / horizon_s);
-    // sample_initial_endpoints, index m = v*m_h + h
+    // sample_initial_endpoints (index m = v*m_h + h) + refine_endpoints.
+    // Pass 0 uses CUDA's libm (<= 2 ulp); if either refined-direction
+    // quotient lands within 1e-9 of a cell boundary the anchor is recomputed
+    // with correctly-rounded atan2/sin/cos (pass 1) so its cell equals the
+    // glibc-based reference's.
     const int v = m / cfg.m_h, h = m % cfg.m_h;
     const V3<double> tg = goal_p - x.p;
-    const double az0 = crm::atan2_cr(tg.y, tg.x);
-    const double el0 = crm::atan2_cr(tg.z, sqrt(tg.x * tg.x + tg.y * tg.y));
     const double spacing = cfg.spacing_deg * kPiD / 180.0;
-    const double el_off = (static_cast<double>(v) - 0.5 * static_cast<double>(cfg.m_v - 1)) * spacing;
-    const double el = clampv(el0 + el_off, -kMaxElevation, kMaxElevation);
-    const double az = az0 + (static_cast<double>(h) - 0.5 * static_cast<double>(cfg.m_h - 1)) * spacing;
-    initial = x.p + lookahead * direction_from_angles(az, el);
-    // refine_endpoints
-    V3<double> dir_world = initial - pose_p;
-    if (sqnorm(dir_world) < 1e-18) dir_world = {1.0, 0.0, 0.0};
-    const double n2 = sqnorm(dir_world);
-    if (n2 > 0.0) {
-      const double n = sqrt(n2);
-      dir_world = {dir_world.x / n, dir_world.y / n, dir_world.z / n};
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool cr = pass == 1;
+      auto t_atan2 = [cr](double yy, double xx) { return cr ? crm::atan2_cr(yy, xx) : atan2(yy, xx); };
+      const double az0 = t_atan2(tg.y, tg.x);
+      const double el0 = t_atan2(tg.z, sqrt(tg.x * tg.x + tg.y * tg.y));
+      const double el_off = (static_cast<double>(v) - 0.5 * static_cast<double>(cfg.m_v - 1)) * spacing;
+      const double el = clampv(el0 + el_off, -kMaxElevation, kMaxElevation);
+      const double az = az0 + (static_cast<double>(h) - 0.5 * static_cast<double>(cfg.m_h - 1)) * spacing;
+      initial = x.p + lookahead * direction_from_angles(az, el, cr);
+      V3<double> dir_world = initial - pose_p;
+      if (sqnorm(dir_world) < 1e-18) dir_world = {1.0, 0.0, 0.0};
+      const double n2 = sqnorm(dir_world);
+      if (n2 > 0.0) {
+        const double n = sqrt(n2);
+        dir_world = {dir_world.x / n, dir_world.y / n, dir_world.z / n};
+      }
+      const V3<double> db = mat_t_vec(body_to_world, dir_world);
+      const double azb = t_atan2(db.y, db.x);
+      const double elb = t_atan2(db.z, sqrt(db.x * db.x + db.y * db.y));
+      const double qa = (azb + kPiD) / kAzStep, qe = (elb + kHalfPi) / kAzStep;
+      if (!cr && (near_integer(qa) || near_integer(qe))) continue;
+      ci = az_cell_exact(azb) / kPool;
+      cj = el_cell_exact(elb) / kPool;
+      break;
     }
-    const V3<double> db = mat_t_vec(body_to_world, dir_world);
-    const double azb = crm::atan2_cr(db.y, db.x);
-    const double elb = crm::atan2_cr(db.z, sqrt(db.x * db.x + db.y * db.y));
-    ci = az_cell_exact(azb) / kPool;
-    cj = el_cell_exact(elb) / kPool;
     const int64_t f = static_cast<int64_t>(s) * kCoarse + ci * kCEl + cj;
     safe_range = P.safe_range[f];
     safe_dir = mat_vec(body_to_world, V3<double>{P.safe_dir[3 * f], P.safe_dir[3 * f + 1], P.safe_dir[3 * f + 2]});
@@ -227,9 +246,11 @@ __device__ __forceinline__ RolloutEnv<double> make_env64(const BatchIn& in, cons
   e.cdmin = cfg.col_d_min;
   e.cdmax = cfg.col_d_max;
   e.grid = P.grid[s];
-  e.gstart = P.grid_start + static_cast<int64_t>(s) * (kGridCells + 1);
+  e.gcells = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  e.gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
   e.gpts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
   e.has_guide = true;
+  e.abort_above = __longlong_as_double(0x7ff0000000000000ll);
   return e;
 }
 
@@ -277,9 +298,17 @@ __global__ void __launch_bounds__(128) k_stage1_f64(BatchIn in, Perception P, Pl
 }
 
 // ---------------------------------------------------------------------------
-// K4b: update + stage II + selection
+// K4b: MPPI update (compute_weights + update_nominal, mppi.cpp:70-101) as
+//   k_support  one CTA per instance: screening minimum, softmin support
+//              (samples whose weight can exceed e^-64 of the maximum) in k order
+//   k_refine   one warp per instance: exact FP64 stage-I cost of the support
+//              (FP32 screening only)
+//   k_nominal  one CTA per instance: rho / weights / eta / ess in k order,
+//              weighted perturbation sum, clamp
+// K5: k_stage2 one thread per instance (noise-free re-rollout, stage-II cost,
+//     breakdown); k_select one thread per scene (first minimum wins).
 // ---------------------------------------------------------------------------
-constexpr int kUpdateThreads = 256;
+constexpr int kSupportThreads = 128;
 
 struct UpdateScratch {  // global, per (scene, instance): [K] each
   uint32_t* cand_k;
@@ -287,211 +316,208 @@ struct UpdateScratch {  // global, per (scene, instance): [K] each
   double* cand_w;
 };
 
-__device__ __forceinline__ double warp_min(double v) {
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+__device__ __forceinline__ double load_cost(const Plan& pl, int precision, int64_t i) {
+  return precision == 32 ? static_cast<double>(pl.cost32[i]) : pl.cost64[i];
 }
 
-__global__ void __launch_bounds__(kUpdateThreads) k_update(BatchIn in, Perception P, Plan pl, DevConfig cfg,
-                                                           UpdateScratch us, int iter, int precision, int last_iter) {
-  __shared__ double s_unom[4 * 64];
-  __shared__ double s_red[kUpdateThreads / 32];
-  __shared__ uint32_t s_cnt[kUpdateThreads / 32 + 1];
-  __shared__ double s_rho_screen, s_rho, s_eta;
-  __shared__ uint32_t s_ncand;
-  __shared__ int s_dead;
-  __shared__ bool s_last;
-
-  const int m = blockIdx.x % cfg.M;
-  const int s = blockIdx.x / cfg.M;
-  const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
-  const int K = cfg.K, N = cfg.N;
+__global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig cfg, UpdateScratch us, int precision) {
+  __shared__ double s_red[kSupportThreads / 32];
+  __shared__ uint32_t s_cnt[kSupportThreads / 32];
+  __shared__ double s_rho;
+  const int64_t smi = blockIdx.x;
+  const int K = cfg.K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-  uint32_t* cand_k = us.cand_k + smi * K;
-  double* cand_s = us.cand_s + smi * K;
-  double* cand_w = us.cand_w + smi * K;
-
-  for (int i = tid; i < 4 * N; i += blockDim.x) s_unom[i] = pl.nominal[smi * N * 4 + i];
-  const bool alive = pl.alive[smi] != 0;
-
-  if (alive) {
-    // 1. screening minimum over finite costs
-    double lmin = kInf;
-    for (int k = tid; k < K; k += blockDim.x) {
-      const double c = precision == 32 ? static_cast<double>(pl.cost32[smi * K + k]) : pl.cost64[smi * K + k];
-      if (isfinite(c)) lmin = fmin(lmin, c);
-    }
-    lmin = warp_min(lmin);
-    if (lane == 0) s_red[warp] = lmin;
-    __syncthreads();
-    if (tid == 0) {
-      double r = kInf;
-      for (int w = 0; w < kUpdateThreads / 32; ++w) r = fmin(r, s_red[w]);
-      s_rho_screen = r;
-      s_dead = !isfinite(r);
-    }
-    __syncthreads();
-  } else {
-    if (tid == 0) s_dead = 1;
-    __syncthreads();
+  if (!pl.alive[smi]) {
+    if (tid == 0) pl.n_support[smi] = 0;
+    return;
   }
-
-  if (!s_dead) {
-    // 2. softmin support in k order: every sample whose weight can exceed
-    //    e^-64 relative to the minimum (FP32 screening adds a safety margin)
-    const double rho_s = s_rho_screen;
-    const double window = precision == 32 ? 64.0 * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
-    const int per = (K + blockDim.x - 1) / blockDim.x;
-    const int k0 = min(tid * per, K), k1 = min(k0 + per, K);
-    uint32_t mine = 0;
-    for (int k = k0; k < k1; ++k) {
-      const double c = precision == 32 ? static_cast<double>(pl.cost32[smi * K + k]) : pl.cost64[smi * K + k];
-      mine += (isfinite(c) && c - rho_s <= window);
-    }
-    // block exclusive scan
-    uint32_t x = mine;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_cnt[warp] = x;
-    __syncthreads();
+  const int64_t base = smi * K;
+  double lmin = kInf;
+  for (int k = tid; k < K; k += blockDim.x) {
+    const double c = load_cost(pl, precision, base + k);
+    if (isfinite(c)) lmin = fmin(lmin, c);
+  }
+  for (int o = 16; o > 0; o >>= 1) lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+  if (lane == 0) s_red[warp] = lmin;
+  __syncthreads();
+  if (tid == 0) {
+    double r = kInf;
+    for (int w = 0; w < kSupportThreads / 32; ++w) r = fmin(r, s_red[w]);
+    s_rho = r;
+  }
+  __syncthreads();
+  const double rho_s = s_rho;
+  if (!isfinite(rho_s)) {  // "no valid rollout": the instance dies
     if (tid == 0) {
-      uint32_t run = 0;
-      for (int w = 0; w < kUpdateThreads / 32; ++w) {
-        const uint32_t t = s_cnt[w];
-        s_cnt[w] = run;
-        run += t;
-      }
-      s_ncand = run;
+      pl.alive[smi] = 0;
+      pl.n_support[smi] = 0;
     }
-    __syncthreads();
-    uint32_t pos = s_cnt[warp] + x - mine;
-    for (int k = k0; k < k1; ++k) {
-      const double c = precision == 32 ? static_cast<double>(pl.cost32[smi * K + k]) : pl.cost64[smi * K + k];
-      if (isfinite(c) && c - rho_s <= window) {
-        cand_k[pos] = static_cast<uint32_t>(k);
-        cand_s[pos] = c;
-        ++pos;
-      }
+    return;
+  }
+  const double window = precision == 32 ? 64.0 * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
+  const int per = (K + blockDim.x - 1) / blockDim.x;
+  const int k0 = min(tid * per, K), k1 = min(k0 + per, K);
+  uint32_t mine = 0;
+  for (int k = k0; k < k1; ++k) {
+    const double c = load_cost(pl, precision, base + k);
+    mine += (isfinite(c) && c - rho_s <= window);
+  }
+  uint32_t x = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_cnt[warp] = x;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int w = 0; w < kSupportThreads / 32; ++w) {
+      const uint32_t t = s_cnt[w];
+      s_cnt[w] = run;
+      run += t;
     }
-    __syncthreads();
-    const uint32_t ncand = s_ncand;
-    const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+    pl.n_support[smi] = run;
+  }
+  __syncthreads();
+  uint32_t pos = s_cnt[warp] + x - mine;
+  for (int k = k0; k < k1; ++k) {
+    const double c = load_cost(pl, precision, base + k);
+    if (isfinite(c) && c - rho_s <= window) {
+      us.cand_k[base + pos] = static_cast<uint32_t>(k);
+      us.cand_s[base + pos] = c;
+      ++pos;
+    }
+  }
+}
 
-    // 3. exact FP64 stage-I cost of the support (FP32 screening only)
-    if (precision == 32) {
-      const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, s_unom);
-      const St<double> x0 = load_state(in.states + 10 * s);
-      for (uint32_t c = tid; c < ncand; c += blockDim.x) {
-        const int k = static_cast<int>(cand_k[c]);
-        CostSums<double> cs;
-        if (in.injected) {
-          cs = rollout_costs(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)});
-        } else {
-          const PertRngD pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
-                            cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
-          cs = rollout_costs(x0, env, pr);
-        }
-        cand_s[c] = cs.valid ? stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta) : kInf;
-      }
-      __syncthreads();
+__global__ void __launch_bounds__(32) k_refine(BatchIn in, Perception P, Plan pl, DevConfig cfg, UpdateScratch us,
+                                               int iter) {
+  __shared__ double s_unom[4 * 64];
+  const int64_t smi = blockIdx.x;
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  const uint32_t n = pl.n_support[smi];
+  if (n == 0) return;
+  const int N = cfg.N;
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) s_unom[i] = pl.nominal[smi * N * 4 + i];
+  __syncwarp();
+  const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, s_unom);
+  const St<double> x0 = load_state(in.states + 10 * s);
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  const int64_t base = smi * cfg.K;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const int k = static_cast<int>(us.cand_k[base + c]);
+    CostSums<double> cs;
+    if (in.injected) {
+      cs = rollout_costs(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)});
+    } else {
+      const PertRngD pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                        cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+      cs = rollout_costs(x0, env, pr);
     }
+    us.cand_s[base + c] = cs.valid ? stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta) : kInf;
+  }
+}
 
-    // 4. rho, weights, eta, ess in k order (compute_weights, mppi.cpp:70-87)
-    if (tid == 0) {
-      double rho = kInf;
-      for (uint32_t c = 0; c < ncand; ++c)
-        if (isfinite(cand_s[c])) rho = dmin(rho, cand_s[c]);
+__global__ void __launch_bounds__(128) k_nominal(BatchIn in, Plan pl, DevConfig cfg, UpdateScratch us, int iter) {
+  __shared__ int s_dead;
+  const int64_t smi = blockIdx.x;
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  const uint32_t n = pl.n_support[smi];
+  if (n == 0) return;  // dead (or died this iteration)
+  const int N = cfg.N, tid = threadIdx.x;
+  const int64_t base = smi * cfg.K;
+  const uint32_t* cand_k = us.cand_k + base;
+  const double* cand_s = us.cand_s + base;
+  double* cand_w = us.cand_w + base;
+  if (tid == 0) {
+    // compute_weights (mppi.cpp:70-87): rho, e_k, eta, w_k = e_k / eta, ess
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double rho = kInf;
+    for (uint32_t c = 0; c < n; ++c)
+      if (isfinite(cand_s[c])) rho = dmin(rho, cand_s[c]);
+    s_dead = !isfinite(rho);
+    if (!s_dead) {
       double eta = 0.0;
-      for (uint32_t c = 0; c < ncand; ++c) {
+      for (uint32_t c = 0; c < n; ++c) {
         const double e = isfinite(cand_s[c]) ? exp(-(cand_s[c] - rho) / cfg.lambda) : 0.0;
         cand_w[c] = e;
         eta += e;
       }
       double w2 = 0.0;
-      for (uint32_t c = 0; c < ncand; ++c) {
+      for (uint32_t c = 0; c < n; ++c) {
         const double w = cand_w[c] / eta;
         cand_w[c] = w;
         w2 += w * w;
       }
-      s_rho = rho;
-      s_eta = eta;
-      if (isfinite(rho)) {
-        pl.stage1[smi] = rho;
-        pl.ess[smi] = w2 > 0.0 ? 1.0 / w2 : 0.0;
+      pl.stage1[smi] = rho;
+      pl.ess[smi] = w2 > 0.0 ? 1.0 / w2 : 0.0;
+    } else {
+      pl.alive[smi] = 0;
+    }
+  }
+  __syncthreads();
+  if (s_dead) return;
+  // update_nominal (mppi.cpp:89-101): deltas regenerated from the counter RNG
+  // and clamped against u_j exactly as rollout_into rewrote them
+  const Dyn<double> dy = make_dyn<double>(cfg);
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  double* nom = pl.nominal + smi * N * 4;
+  for (int jc = tid; jc < 4 * N; jc += blockDim.x) {
+    const int c = jc & 3;
+    const double u = nom[jc];
+    const double lo = c == 0 ? dy.tmin : (c == 3 ? -dy.wz : -dy.wxy);
+    const double hi = c == 0 ? dy.tmax : (c == 3 ? dy.wz : dy.wxy);
+    double du = 0.0;
+    for (uint32_t ci = 0; ci < n; ++ci) {
+      const double w = cand_w[ci];
+      if (w == 0.0) continue;  // 0 * delta adds exactly nothing
+      const int k = static_cast<int>(cand_k[ci]);
+      double draw;
+      if (in.injected) {
+        draw = injected_row(in, cfg, s, iter, m, k)[jc];
       } else {
-        s_dead = 1;  // "no valid rollout" after exact re-evaluation
-        pl.alive[smi] = 0;
+        const uint64_t key = stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
+        double n0, n1;
+        normal_pair(key, static_cast<uint32_t>(jc >> 1), n0, n1);
+        draw = cfg.sigma[c] * ((jc & 1) ? n1 : n0);
       }
-      pl.n_support[smi] = ncand;
+      const double applied = clampv(u + draw, lo, hi) - u;
+      du = du + w * applied;
     }
-    __syncthreads();
-
-    // 5. u_j <- clamp(u_j + sum_k w_k delta_k[j]) (update_nominal, mppi.cpp:89-101),
-    //    deltas regenerated from the counter RNG and clamped against u_j
-    const Dyn<double> dy = make_dyn<double>(cfg);
-    for (int jc = tid; jc < 4 * N && !s_dead; jc += blockDim.x) {
-      const int j = jc >> 2, c = jc & 3;
-      const double u = s_unom[jc];
-      const double lo = c == 0 ? dy.tmin : (c == 3 ? -dy.wz : -dy.wxy);
-      const double hi = c == 0 ? dy.tmax : (c == 3 ? dy.wz : dy.wxy);
-      double du = 0.0;
-      for (uint32_t ci = 0; ci < ncand; ++ci) {
-        const double w = cand_w[ci];
-        if (w == 0.0) continue;
-        const int k = static_cast<int>(cand_k[ci]);
-        double draw;
-        if (in.injected) {
-          draw = injected_row(in, cfg, s, iter, m, k)[jc];
-        } else {
-          const uint64_t key = stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
-          double n0, n1;
-          normal_pair(key, static_cast<uint32_t>(jc >> 1), n0, n1);
-          draw = cfg.sigma[c] * ((jc & 1) ? n1 : n0);
-        }
-        const double applied = clampv(u + draw, lo, hi) - u;
-        du = du + w * applied;
-      }
-      pl.nominal[smi * N * 4 + jc] = clampv(u + du, lo, hi);
-    }
-  } else if (alive) {
-    if (tid == 0) pl.alive[smi] = 0;  // no valid rollout: the instance dies
+    nom[jc] = clampv(u + du, lo, hi);
   }
-  __syncthreads();
+}
 
-  if (!last_iter) return;
-
-  // 6. stage II (ensemble.cpp:132-149): noise-free re-rollout, goal + collision
-  if (tid == 0) {
-    double st2 = kInf;
-    bool valid = false;
-    double bd[5] = {0, 0, 0, 0, 0};
-    if (!s_dead) {
-      const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * N * 4);
-      const CostSums<double> cs = rollout_costs(load_state(in.states + 10 * s), env, PertZero<double>{});
-      if (cs.valid) {
-        st2 = cs.goal + cs.col;
-        valid = isfinite(st2);
-        bd[0] = cfg.q_track * cs.trk;
-        bd[1] = cfg.q_vnorm * cs.vn;
-        bd[2] = cfg.q_c * cs.mag + cfg.q_c_delta * cs.rate;
-        bd[3] = cs.goal;
-        bd[4] = cs.col;
-      }
+__global__ void __launch_bounds__(64) k_stage2(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+  const int64_t smi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  double st2 = __longlong_as_double(0x7ff0000000000000ll);
+  bool valid = false;
+  double bd[5] = {0, 0, 0, 0, 0};
+  if (pl.alive[smi]) {
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    const CostSums<double> cs = rollout_costs(load_state(in.states + 10 * s), env, PertZero<double>{});
+    if (cs.valid) {
+      st2 = cs.goal + cs.col;  // stage2_cost (costs.hpp:139-147)
+      valid = isfinite(st2);
+      bd[0] = cfg.q_track * cs.trk;
+      bd[1] = cfg.q_vnorm * cs.vn;
+      bd[2] = cfg.q_c * cs.mag + cfg.q_c_delta * cs.rate;
+      bd[3] = cs.goal;
+      bd[4] = cs.col;
     }
-    pl.stage2[smi] = st2;
-    pl.valid[smi] = valid ? 1 : 0;
-    for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
-    __threadfence();
-    const int arrived = atomicAdd(pl.done + s, 1);
-    s_last = arrived == cfg.M - 1;
   }
-  __syncthreads();
-  if (!s_last || tid != 0) return;
-  __threadfence();
-  // 7. selection: first minimum stage-2 among valid instances
+  pl.stage2[smi] = st2;
+  pl.valid[smi] = valid ? 1 : 0;
+  for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
+}
+
+__global__ void k_select(Plan pl, DevConfig cfg, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
   int winner = -1;
   const int64_t base = static_cast<int64_t>(s) * cfg.M;
   for (int mm = 0; mm < cfg.M; ++mm) {
@@ -502,13 +528,12 @@ __global__ void __launch_bounds__(kUpdateThreads) k_update(BatchIn in, Perceptio
   pl.status[s] = winner < 0 ? 1 : 0;
   if (winner >= 0) {
     const Dyn<double> dy = make_dyn<double>(cfg);
-    const double* u = pl.nominal + (base + winner) * N * 4;
+    const double* u = pl.nominal + (base + winner) * cfg.N * 4;
     pl.control[4 * s] = clampv(u[0], dy.tmin, dy.tmax);
     pl.control[4 * s + 1] = clampv(u[1], -dy.wxy, dy.wxy);
     pl.control[4 * s + 2] = clampv(u[2], -dy.wxy, dy.wxy);
     pl.control[4 * s + 3] = clampv(u[3], -dy.wz, dy.wz);
   }
-  pl.done[s] = 0;
 }
 
 // Winner re-rollout states/controls (PlanResult::winner_rollout) on request.
@@ -567,8 +592,26 @@ cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan&
       TimedRegion t(timer, "k_stage1_f64", st);
       k_stage1_f64<<<SM * tiles, threads, 4 * cfg.N * sizeof(double), st>>>(in, P, pl, cfg, iter);
     }
-    TimedRegion t(timer, "k_update", st);
-    k_update<<<SM, kUpdateThreads, 0, st>>>(in, P, pl, cfg, us, iter, precision, iter + 1 == cfg.iterations);
+    {
+      TimedRegion t(timer, "k_support", st);
+      k_support<<<SM, kSupportThreads, 0, st>>>(pl, cfg, us, precision);
+    }
+    if (precision == 32) {
+      TimedRegion t(timer, "k_refine", st);
+      k_refine<<<SM, 32, 0, st>>>(in, P, pl, cfg, us, iter);
+    }
+    {
+      TimedRegion t(timer, "k_nominal", st);
+      k_nominal<<<SM, 128, 0, st>>>(in, pl, cfg, us, iter);
+    }
+  }
+  {
+    TimedRegion t(timer, "k_stage2", st);
+    k_stage2<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+  }
+  {
+    TimedRegion t(timer, "k_select", st);
+    k_select<<<(in.S + 127) / 128, 128, 0, st>>>(pl, cfg, in.S);
   }
   if (want_winner_rollout) {
     TimedRegion t(timer, "k_winner_rollout", st);

@@ -40,7 +40,7 @@ struct GridMeta {
   double origin[3];
   double h, inv_h;
   float origin_f[3];
-  float inv_h_f;
+  float inv_h_f, h_f;
   int dims[3];
   int n_points;
 };
@@ -87,7 +87,9 @@ struct Perception {
   double* safe_point;          // [S*600]
   int32_t* n_filtered;         // [S]
   GridMeta* grid;              // [S]
-  uint32_t* grid_start;        // [S*(kGridCells+1)]
+  uint32_t* grid_start;        // [S*(kGridCells+1)] (build scratch)
+  uint4* grid_cell;            // [S*kGridCells] {start, count, box lo, box hi}: points of the
+                               // cell and their bounding box quantised outward to h/255
   uint32_t* grid_occ;          // [S*kOccWords]
   double* grid_pts64;          // [S*7200*3] sorted by grid cell
   float4* grid_pts32;          // [S*7200]

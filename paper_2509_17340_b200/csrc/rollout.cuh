@@ -17,6 +17,7 @@ template <typename R>
 struct CostSums {
   R trk, vn, mag, rate, goal, col;
   bool valid;
+  bool aborted;  // partial stage-I cost passed RolloutEnv::abort_above (FP32 screening only)
 };
 
 // Read-only per-(scene, instance) environment of a rollout.
@@ -34,9 +35,11 @@ struct RolloutEnv<double> {
   double q_p, q_v, q_q;
   double cs, ca, cdmin, cdmax;
   GridMeta grid;
-  const uint32_t* gstart;
+  const uint4* gcells;
+  const uint32_t* gocc;
   const double* gpts;
   bool has_guide;
+  double abort_above;
 
   __device__ __forceinline__ V3<double> guide_at(int j) const {
     return {guide[3 * j], guide[3 * j + 1], guide[3 * j + 2]};
@@ -44,7 +47,7 @@ struct RolloutEnv<double> {
   __device__ __forceinline__ double unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ double attitude(Q4<double> q) const { return attitude_err_exact(q, gt); }
   __device__ __forceinline__ double collision(V3<double> p) const {
-    const double d2 = nearest_sq_exact(grid, gstart, gpts, p);
+    const double d2 = nearest_sq_exact(grid, gcells, gocc, gpts, p, cdmax * cdmax, cdmin * cdmin);
     return collision_term(sqrt(d2), cs, ca, cdmin, cdmax);
   }
 };
@@ -60,10 +63,12 @@ struct RolloutEnv<float> {
   float q_p, q_v, q_q;
   float cs, ca, cdmin, cdmax;
   GridMeta grid;
-  const uint32_t* gstart;
+  const uint4* gcells;
   const uint32_t* gocc;
   const float4* gpts;
   bool has_guide;
+  float abort_above;
+  float wq_track, wq_vnorm, wq_c, wq_cd;  // stage-I weights for the partial-cost bound
 
   __device__ __forceinline__ V3<float> guide_at(int j) const {
     const float4 g = guide[j];
@@ -72,7 +77,7 @@ struct RolloutEnv<float> {
   __device__ __forceinline__ float unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ float attitude(Q4<float> q) const { return attitude_err_fast(q, qg); }
   __device__ __forceinline__ float collision(V3<float> p) const {
-    const float d2 = nearest_sq_fast(grid, gstart, gocc, gpts, p);
+    const float d2 = nearest_sq_fast(grid, gcells, gocc, gpts, p, cdmax * cdmax * 1.0001f, cdmin * cdmin);
     return collision_term(sqrtf(d2), cs, ca, cdmin, cdmax);
   }
 };
@@ -128,7 +133,7 @@ struct PertZero {
 template <typename R, typename Pert>
 __device__ __forceinline__ CostSums<R> rollout_costs(St<R> x, const RolloutEnv<R>& env, const Pert& pert,
                                                       R* states_out = nullptr, R* controls_out = nullptr) {
-  CostSums<R> s{R(0), R(0), R(0), R(0), R(0), R(0), true};
+  CostSums<R> s{R(0), R(0), R(0), R(0), R(0), R(0), true, false};
   const Dyn<R>& dy = env.dyn;
   R up0 = R(0), up1 = R(0), up2 = R(0), up3 = R(0);
   const int N = env.N;
@@ -169,6 +174,15 @@ __device__ __forceinline__ CostSums<R> rollout_costs(St<R> x, const RolloutEnv<R
       }
     }
     up0 = u0; up1 = u1; up2 = u2; up3 = u3;
+    if constexpr (std::is_same_v<R, float>) {
+      // every stage-I term is >= 0, so the partial sum bounds the final cost
+      // from below: past the bound the sample cannot be in the softmin support
+      if (((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) +
+              (s.goal + s.col) > env.abort_above) {
+        s.aborted = true;
+        return s;
+      }
+    }
     const St<R> nx = rk4_normalized(x, u0, V3<R>{u1, u2, u3}, dy);
     if (!state_finite(nx)) {
       s.valid = false;

@@ -111,10 +111,16 @@ def run_case(oracle, cfg, pts, pose, x, goal_target=None, goal=None, previous=No
     bd = [r.breakdown.track, r.breakdown.vnorm, r.breakdown.ctrl, r.breakdown.goal, r.breakdown.collision]
     assert rel(bd, o["breakdown"]) <= 1e-9
     assert rel(r.winner_states, o["winner_states"]) <= 1e-9
-    # screening costs
+    # screening costs; FP32 screening may stop a sample early (reported as
+    # FLT_MAX) only when it provably lies outside the softmin support
     sc, osc, margin = r.sample_costs, o["sample_costs"], o["sample_margin"]
-    fin = np.isfinite(osc)
-    assert np.array_equal(np.isfinite(sc), fin)
+    aborted = sc >= 3.0e38
+    if aborted.any():
+        assert precision == 32
+        rho = np.min(np.where(np.isfinite(osc), osc, np.inf), axis=1, keepdims=True)
+        assert np.all((osc > rho + 64 * cfg.mppi.lambda_)[aborted]), "an aborted sample was in the support"
+    fin = np.isfinite(osc) & ~aborted
+    assert np.array_equal(np.isfinite(sc) & ~aborted, fin)
     ok = fin & (margin > 1e-4)
     tol = 1e-4 if precision == 32 else 1e-11
     assert rel(sc[ok], osc[ok]) <= tol
