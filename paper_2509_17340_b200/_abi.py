@@ -143,7 +143,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("AMPPI_LIB_PATH") or LIB_PATH
     if not os.path.exists(p):
         raise RuntimeError(f"{p} not found: run __graft_entry__.build() (no CPU fallback exists)")
     lib = ctypes.CDLL(p)

@@ -4,6 +4,7 @@
 // cannot be created without a CUDA device.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -156,6 +157,8 @@ struct amppi_ctx {
   uint32_t* cand_k{nullptr};
   double* cand_s{nullptr};
   double* cand_w{nullptr};
+  uint2* pairs{nullptr};
+  unsigned long long* pair_count{nullptr};
   unsigned char* d_gather{nullptr};
   // single-scene snapshot bookkeeping
   bool have_snapshot{false};
@@ -384,6 +387,15 @@ int create_impl(amppi_ctx* ctx) {
   pl.cost32 = static_cast<float*>(p);
   CK(A.alloc(&p, SM * K * sizeof(double)));
   pl.cost64 = static_cast<double*>(p);
+  {
+    const size_t jobs = std::max<size_t>(SM, static_cast<size_t>(kLatencyRollouts));
+    CK(A.alloc(&p, static_cast<size_t>(kLatencyRollouts) * N * 4 * sizeof(float)));
+    pl.pos32 = static_cast<float*>(p);
+    CK(A.alloc(&p, jobs * N * 4 * sizeof(double)));
+    pl.pos64 = static_cast<double*>(p);
+    CK(A.alloc(&p, jobs * sizeof(TrajSums)));
+    pl.tsum = static_cast<TrajSums*>(p);
+  }
   CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(int32_t)));
   pl.done = static_cast<int32_t*>(p);
   CK(cudaMemset(pl.done, 0, static_cast<size_t>(S) * sizeof(int32_t)));
@@ -397,6 +409,10 @@ int create_impl(amppi_ctx* ctx) {
   ctx->cand_s = static_cast<double*>(p);
   CK(A.alloc(&p, SM * K * sizeof(double)));
   ctx->cand_w = static_cast<double*>(p);
+  CK(A.alloc(&p, SM * K * sizeof(uint2)));
+  ctx->pairs = static_cast<uint2*>(p);
+  CK(A.alloc(&p, sizeof(unsigned long long)));
+  ctx->pair_count = static_cast<unsigned long long*>(p);
   ctx->timer.enabled = ctx->opt.profile != 0;
   return AMPPI_OK;
 }
@@ -428,7 +444,7 @@ int run_cycle(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, bool do_
   }
   if (do_plan) {
     cudaError_t e = launch_plan_impl(in, ctx->P, ctx->pl, ctx->dc, ctx->opt.precision, winner_rollout, ctx->cand_k,
-                                     ctx->cand_s, ctx->cand_w, ctx->stream, &ctx->timer);
+                                     ctx->cand_s, ctx->cand_w, ctx->pairs, ctx->pair_count, ctx->stream, &ctx->timer);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_plan");
   }
   return AMPPI_OK;

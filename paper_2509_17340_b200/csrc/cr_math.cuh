@@ -114,25 +114,74 @@ CRM_HD dd reduce_pio2(double x, int& quadrant) {
   return r;
 }
 
-// sin(r), cos(r) for |r| <= pi/4 + eps, Taylor series in double-double.
+// 1/n! as double-doubles (hi + lo, generated with mpmath at 400 bits).
+#ifdef __CUDACC__
+__device__ __constant__
+#endif
+static const dd kInvFact[36] = {
+    {0x1.0000000000000p+0, 0x0.0p+0},  // 1/0!
+    {0x1.0000000000000p+0, 0x0.0p+0},  // 1/1!
+    {0x1.0000000000000p-1, 0x0.0p+0},  // 1/2!
+    {0x1.5555555555555p-3, 0x1.5555555555555p-57},  // 1/3!
+    {0x1.5555555555555p-5, 0x1.5555555555555p-59},  // 1/4!
+    {0x1.1111111111111p-7, 0x1.1111111111111p-63},  // 1/5!
+    {0x1.6c16c16c16c17p-10, -0x1.f49f49f49f49fp-65},  // 1/6!
+    {0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-73},  // 1/7!
+    {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76},  // 1/8!
+    {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73},  // 1/9!
+    {0x1.27e4fb7789f5cp-22, 0x1.cbbc05b4fa99ap-76},  // 1/10!
+    {0x1.ae64567f544e4p-26, -0x1.c062e06d1f209p-80},  // 1/11!
+    {0x1.1eed8eff8d898p-29, -0x1.2aec959e14c06p-83},  // 1/12!
+    {0x1.6124613a86d09p-33, 0x1.f28e0cc748ebep-87},  // 1/13!
+    {0x1.93974a8c07c9dp-37, 0x1.05d6f8a2efd1fp-92},  // 1/14!
+    {0x1.ae7f3e733b81fp-41, 0x1.1d8656b0ee8cbp-97},  // 1/15!
+    {0x1.ae7f3e733b81fp-45, 0x1.1d8656b0ee8cbp-101},  // 1/16!
+    {0x1.952c77030ad4ap-49, 0x1.ac981465ddc6cp-103},  // 1/17!
+    {0x1.6827863b97d97p-53, 0x1.eec01221a8b0bp-107},  // 1/18!
+    {0x1.2f49b46814157p-57, 0x1.2650f61dbdcb4p-112},  // 1/19!
+    {0x1.e542ba4020225p-62, 0x1.ea72b4afe3c2fp-120},  // 1/20!
+    {0x1.71b8ef6dcf572p-66, -0x1.d043ae40c4647p-120},  // 1/21!
+    {0x1.0ce396db7f853p-70, -0x1.aebcdbd20331cp-124},  // 1/22!
+    {0x1.761b41316381ap-75, -0x1.3423c7d91404fp-130},  // 1/23!
+    {0x1.f2cf01972f578p-80, -0x1.9ada5fcc1ab14p-135},  // 1/24!
+    {0x1.3f3ccdd165fa9p-84, -0x1.58ddadf344487p-139},  // 1/25!
+    {0x1.88e85fc6a4e5ap-89, -0x1.71c37ebd16540p-143},  // 1/26!
+    {0x1.d1ab1c2dccea3p-94, 0x1.054d0c78aea14p-149},  // 1/27!
+    {0x1.0a18a2635085dp-98, 0x1.b9e2e28e1aa54p-153},  // 1/28!
+    {0x1.259f98b4358adp-103, 0x1.eaf8c39dd9bc5p-157},  // 1/29!
+    {0x1.3932c5047d60ep-108, 0x1.832b7b530a627p-162},  // 1/30!
+    {0x1.434d2e783f5bcp-113, 0x1.0b87b91be9affp-167},  // 1/31!
+    {0x1.434d2e783f5bcp-118, 0x1.0b87b91be9affp-172},  // 1/32!
+    {0x1.3981254dd0d52p-123, -0x1.2b1f4c8015a2fp-177},  // 1/33!
+    {0x1.2710231c0fd7ap-128, 0x1.3f8a2b4af9d6bp-184},  // 1/34!
+    {0x1.0dc59c716d91fp-133, 0x1.419e3fad3f031p-188},  // 1/35!
+};
+
+CRM_HD dd inv_fact(int n) {
+#ifdef __CUDA_ARCH__
+  return kInvFact[n];
+#else
+  return kInvFact[n];
+#endif
+}
+
+// sin(r), cos(r) for |r| <= pi/4 + eps: Horner in r^2 over double-double
+// Taylor coefficients (terms through r^33 / r^32, truncation < 2^-110).
+//   sin r = r * sum_i (-1)^i r^2i / (2i+1)!,   cos r = sum_i (-1)^i r^2i / (2i)!
 CRM_HD void dd_sincos_small(dd r, dd& s, dd& c) {
   const dd r2 = dd_mul(r, r);
-  // sin: r - r^3/3! + ...  (terms up to r^33)
-  dd term = r;
-  dd sum_s = r;
-  for (int n = 3; n <= 33; n += 2) {
-    term = dd_div_d(dd_mul(term, r2), -static_cast<double>(n * (n - 1)));
-    sum_s = dd_add(sum_s, term);
+  dd ps = inv_fact(33);  // i = 16: positive
+  for (int i = 15; i >= 0; --i) {
+    const dd a = (i & 1) ? dd_neg(inv_fact(2 * i + 1)) : inv_fact(2 * i + 1);
+    ps = dd_add(a, dd_mul(r2, ps));
   }
-  // cos: 1 - r^2/2! + ... (terms up to r^32)
-  term = dd{1.0, 0.0};
-  dd sum_c = term;
-  for (int n = 2; n <= 32; n += 2) {
-    term = dd_div_d(dd_mul(term, r2), -static_cast<double>(n * (n - 1)));
-    sum_c = dd_add(sum_c, term);
+  s = dd_mul(ps, r);
+  dd pc = inv_fact(32);  // i = 16: positive
+  for (int i = 15; i >= 0; --i) {
+    const dd b = (i & 1) ? dd_neg(inv_fact(2 * i)) : inv_fact(2 * i);
+    pc = dd_add(b, dd_mul(r2, pc));
   }
-  s = sum_s;
-  c = sum_c;
+  c = pc;
 }
 
 CRM_HD void dd_sincos(double x, dd& s, dd& c) {
@@ -167,6 +216,18 @@ CRM_HD double cos_cr(double x) {
   dd s, c;
   dd_sincos(x, s, c);
   return round_dd(c);
+}
+
+CRM_HD void sincos_cr(double x, double& sn, double& cs) {
+  if (plain_args(x) || fabs(x) > 1e5) {
+    sn = sin(x);
+    cs = cos(x);
+    return;
+  }
+  dd s, c;
+  dd_sincos(x, s, c);
+  sn = round_dd(s);
+  cs = round_dd(c);
 }
 
 // Correction of a near-correct atan2 estimate t0: rotate (x, y) by -t0 in

@@ -16,6 +16,15 @@
 
 namespace amppi_dev {
 
+#ifdef AMPPI_STATS
+// Query statistics (stats builds only): queries, queries past the occupancy
+// bit, cell records tested, cells scanned, points scanned.
+__device__ unsigned long long g_query_stats[5];
+#define AMPPI_STAT(i, v) atomicAdd(&g_query_stats[i], static_cast<unsigned long long>(v))
+#else
+#define AMPPI_STAT(i, v) ((void)0)
+#endif
+
 template <typename R>
 struct V3 {
   R x, y, z;
@@ -324,14 +333,10 @@ __device__ __forceinline__ R collision_term(R d, R scale, R slope, R dmin, R dma
   return R(0);
 }
 
-// Collision-grid neighbourhood order: the query's own cell, then the 6 face,
-// 12 edge and 8 corner neighbours (closest first, so the branch-and-bound
-// below prunes early).
-__constant__ __device__ signed char kNbrOrder[27][3] = {
-    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
-    {-1, -1, 0}, {-1, 1, 0},  {1, -1, 0},  {1, 1, 0},   {-1, 0, -1}, {-1, 0, 1},  {1, 0, -1},
-    {1, 0, 1},   {0, -1, -1}, {0, -1, 1},  {0, 1, -1},  {0, 1, 1},   {-1, -1, -1}, {-1, -1, 1},
-    {-1, 1, -1}, {-1, 1, 1},  {1, -1, -1}, {1, -1, 1},  {1, 1, -1},  {1, 1, 1}};
+// Collision-grid neighbourhood walk: offsets 0, -1, +1 per axis (x outer),
+// so the query's own cell comes first and the branch and bound below prunes
+// early.  Small nested loops keep the kernel's code footprint small.
+__device__ __forceinline__ int nbr_delta(int i) { return i == 0 ? 0 : (i == 1 ? -1 : 1); }
 
 __device__ __forceinline__ bool occupancy_maybe_near(const GridMeta& g, const uint32_t* __restrict__ occ, int cx,
                                                      int cy, int cz) {
@@ -357,8 +362,10 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
   const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
   if (!occupancy_maybe_near(g, occ, cx, cy, cz)) return best;
   const double q = g.h * (1.0 / 255.0);
-  for (int o = 0; o < 27; ++o) {
-    const int x = cx + kNbrOrder[o][0], y = cy + kNbrOrder[o][1], z = cz + kNbrOrder[o][2];
+  for (int ix = 0; ix < 3; ++ix)
+  for (int iy = 0; iy < 3; ++iy)
+  for (int iz = 0; iz < 3; ++iz) {
+    const int x = cx + nbr_delta(ix), y = cy + nbr_delta(iy), z = cz + nbr_delta(iz);
     if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
     const uint4 rec = cells[(x * g.dims[1] + y) * g.dims[2] + z];
     if (rec.y == 0) continue;
@@ -374,7 +381,7 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
       const double d2 = sqnorm(p - qq);
       best = d2 < best ? d2 : best;
     }
-    if (best < stop2) break;
+    if (best < stop2) return best;
   }
   return best;
 }
@@ -388,19 +395,24 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
   const float fy = (p.y - g.origin_f[1]) * g.inv_h_f;
   const float fz = (p.z - g.origin_f[2]) * g.inv_h_f;
   const int cx = __float2int_rd(fx), cy = __float2int_rd(fy), cz = __float2int_rd(fz);
+  AMPPI_STAT(0, 1);
   if (!occupancy_maybe_near(g, occ, cx, cy, cz)) return best;
-  // p relative to the query cell's corner, in cells (box quanta: 1/255 cell)
+  AMPPI_STAT(1, 1);
+  // p relative to the query cell's corner, in box quanta (1/255 cell)
   const float rx = (fx - static_cast<float>(cx)) * 255.f, ry = (fy - static_cast<float>(cy)) * 255.f,
               rz = (fz - static_cast<float>(cz)) * 255.f;
   const float q2 = g.h_f * g.h_f * (1.f / (255.f * 255.f));
   const float lim = lim2 / q2;  // thresholds in quanta^2
-  for (int o = 0; o < 27; ++o) {
-    const int ox = kNbrOrder[o][0], oy = kNbrOrder[o][1], oz = kNbrOrder[o][2];
+  for (int ix = 0; ix < 3; ++ix)
+  for (int iy = 0; iy < 3; ++iy)
+  for (int iz = 0; iz < 3; ++iz) {
+    const int ox = nbr_delta(ix), oy = nbr_delta(iy), oz = nbr_delta(iz);
     const int x = cx + ox, y = cy + oy, z = cz + oz;
     if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
     const uint4 rec = __ldg(cells + (x * g.dims[1] + y) * g.dims[2] + z);
+    AMPPI_STAT(2, 1);
     if (rec.y == 0) continue;
-    // box in quanta relative to the query cell's corner
+    // box in quanta relative to the query cell's corner (+-1 quantum of slack)
     const float bx0 = static_cast<float>(ox * 255 + static_cast<int>(rec.z & 255u)) - 1.f;
     const float bx1 = static_cast<float>(ox * 255 + static_cast<int>(rec.w & 255u)) + 1.f;
     const float by0 = static_cast<float>(oy * 255 + static_cast<int>((rec.z >> 8) & 255u)) - 1.f;
@@ -412,12 +424,14 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
     const float gz = fmaxf(fmaxf(bz0 - rz, rz - bz1), 0.f);
     const float bd2 = gx * gx + gy * gy + gz * gz;
     if (bd2 >= fminf(best / q2, lim)) continue;
+    AMPPI_STAT(3, 1);
+    AMPPI_STAT(4, rec.y);
     for (uint32_t k = rec.x; k < rec.x + rec.y; ++k) {
       const float4 qq = __ldg(pts + k);
       const float dx = p.x - qq.x, dy = p.y - qq.y, dz = p.z - qq.z;
       best = fminf(best, dx * dx + dy * dy + dz * dz);
     }
-    if (best < stop2) break;
+    if (best < stop2) return best;
   }
   return best;
 }

@@ -6,16 +6,22 @@
 // (cell keys, per-cell argmin, pooled argmax) is computed with the oracle's
 // operation order and IEEE rounding, so keys and ranges are bit-exact.
 //
-//   K1 k_key_points      one thread per point: world->body (FP64), range,
-//                        (i, j) cell key, 64-bit atomicMin of the range bits
-//                        per cell + candidate log for the (r, index) tie-break
-//   K1b k_resolve_ties   candidates whose range equals the cell minimum take
-//                        atomicMin of their point index (lexicographic
-//                        (r, idx) minimum == "strict <, first point wins",
-//                        perception.cpp:80-86)
-//   K2 k_finalize_scene  one CTA per scene: ranges/has_point, 6x6 argmax
-//                        pooling, flat-order compaction + world transform,
-//                        collision grid (counting sort) + dilated occupancy
+// Cell keys: FP32 atan2 decides unless its quotient lies within 1e-3 cells of
+// a boundary (FP32 error < 3e-5 cells); then FP64 atan2 decides unless within
+// 1e-9 cells (CUDA's FP64 error < 1e-13 cells); then the correctly rounded
+// atan2 (cr_math.cuh) decides, matching glibc's floor() result.
+//
+// Two schedules:
+//   scenes of <= kFusedMaxPoints points: k_snapshot_scene, one CTA per scene,
+//     per-cell (range, index) minimum with shared-memory atomics (pass A:
+//     64-bit atomicMin of the range bits, pass B: points at the minimum take
+//     atomicMin of their index = "strict <, first point wins",
+//     perception.cpp:80-86), then the finalize body below;
+//   larger scenes: k_key_points (global 64-bit atomicMin + candidate log over
+//     many CTAs), k_resolve_ties, k_finalize_scene.
+// Finalize body (per scene): ranges / has_point, 6x6 argmax pooling, flat-order
+// compaction + world transform, collision grid (counting sort, dilated
+// occupancy, per-cell point boxes).
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -33,41 +39,62 @@ constexpr double kPiD = 0x1.921fb54442d18p+1;      // std::numbers::pi
 constexpr double kHalfPi = 0x1.921fb54442d18p+0;   // 0.5 * pi
 constexpr double kAzStep = 0x1.acee9f37bebd5p-5;   // 2*pi/120 == pi/60
 constexpr double kElStep = 0x1.acee9f37bebd5p-5;
-constexpr double kGuard = 1e-9;  // cells; CUDA atan2 error is < 1e-13 cells
+constexpr double kGuard = 1e-9;   // cells, FP64 stage
+constexpr float kGuardF = 1e-3f;  // cells, FP32 stage
+constexpr int kFusedMaxPoints = 1 << 16;
+
+// Correctly-rounded recomputation, kept out of line: taken only for keys
+// within 1e-9 of a cell boundary.
+__device__ __noinline__ double atan2_slow(double y, double x) { return crm::atan2_cr(y, x); }
 
 __device__ __forceinline__ bool near_integer(double v) {
   const double fl = floor(v);
   return (v - fl) < kGuard || ((fl + 1.0) - v) < kGuard;
 }
 
-}  // namespace
+// FP32 quotient -> cell index, or -1 when within the guard band.
+__device__ __forceinline__ int fast_cell(float num, float den, float offset, float inv_step) {
+  const float v = (atan2f(num, den) + offset) * inv_step;
+  const float fl = floorf(v);
+  if (v - fl < kGuardF || (fl + 1.f) - v < kGuardF) return -1;
+  return static_cast<int>(fl);
+}
 
-// azimuth_cell(atan2(y, x)) (perception.cpp:17-21) with glibc-equal keys.
-__device__ int az_cell_of(double y, double x) {
+// azimuth_cell(atan2(y, x)) (perception.cpp:17-21), FP64 stages.
+__device__ __noinline__ int az_cell_slow(double y, double x) {
   double az = atan2(y, x);
   double v = (az + kPiD) / kAzStep;
   if (near_integer(v)) {
-    az = crm::atan2_cr(y, x);
+    az = atan2_slow(y, x);
     v = (az + kPiD) / kAzStep;
   }
-  int i = static_cast<int>(floor(v));
-  if (i >= kAz) i -= kAz;
-  return i < 0 ? 0 : (i > kAz - 1 ? kAz - 1 : i);
+  return static_cast<int>(floor(v));
 }
 
-// elevation_cell(atan2(z, rho)) (perception.cpp:23-26).
-__device__ int el_cell_of(double z, double rho) {
+// elevation_cell(atan2(z, rho)) (perception.cpp:23-26), FP64 stages.
+__device__ __noinline__ int el_cell_slow(double z, double rho) {
   double el = atan2(z, rho);
   double v = (el + kHalfPi) / kElStep;
   if (near_integer(v)) {
-    el = crm::atan2_cr(z, rho);
+    el = atan2_slow(z, rho);
     v = (el + kHalfPi) / kElStep;
   }
-  const int j = static_cast<int>(floor(v));
-  return j < 0 ? 0 : (j > kEl - 1 ? kEl - 1 : j);
+  return static_cast<int>(floor(v));
 }
 
-namespace {
+// Flat cell f = i*60 + j of a body-frame point.
+__device__ __forceinline__ int cell_key(V3<double> p) {
+  const double rho = sqrt(p.x * p.x + p.y * p.y);
+  constexpr float kInvStepF = static_cast<float>(1.0 / 0x1.acee9f37bebd5p-5);
+  int i = fast_cell(static_cast<float>(p.y), static_cast<float>(p.x), 3.14159265358979f, kInvStepF);
+  if (i < 0) i = az_cell_slow(p.y, p.x);
+  if (i >= kAz) i -= kAz;  // +pi wraps onto -pi
+  i = i < 0 ? 0 : (i > kAz - 1 ? kAz - 1 : i);
+  int j = fast_cell(static_cast<float>(p.z), static_cast<float>(rho), 1.57079632679490f, kInvStepF);
+  if (j < 0) j = el_cell_slow(p.z, rho);
+  j = j < 0 ? 0 : (j > kEl - 1 ? kEl - 1 : j);  // pole belongs to the top cell
+  return i * kEl + j;
+}
 
 struct PoseFrame {
   V3<double> p;
@@ -92,23 +119,32 @@ __device__ __forceinline__ V3<double> to_body(const PoseFrame& f, V3<double> w) 
   return mat_t_vec(f.r, w - f.p);
 }
 
+// build_partition's per-point work (perception.cpp:72-79): false when the
+// point is outside (kMinPointRange, r_max].
+__device__ __forceinline__ bool key_point(const PoseFrame& pose, V3<double> w, double r_max, int& f, uint64_t& bits) {
+  const V3<double> p = to_body(pose, w);
+  const double r = sqrt(sqnorm(p));
+  if (!(r > kMinPointRange) || r > r_max) return false;
+  f = cell_key(p);
+  bits = static_cast<uint64_t>(__double_as_longlong(r));
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// global schedule (large scenes)
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_key_points(BatchIn in, Perception P) {
   const int s = blockIdx.y;
   __shared__ PoseFrame pose;
   if (threadIdx.x == 0) pose = load_pose(in.poses + 10 * s);
   __syncthreads();
   const int64_t b = in.offsets[s], e = in.offsets[s + 1];
-  const double r_max = in.r_max;
   uint64_t* __restrict__ cell_r = P.cell_r + static_cast<int64_t>(s) * kCells;
   for (int64_t g = b + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < e;
        g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const V3<double> p = to_body(pose, load_point(in, g));
-    const double r = sqrt(sqnorm(p));
-    if (!(r > kMinPointRange) || r > r_max) continue;  // perception.cpp:74
-    const int i = az_cell_of(p.y, p.x);
-    const int j = el_cell_of(p.z, sqrt(p.x * p.x + p.y * p.y));
-    const int f = i * kEl + j;
-    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(r));
+    int f;
+    uint64_t bits;
+    if (!key_point(pose, load_point(in, g), in.r_max, f, bits)) continue;
     const uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(cell_r + f), bits);
     if (old >= bits) {  // may be the cell minimum: log for the index tie-break
       const unsigned long long slot = atomicAdd(P.cand_count, 1ull);
@@ -128,15 +164,15 @@ __global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
 }
 
 // ---------------------------------------------------------------------------
-// K2
+// finalize body
 // ---------------------------------------------------------------------------
 constexpr int kFinalizeThreads = 512;
 constexpr int kChunk = (kCells + kFinalizeThreads - 1) / kFinalizeThreads;  // 15
+constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 
 struct FinalizeSmem {
-  double rng[kCells];
-  uint32_t idx[kCells];
-  uint32_t counts[kGridCells + 1];
+  double rng[kCells];  // also the u64 range-bits table during fused keying, and
+  uint32_t idx[kCells];  // (rng..idx, 86 KB) the sort keys / values of the grid build
   uint32_t occ[kOccWords];
   uint32_t warp_sums[kFinalizeThreads / 32];
   double bbox_lo[kFinalizeThreads / 32][3];
@@ -176,31 +212,22 @@ __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32
   return out;
 }
 
-__global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
-  const int s = blockIdx.x;
+// Everything after the per-cell (range, index) minimum.  Expects sm.rng /
+// sm.idx (empty cells: r_max / 0xFFFFFFFF) and sm.pose filled and a
+// preceding __syncthreads().
+__device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Perception& P, const DevConfig& cfg,
+                              int s) {
   const int tid = threadIdx.x;
-  const double r_max = in.r_max;
   const int64_t cell_base = static_cast<int64_t>(s) * kCells;
   const int64_t pt_base = in.offsets[s];
-  if (tid == 0) sm.pose = load_pose(in.poses + 10 * s);
-
-  // 1. per-cell range / argmin; reset the atomics tables for the next cycle
-  for (int f = tid; f < kCells; f += blockDim.x) {
-    const uint64_t bits = P.cell_r[cell_base + f];
-    const bool has = bits != kEmptyCell;
-    sm.rng[f] = has ? __longlong_as_double(static_cast<long long>(bits)) : r_max;
-    sm.idx[f] = has ? P.cell_idx[cell_base + f] : 0xFFFFFFFFu;
-    P.cell_r[cell_base + f] = kEmptyCell;
-    P.cell_idx[cell_base + f] = 0xFFFFFFFFu;
-    if (P.ranges) P.ranges[cell_base + f] = sm.rng[f];
-    if (P.has_point) P.has_point[cell_base + f] = has ? 1 : 0;
-  }
   for (int w = tid; w < kOccWords; w += blockDim.x) sm.occ[w] = 0u;
-  __syncthreads();
+  if (P.ranges)
+    for (int f = tid; f < kCells; f += blockDim.x) {
+      P.ranges[cell_base + f] = sm.rng[f];
+      P.has_point[cell_base + f] = sm.idx[f] != 0xFFFFFFFFu ? 1 : 0;
+    }
 
-  // 2. 6x6 argmax pooling, i outer / j inner, strict > (perception.cpp:99-121)
+  // pool_coarse: 6x6 argmax, i outer / j inner, strict > (perception.cpp:99-121)
   if (tid < kCoarse) {
     const int I = tid / kCEl, J = tid % kCEl;
     int bi = I * kPool, bj = J * kPool;
@@ -226,7 +253,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
     P.safe_point[3 * o + 2] = best * dz;
   }
 
-  // 3. filtered cloud in flat order (perception.cpp:124-144): compaction
+  // filtered_cloud + to_world_frame in flat order (perception.cpp:124-144)
   const int f0 = tid * kChunk;
   const int f1 = min(f0 + kChunk, kCells);
   uint32_t mine = 0;
@@ -236,6 +263,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
   double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
   double* __restrict__ filt = P.filtered + cell_base * 3;
   uint32_t pos = pos0;
+#pragma unroll 5
   for (int f = f0; f < f1; ++f) {
     const uint32_t k = sm.idx[f];
     if (k == 0xFFFFFFFFu) {
@@ -247,7 +275,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
       continue;
     }
     const V3<double> pb = to_body(sm.pose, load_point(in, pt_base + k));
-    const V3<double> pw = sm.pose.p + mat_vec(sm.pose.r, pb);  // to_world_frame
+    const V3<double> pw = sm.pose.p + mat_vec(sm.pose.r, pb);
     if (P.nearest) {
       P.nearest[(cell_base + f) * 3] = pb.x;
       P.nearest[(cell_base + f) * 3 + 1] = pb.y;
@@ -260,7 +288,6 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
     hi[0] = fmax(hi[0], pw.x); hi[1] = fmax(hi[1], pw.y); hi[2] = fmax(hi[2], pw.z);
     ++pos;
   }
-  // bbox reduction
   const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -316,91 +343,179 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
     return;
   }
 
-  // 4. counting sort into the grid
-  for (int c = tid; c <= ncell; c += blockDim.x) sm.counts[c] = 0u;
-  __syncthreads();
-  auto cell_of = [&](const V3<double>& p, int* c3) {
+  // collision grid: sort the filtered points by (cell, Morton code of the
+  // 1/8-cell sub-position) with a block bitonic sort in shared memory (the
+  // per-cell tables are dead by now): each cell's points become contiguous and
+  // spatially ordered.
+  uint32_t* keys = reinterpret_cast<uint32_t*>(sm.rng);             // [<= 8192]
+  uint16_t* vals = reinterpret_cast<uint16_t*>(keys + kCellsPow2);  // [<= 8192]
+  uint32_t n2 = 1;
+  while (n2 < n_pts) n2 <<= 1;
+  auto cell_of = [&](const V3<double>& p, int* c3, int* sub3) {
     const double rel[3] = {p.x - meta.origin[0], p.y - meta.origin[1], p.z - meta.origin[2]};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      int c = static_cast<int>(floor(rel[a] * meta.inv_h));
-      c3[a] = c < 0 ? 0 : (c > meta.dims[a] - 1 ? meta.dims[a] - 1 : c);
+      const double u = rel[a] * meta.inv_h;
+      int c = static_cast<int>(floor(u));
+      c = c < 0 ? 0 : (c > meta.dims[a] - 1 ? meta.dims[a] - 1 : c);
+      int sc = static_cast<int>(floor((u - c) * 8.0));
+      c3[a] = c;
+      sub3[a] = sc < 0 ? 0 : (sc > 7 ? 7 : sc);
     }
     return (c3[0] * meta.dims[1] + c3[1]) * meta.dims[2] + c3[2];
   };
-  for (uint32_t k = pos0; k < pos; ++k) {
-    const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
-    int c3[3];
-    const int c = cell_of(pw, c3);
-    atomicAdd(&sm.counts[c], 1u);
-    // dilated occupancy over the padded (dims+2)^3 lattice
-    const int py = meta.dims[1] + 2, pz = meta.dims[2] + 2;
-    for (int dx = 0; dx < 3; ++dx)
-      for (int dy = 0; dy < 3; ++dy)
-        for (int dz = 0; dz < 3; ++dz) {
-          const int oc = ((c3[0] + dx) * py + (c3[1] + dy)) * pz + (c3[2] + dz);
-          atomicOr(&sm.occ[oc >> 5], 1u << (oc & 31));
+  for (uint32_t k = tid; k < n2; k += blockDim.x) {
+    uint32_t key = 0xFFFFFFFFu;
+    if (k < n_pts) {
+      const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
+      int c3[3], s3[3];
+      const int c = cell_of(pw, c3, s3);
+      uint32_t mort = 0;
+#pragma unroll
+      for (int bit = 2; bit >= 0; --bit)
+        mort = (mort << 3) | (((s3[0] >> bit) & 1) << 2) | (((s3[1] >> bit) & 1) << 1) | ((s3[2] >> bit) & 1);
+      key = (static_cast<uint32_t>(c) << 9) | mort;
+    }
+    keys[k] = key;
+    vals[k] = static_cast<uint16_t>(k);
+  }
+  for (int w = tid; w < kOccWords; w += blockDim.x) sm.occ[w] = 0u;
+  __syncthreads();
+  for (uint32_t size = 2; size <= n2; size <<= 1)
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t t = tid; t < (n2 >> 1); t += blockDim.x) {
+        const uint32_t i = 2 * t - (t & (stride - 1));
+        const uint32_t j = i + stride;
+        const bool up = (i & size) == 0;
+        const uint32_t ki = keys[i], kj = keys[j];
+        if ((ki > kj) == up) {
+          keys[i] = kj;
+          keys[j] = ki;
+          const uint16_t v = vals[i];
+          vals[i] = vals[j];
+          vals[j] = v;
         }
-  }
-  __syncthreads();
-  // exclusive scan of counts (each thread a contiguous chunk of cells)
-  const int cchunk = (ncell + blockDim.x - 1) / blockDim.x;
-  const int c0 = min(tid * cchunk, ncell), c1 = min(c0 + cchunk, ncell);
-  uint32_t local = 0;
-  for (int c = c0; c < c1; ++c) local += sm.counts[c];
-  uint32_t run = block_exclusive_scan(local, sm.warp_sums, &sm.total);
-  for (int c = c0; c < c1; ++c) {
-    const uint32_t cnt = sm.counts[c];
-    gstart[c] = run;
-    sm.counts[c] = run;  // becomes the scatter cursor
-    run += cnt;
-  }
-  if (tid == 0) gstart[ncell] = n_pts;
-  for (int w = tid; w < kOccWords; w += blockDim.x) gocc[w] = sm.occ[w];
-  __syncthreads();
+      }
+      __syncthreads();
+    }
+  // scatter into sorted order; cell ranges from the key boundaries; dilated
+  // occupancy over the padded (dims+2)^3 lattice
   double* __restrict__ gp64 = P.grid_pts64 + cell_base * 3;
   float4* __restrict__ gp32 = P.grid_pts32 + cell_base;
-  for (uint32_t k = pos0; k < pos; ++k) {
-    const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
-    int c3[3];
-    const int c = cell_of(pw, c3);
-    const uint32_t slot = atomicAdd(&sm.counts[c], 1u);
-    gp64[3 * slot] = pw.x;
-    gp64[3 * slot + 1] = pw.y;
-    gp64[3 * slot + 2] = pw.z;
-    gp32[slot] = make_float4(static_cast<float>(pw.x), static_cast<float>(pw.y), static_cast<float>(pw.z), 0.f);
+  uint4* __restrict__ gcell = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  for (int c = tid; c < ncell; c += blockDim.x) gcell[c] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  for (uint32_t i = tid; i < n_pts; i += blockDim.x) {
+    const uint32_t k = vals[i];
+    const double x = filt[3 * k], y = filt[3 * k + 1], z = filt[3 * k + 2];
+    gp64[3 * i] = x;
+    gp64[3 * i + 1] = y;
+    gp64[3 * i + 2] = z;
+    gp32[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.f);
+    const uint32_t c = keys[i] >> 9;
+    if (i == 0 || (keys[i - 1] >> 9) != c) {  // first point of cell c
+      uint32_t e = i + 1;
+      while (e < n_pts && (keys[e] >> 9) == c) ++e;
+      gcell[c].x = i;
+      gcell[c].y = e - i;
+      const int cz = static_cast<int>(c % meta.dims[2]);
+      const int cy = static_cast<int>((c / meta.dims[2]) % meta.dims[1]);
+      const int cx = static_cast<int>(c / (meta.dims[2] * meta.dims[1]));
+      const int py = meta.dims[1] + 2, pz = meta.dims[2] + 2;
+      for (int dx = 0; dx < 3; ++dx)
+        for (int dy = 0; dy < 3; ++dy)
+          for (int dz = 0; dz < 3; ++dz) {
+            const int oc = ((cx + dx) * py + (cy + dy)) * pz + (cz + dz);
+            atomicOr(&sm.occ[oc >> 5], 1u << (oc & 31));
+          }
+    }
   }
   __syncthreads();
-  // 5. per-cell records: point range + point bounding box relative to the
-  //    cell corner, quantised outward to h/255 (one extra quantum of slack)
-  uint4* __restrict__ gcell = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  for (int w = tid; w < kOccWords; w += blockDim.x) gocc[w] = sm.occ[w];
+  // per-cell point boxes relative to the cell corner, quantised outward to
+  // h/255 with one extra quantum of slack
   const double quanta = 255.0 * meta.inv_h;
   for (int c = tid; c < ncell; c += blockDim.x) {
-    const uint32_t b = gstart[c], e = gstart[c + 1];
-    if (b == e) {
-      gcell[c] = make_uint4(b, 0u, 0u, 0u);
-      continue;
-    }
+    const uint4 rec = gcell[c];
+    if (rec.y == 0) continue;
     const int cz = c % meta.dims[2], cy = (c / meta.dims[2]) % meta.dims[1], cx = c / (meta.dims[2] * meta.dims[1]);
     const int cc[3] = {cx, cy, cz};
-    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
-    for (uint32_t k = b; k < e; ++k)
+    double blo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, bhi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (uint32_t k = rec.x; k < rec.x + rec.y; ++k)
       for (int a = 0; a < 3; ++a) {
-        lo[a] = fmin(lo[a], gp64[3 * k + a]);
-        hi[a] = fmax(hi[a], gp64[3 * k + a]);
+        blo[a] = fmin(blo[a], gp64[3 * k + a]);
+        bhi[a] = fmax(bhi[a], gp64[3 * k + a]);
       }
     uint32_t ql = 0u, qh = 0u;
     for (int a = 0; a < 3; ++a) {
       const double corner = meta.origin[a] + cc[a] * meta.h;
-      double fl = floor((lo[a] - corner) * quanta) - 1.0;
-      double fh = ceil((hi[a] - corner) * quanta) + 1.0;
+      double fl = floor((blo[a] - corner) * quanta) - 1.0;
+      double fh = ceil((bhi[a] - corner) * quanta) + 1.0;
       fl = fl < 0.0 ? 0.0 : (fl > 255.0 ? 255.0 : fl);
       fh = fh < 0.0 ? 0.0 : (fh > 255.0 ? 255.0 : fh);
       ql |= static_cast<uint32_t>(fl) << (8 * a);
       qh |= static_cast<uint32_t>(fh) << (8 * a);
     }
-    gcell[c] = make_uint4(b, e - b, ql, qh);
+    gcell[c] = make_uint4(rec.x, rec.y, ql, qh);
   }
+}
+
+// Global schedule, last step: tables from K1/K1b (reset for the next cycle).
+__global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
+  const int s = blockIdx.x;
+  const int64_t cell_base = static_cast<int64_t>(s) * kCells;
+  if (threadIdx.x == 0) sm.pose = load_pose(in.poses + 10 * s);
+  for (int f = threadIdx.x; f < kCells; f += blockDim.x) {
+    const uint64_t bits = P.cell_r[cell_base + f];
+    const bool has = bits != kEmptyCell;
+    sm.rng[f] = has ? __longlong_as_double(static_cast<long long>(bits)) : in.r_max;
+    sm.idx[f] = has ? P.cell_idx[cell_base + f] : 0xFFFFFFFFu;
+    P.cell_r[cell_base + f] = kEmptyCell;
+    P.cell_idx[cell_base + f] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  finalize_body(sm, in, P, cfg, s);
+}
+
+// Fused schedule: one CTA per scene, per-cell minimum in shared memory.
+__global__ void __launch_bounds__(kFinalizeThreads, 1) k_snapshot_scene(BatchIn in, Perception P, DevConfig cfg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
+  unsigned long long* cell_bits = reinterpret_cast<unsigned long long*>(sm.rng);
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) sm.pose = load_pose(in.poses + 10 * s);
+  for (int f = tid; f < kCells; f += blockDim.x) {
+    cell_bits[f] = kEmptyCell;
+    sm.idx[f] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  const PoseFrame pose = sm.pose;
+  const int64_t b = in.offsets[s], e = in.offsets[s + 1];
+  const double r_max = in.r_max;
+  // pass A: minimum range bits per cell
+  for (int64_t g = b + tid; g < e; g += blockDim.x) {
+    int f;
+    uint64_t bits;
+    if (key_point(pose, load_point(in, g), r_max, f, bits)) atomicMin(cell_bits + f, bits);
+  }
+  __syncthreads();
+  // pass B: lowest point index among the points at the minimum
+  for (int64_t g = b + tid; g < e; g += blockDim.x) {
+    int f;
+    uint64_t bits;
+    if (key_point(pose, load_point(in, g), r_max, f, bits) && cell_bits[f] == bits)
+      atomicMin(sm.idx + f, static_cast<uint32_t>(g - b));
+  }
+  __syncthreads();
+  for (int f = tid; f < kCells; f += blockDim.x) {
+    const uint64_t bits = cell_bits[f];
+    sm.rng[f] = bits != kEmptyCell ? __longlong_as_double(static_cast<long long>(bits)) : r_max;
+  }
+  __syncthreads();
+  finalize_body(sm, in, P, cfg, s);
 }
 
 }  // namespace
@@ -408,12 +523,22 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
 size_t finalize_smem_bytes() { return sizeof(FinalizeSmem); }
 
 cudaError_t init_kernel_attributes() {
-  return cudaFuncSetAttribute(k_finalize_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_finalize_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(FinalizeSmem)));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_snapshot_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(sizeof(FinalizeSmem)));
 }
 
 cudaError_t launch_snapshot(const BatchIn& in, const Perception& P, const DevConfig& cfg, int64_t max_points_per_scene,
                             cudaStream_t st, KernelTimer* timer) {
+  // fused per-scene CTAs once there is at least a GPU's worth of scenes; the
+  // many-CTA keying has lower latency for a handful of scenes
+  if (max_points_per_scene <= kFusedMaxPoints && in.S >= 148) {
+    TimedRegion t(timer, "k_snapshot_scene", st);
+    k_snapshot_scene<<<in.S, kFinalizeThreads, sizeof(FinalizeSmem), st>>>(in, P, cfg);
+    return cudaGetLastError();
+  }
   cudaError_t err = cudaMemsetAsync(P.cand_count, 0, sizeof(unsigned long long), st);
   if (err != cudaSuccess) return err;
   const int threads = 256;

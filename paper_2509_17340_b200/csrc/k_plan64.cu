@@ -56,8 +56,10 @@ __device__ __forceinline__ int el_cell_exact(double el) {
 
 __device__ __forceinline__ V3<double> direction_from_angles(double az, double el, bool cr) {
   if (cr) {
-    const double ce = crm::cos_cr(el);
-    return {ce * crm::cos_cr(az), ce * crm::sin_cr(az), crm::sin_cr(el)};
+    double se, ce, sa, ca;
+    crm::sincos_cr(el, se, ce);
+    crm::sincos_cr(az, sa, ca);
+    return {ce * ca, ce * sa, se};
   }
   const double ce = cos(el);
   return {ce * cos(az), ce * sin(az), sin(el)};
@@ -247,6 +249,7 @@ __device__ __forceinline__ RolloutEnv<double> make_env64(const BatchIn& in, cons
   e.cdmax = cfg.col_d_max;
   e.grid = P.grid[s];
   e.gcells = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+
   e.gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
   e.gpts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
   e.has_guide = true;
@@ -314,6 +317,8 @@ struct UpdateScratch {  // global, per (scene, instance): [K] each
   uint32_t* cand_k;
   double* cand_s;
   double* cand_w;
+  uint2* pairs;                     // [S*M*K] (instance, support slot) work list for k_refine
+  unsigned long long* pair_count;
 };
 
 __device__ __forceinline__ double load_cost(const Plan& pl, int precision, int64_t i) {
@@ -378,6 +383,10 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
       run += t;
     }
     pl.n_support[smi] = run;
+    if (precision == 32 && run > 0) {  // reserve this instance's refine work items
+      const unsigned long long at = atomicAdd(us.pair_count, static_cast<unsigned long long>(run));
+      for (uint32_t c = 0; c < run; ++c) us.pairs[at + c] = make_uint2(static_cast<uint32_t>(smi), c);
+    }
   }
   __syncthreads();
   uint32_t pos = s_cnt[warp] + x - mine;
@@ -391,32 +400,31 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
   }
 }
 
-__global__ void __launch_bounds__(32) k_refine(BatchIn in, Perception P, Plan pl, DevConfig cfg, UpdateScratch us,
+// One thread per (instance, support slot) over the flattened work list:
+// full warps regardless of how the support sizes are distributed.
+__global__ void __launch_bounds__(64) k_refine(BatchIn in, Perception P, Plan pl, DevConfig cfg, UpdateScratch us,
                                                int iter) {
-  __shared__ double s_unom[4 * 64];
-  const int64_t smi = blockIdx.x;
-  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
-  const uint32_t n = pl.n_support[smi];
-  if (n == 0) return;
-  const int N = cfg.N;
-  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) s_unom[i] = pl.nominal[smi * N * 4 + i];
-  __syncwarp();
-  const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, s_unom);
-  const St<double> x0 = load_state(in.states + 10 * s);
-  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
-  const int64_t base = smi * cfg.K;
+  const unsigned long long n = *us.pair_count;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
-    const int k = static_cast<int>(us.cand_k[base + c]);
+  for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < n;
+       w += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const uint2 pr = us.pairs[w];
+    const int64_t smi = pr.x;
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+    const int64_t slot = smi * cfg.K + pr.y;
+    const int k = static_cast<int>(us.cand_k[slot]);
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    const St<double> x0 = load_state(in.states + 10 * s);
     CostSums<double> cs;
     if (in.injected) {
       cs = rollout_costs(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)});
     } else {
-      const PertRngD pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
-                        cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
-      cs = rollout_costs(x0, env, pr);
+      const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+      const PertRngD prng{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                          cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+      cs = rollout_costs(x0, env, prng);
     }
-    us.cand_s[base + c] = cs.valid ? stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta) : kInf;
+    us.cand_s[slot] = cs.valid ? stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta) : kInf;
   }
 }
 
@@ -490,29 +498,114 @@ __global__ void __launch_bounds__(128) k_nominal(BatchIn in, Plan pl, DevConfig 
   }
 }
 
-__global__ void __launch_bounds__(64) k_stage2(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+// Stage II (ensemble.cpp:132-149) in two passes: a sequential FP64 trajectory
+// per instance with the collision queries deferred, then one warp per
+// instance evaluating the N collision terms in parallel and summing them in
+// step order (costs.hpp:121-127).
+__global__ void __launch_bounds__(64) k_stage2_traj(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
   const int64_t smi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
-  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  TrajSums t{0, 0, 0, 0, 0, 0};
+  if (pl.alive[smi]) {
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    const CostSums<double> cs = rollout_costs<double, PertZero<double>, true>(
+        load_state(in.states + 10 * s), env, PertZero<double>{}, nullptr, nullptr, pl.pos64 + smi * cfg.N * 4);
+    t = TrajSums{cs.trk, cs.vn, cs.mag, cs.rate, cs.goal, cs.valid ? 1 : 0};
+  }
+  pl.tsum[smi] = t;
+}
+
+// Sum of the N collision terms of one deferred trajectory, in step order
+// (warp-cooperative; the result is valid in every lane).
+__device__ __forceinline__ double collision_sum_warp(const RolloutEnv<double>& env, const double* pos, int N,
+                                                     double* sm_terms) {
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j < N; j += 32)
+    sm_terms[j] = env.collision(V3<double>{pos[4 * j], pos[4 * j + 1], pos[4 * j + 2]});
+  __syncwarp();
+  double col = 0.0;
+  if (lane == 0)
+    for (int j = 0; j < N; ++j) col = col + sm_terms[j];
+  return __shfl_sync(0xffffffffu, col, 0);
+}
+
+__global__ void __launch_bounds__(128) k_stage2_col(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+  __shared__ double s_terms[4][64];
+  const int64_t smi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
+  const TrajSums t = pl.tsum[smi];
   double st2 = __longlong_as_double(0x7ff0000000000000ll);
   bool valid = false;
   double bd[5] = {0, 0, 0, 0, 0};
-  if (pl.alive[smi]) {
+  if (pl.alive[smi] && t.valid) {
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
     const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
-    const CostSums<double> cs = rollout_costs(load_state(in.states + 10 * s), env, PertZero<double>{});
-    if (cs.valid) {
-      st2 = cs.goal + cs.col;  // stage2_cost (costs.hpp:139-147)
-      valid = isfinite(st2);
-      bd[0] = cfg.q_track * cs.trk;
-      bd[1] = cfg.q_vnorm * cs.vn;
-      bd[2] = cfg.q_c * cs.mag + cfg.q_c_delta * cs.rate;
-      bd[3] = cs.goal;
-      bd[4] = cs.col;
-    }
+    const double col = collision_sum_warp(env, pl.pos64 + smi * cfg.N * 4, cfg.N, s_terms[wid]);
+    st2 = t.goal + col;  // stage2_cost (costs.hpp:139-147)
+    valid = isfinite(st2);
+    bd[0] = cfg.q_track * t.trk;
+    bd[1] = cfg.q_vnorm * t.vn;
+    bd[2] = cfg.q_c * t.mag + cfg.q_c_delta * t.rate;
+    bd[3] = t.goal;
+    bd[4] = col;
   }
-  pl.stage2[smi] = st2;
-  pl.valid[smi] = valid ? 1 : 0;
-  for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
+  if (lane == 0) {
+    pl.stage2[smi] = st2;
+    pl.valid[smi] = valid ? 1 : 0;
+    for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
+  }
+}
+
+// Latency-path refine: deferred-collision FP64 trajectory per support slot,
+// then a warp per slot for the collision terms.
+__global__ void __launch_bounds__(64) k_refine_traj(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                    UpdateScratch us, int iter) {
+  const unsigned long long n = *us.pair_count;
+  for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < n;
+       w += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const uint2 pr = us.pairs[w];
+    const int64_t smi = pr.x;
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+    const int k = static_cast<int>(us.cand_k[smi * cfg.K + pr.y]);
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    const St<double> x0 = load_state(in.states + 10 * s);
+    double* pos = pl.pos64 + static_cast<int64_t>(w) * cfg.N * 4;
+    CostSums<double> cs;
+    if (in.injected) {
+      cs = rollout_costs<double, PertInjected<double>, true>(
+          x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)}, nullptr, nullptr, pos);
+    } else {
+      const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+      const PertRngD prng{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                          cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+      cs = rollout_costs<double, PertRngD, true>(x0, env, prng, nullptr, nullptr, pos);
+    }
+    pl.tsum[w] = TrajSums{cs.trk, cs.vn, cs.mag, cs.rate, cs.goal, cs.valid ? 1 : 0};
+  }
+}
+
+__global__ void __launch_bounds__(128) k_refine_col(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                    UpdateScratch us) {
+  __shared__ double s_terms[4][64];
+  const unsigned long long n = *us.pair_count;
+  const int wid = threadIdx.x >> 5;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  for (unsigned long long w = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n;
+       w += (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5) {
+    const uint2 pr = us.pairs[w];
+    const int64_t smi = pr.x;
+    const TrajSums t = pl.tsum[w];
+    double val = kInf;
+    if (t.valid) {
+      const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+      const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+      const double col = collision_sum_warp(env, pl.pos64 + static_cast<int64_t>(w) * cfg.N * 4, cfg.N, s_terms[wid]);
+      val = ((cfg.q_track * t.trk + cfg.q_vnorm * t.vn) + (cfg.q_c * t.mag + cfg.q_c_delta * t.rate)) + (t.goal + col);
+    }
+    if ((threadIdx.x & 31) == 0) us.cand_s[smi * cfg.K + pr.y] = val;
+  }
 }
 
 __global__ void k_select(Plan pl, DevConfig cfg, int S) {
@@ -575,13 +668,15 @@ cudaError_t launch_gather(const Plan& pl, const DevConfig& cfg, int S, const Gat
 
 cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
                              int precision, bool want_winner_rollout, uint32_t* cand_k, double* cand_s, double* cand_w,
-                             cudaStream_t st, KernelTimer* timer) {
+                             uint2* pairs, unsigned long long* pair_count, cudaStream_t st, KernelTimer* timer) {
   const int SM = in.S * cfg.M;
   {
     TimedRegion t(timer, "k_anchors", st);
     k_anchors<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
   }
-  const UpdateScratch us{cand_k, cand_s, cand_w};
+  const UpdateScratch us{cand_k, cand_s, cand_w, pairs, pair_count};
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (int iter = 0; iter < cfg.iterations; ++iter) {
     if (precision == 32) {
       cudaError_t e = launch_stage1_f32(in, P, pl, cfg, iter, st, timer);
@@ -592,13 +687,26 @@ cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan&
       TimedRegion t(timer, "k_stage1_f64", st);
       k_stage1_f64<<<SM * tiles, threads, 4 * cfg.N * sizeof(double), st>>>(in, P, pl, cfg, iter);
     }
+    cudaMemsetAsync(pair_count, 0, sizeof(unsigned long long), st);
     {
       TimedRegion t(timer, "k_support", st);
       k_support<<<SM, kSupportThreads, 0, st>>>(pl, cfg, us, precision);
     }
     if (precision == 32) {
-      TimedRegion t(timer, "k_refine", st);
-      k_refine<<<SM, 32, 0, st>>>(in, P, pl, cfg, us, iter);
+      const int64_t total = static_cast<int64_t>(SM) * cfg.K;
+      if (total < kLatencyRollouts) {
+        const int blocks = static_cast<int>((total + 63) / 64);
+        {
+          TimedRegion t(timer, "k_refine_traj", st);
+          k_refine_traj<<<blocks, 64, 0, st>>>(in, P, pl, cfg, us, iter);
+        }
+        TimedRegion t(timer, "k_refine_col", st);
+        k_refine_col<<<static_cast<int>((total * 32 + 127) / 128), 128, 0, st>>>(in, P, pl, cfg, us);
+      } else {
+        const int64_t cap = (total + 63) / 64;
+        TimedRegion t(timer, "k_refine", st);
+        k_refine<<<static_cast<int>(cap < sms * 16 ? cap : sms * 16), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+      }
     }
     {
       TimedRegion t(timer, "k_nominal", st);
@@ -606,8 +714,12 @@ cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan&
     }
   }
   {
-    TimedRegion t(timer, "k_stage2", st);
-    k_stage2<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+    TimedRegion t(timer, "k_stage2_traj", st);
+    k_stage2_traj<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+  }
+  {
+    TimedRegion t(timer, "k_stage2_col", st);
+    k_stage2_col<<<(SM * 32 + 127) / 128, 128, 0, st>>>(in, P, pl, cfg);
   }
   {
     TimedRegion t(timer, "k_select", st);

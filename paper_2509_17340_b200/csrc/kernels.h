@@ -87,7 +87,8 @@ cudaError_t launch_snapshot(const BatchIn& in, const Perception& P, const DevCon
 // scratch arrays for the softmin support.
 cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
                              int precision, bool want_winner_rollout, uint32_t* cand_k, double* cand_s,
-                             double* cand_w, cudaStream_t st, KernelTimer* timer);
+                             double* cand_w, uint2* pairs, unsigned long long* pair_count, cudaStream_t st,
+                             KernelTimer* timer);
 
 // Per-scene winner outputs gathered into dense arrays (any pointer may be null).
 struct GatherOut {

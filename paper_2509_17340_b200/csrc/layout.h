@@ -88,12 +88,22 @@ struct Perception {
   int32_t* n_filtered;         // [S]
   GridMeta* grid;              // [S]
   uint32_t* grid_start;        // [S*(kGridCells+1)] (build scratch)
-  uint4* grid_cell;            // [S*kGridCells] {start, count, box lo, box hi}: points of the
-                               // cell and their bounding box quantised outward to h/255
+  uint4* grid_cell;            // [S*kGridCells] {start, count, box lo, box hi}: the cell's sorted
+                               // points and their box quantised outward to h/255 (cell corner)
   uint32_t* grid_occ;          // [S*kOccWords]
   double* grid_pts64;          // [S*7200*3] sorted by grid cell
   float4* grid_pts32;          // [S*7200]
 };
+
+// Non-collision cost sums of a deferred-collision FP64 rollout (latency path).
+struct TrajSums {
+  double trk, vn, mag, rate, goal;
+  int valid;
+};
+
+// Rollouts up to this count per call run the latency path: sequential
+// trajectory pass + parallel collision pass.
+constexpr int kLatencyRollouts = 148 * 128;
 
 struct Plan {
   // anchors / guides (FP64)
@@ -117,6 +127,10 @@ struct Plan {
   uint8_t* valid;              // [S*M]
   double* breakdown;           // [S*M*5]
   uint32_t* n_support;         // [S*M] softmin support size (diagnostics)
+  // deferred-collision scratch (latency path and stage II)
+  float* pos32;                // [kLatencyRollouts*N*4]
+  double* pos64;               // [max(S*M, kLatencyRollouts)*N*4]
+  TrajSums* tsum;              // [max(S*M, kLatencyRollouts)]
   // per scene
   int32_t* done;               // [S] arrival counter (self-resetting)
   int32_t* winner;             // [S]

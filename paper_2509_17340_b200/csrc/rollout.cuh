@@ -130,9 +130,12 @@ struct PertZero {
 // Rollout with all cost sums.  If states/controls are given the trajectory is
 // written out (winner_rollout); on a non-finite step the remaining entries
 // repeat the last finite state / applied control as rollout_into does.
-template <typename R, typename Pert>
+// kDeferCol: skip the collision queries and store the positions p_0..p_{N-1}
+// (stride 4) to pos_out instead; a collision pass evaluates them in parallel.
+template <typename R, typename Pert, bool kDeferCol = false>
 __device__ __forceinline__ CostSums<R> rollout_costs(St<R> x, const RolloutEnv<R>& env, const Pert& pert,
-                                                      R* states_out = nullptr, R* controls_out = nullptr) {
+                                                      R* states_out = nullptr, R* controls_out = nullptr,
+                                                      R* pos_out = nullptr) {
   CostSums<R> s{R(0), R(0), R(0), R(0), R(0), R(0), true, false};
   const Dyn<R>& dy = env.dyn;
   R up0 = R(0), up1 = R(0), up2 = R(0), up3 = R(0);
@@ -153,7 +156,13 @@ __device__ __forceinline__ CostSums<R> rollout_costs(St<R> x, const RolloutEnv<R
     s.goal = s.goal + env.q_p * norm3(x.p - env.pg);
     s.goal = s.goal + env.q_v * norm3(x.v - env.vg);
     s.goal = s.goal + env.q_q * env.attitude(x.q);
-    s.col = s.col + env.collision(x.p);
+    if constexpr (kDeferCol) {
+      pos_out[4 * j] = x.p.x;
+      pos_out[4 * j + 1] = x.p.y;
+      pos_out[4 * j + 2] = x.p.z;
+    } else {
+      s.col = s.col + env.collision(x.p);
+    }
     // perturbed, clamped control (mppi.cpp:40-45)
     R d[4];
     pert(j, d);
