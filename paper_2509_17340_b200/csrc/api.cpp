@@ -349,12 +349,10 @@ int create_impl(amppi_ctx* ctx) {
   CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(GridMeta)));
   P.grid = static_cast<GridMeta*>(p);
   CK(cudaMemset(P.grid, 0, static_cast<size_t>(S) * sizeof(GridMeta)));
-  CK(A.alloc(&p, static_cast<size_t>(S) * (kGridCells + 1) * sizeof(uint32_t)));
-  P.grid_start = static_cast<uint32_t*>(p);
-  CK(A.alloc(&p, static_cast<size_t>(S) * kGridCells * sizeof(uint4)));
-  P.grid_cell = static_cast<uint4*>(p);
-  CK(A.alloc(&p, static_cast<size_t>(S) * kOccWords * sizeof(uint32_t)));
-  P.grid_occ = static_cast<uint32_t*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kGridCells * 2 * sizeof(uint4)));
+  P.grid_rec = static_cast<uint4*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kPadCells * sizeof(uint32_t)));
+  P.grid_nbr = static_cast<uint32_t*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 3 * sizeof(double)));
   P.grid_pts64 = static_cast<double*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kCells * sizeof(float4)));

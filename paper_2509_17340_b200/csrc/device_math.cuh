@@ -333,105 +333,111 @@ __device__ __forceinline__ R collision_term(R d, R scale, R slope, R dmin, R dma
   return R(0);
 }
 
-// Collision-grid neighbourhood walk: offsets 0, -1, +1 per axis (x outer),
-// so the query's own cell comes first and the branch and bound below prunes
-// early.  Small nested loops keep the kernel's code footprint small.
-__device__ __forceinline__ int nbr_delta(int i) { return i == 0 ? 0 : (i == 1 ? -1 : 1); }
+// Collision-grid queries (replacing ClearanceIndex::nearest,
+// perception.cpp:191-235).  The squared distance to the nearest filtered point
+// is exact whenever the true nearest distance is below d_max: every such point
+// lies in the 27 cells (size h >= d_max) around p, and the padded neighbour
+// mask lists the non-empty ones.  Branch and bound over their float boxes
+// (outward-rounded, so box distance <= point distance in the same arithmetic):
+// own cell first, then the 6 face neighbours, then the rest; a cell is skipped
+// when its box is farther than the best so far or than d_max (its points
+// cannot change the cost); the scan stops once a point is closer than d_min
+// (cost = C for any such d).  Returns +inf when no point is within reach.
 
-__device__ __forceinline__ bool occupancy_maybe_near(const GridMeta& g, const uint32_t* __restrict__ occ, int cx,
-                                                     int cy, int cz) {
-  if (cx < -1 || cy < -1 || cz < -1 || cx > g.dims[0] || cy > g.dims[1] || cz > g.dims[2]) return false;
-  const int oc = ((cx + 1) * (g.dims[1] + 2) + (cy + 1)) * (g.dims[2] + 2) + (cz + 1);
-  return (__ldg(occ + (oc >> 5)) >> (oc & 31)) & 1u;
+// Neighbour bit b = i*9 + j*3 + k -> record index offset relative to
+// cbase = ((cx-1)*D1 + (cy-1))*D2 + (cz-1).
+__device__ __forceinline__ int nbr_offset(int b, int d12, int d2) {
+  const int i = (b * 57) >> 9;  // b / 9 for b < 27
+  const int r = b - 9 * i;
+  const int j = (r * 11) >> 5;  // r / 3 for r < 9
+  return i * d12 + j * d2 + (r - 3 * j);
 }
 
-// Squared distance to the nearest filtered point, exact whenever the true
-// nearest distance is below d_max (every such point lies in the 27 cells of
-// size h >= d_max around p).  Branch and bound over the cells' outward-
-// quantised point boxes: a cell is skipped when its box is farther than the
-// best distance so far or than d_max (its points cannot change the cost);
-// the scan stops once a point is closer than d_min (cost = C for any such d).
-// Returns +inf when no point is within reach.
-__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ cells,
-                                                   const uint32_t* __restrict__ occ, const double* __restrict__ pts,
+// Padded-lattice mask of the query cell (cx, cy, cz); 0 when outside.
+__device__ __forceinline__ uint32_t nbr_mask(const GridMeta& g, const uint32_t* __restrict__ nbr, int cx, int cy,
+                                             int cz) {
+  if (static_cast<unsigned>(cx + 1) > static_cast<unsigned>(g.dims[0] + 1) ||
+      static_cast<unsigned>(cy + 1) > static_cast<unsigned>(g.dims[1] + 1) ||
+      static_cast<unsigned>(cz + 1) > static_cast<unsigned>(g.dims[2] + 1))
+    return 0u;
+  return __ldg(nbr + ((cx + 1) * (g.dims[1] + 2) + (cy + 1)) * (g.dims[2] + 2) + (cz + 1));
+}
+
+__device__ __forceinline__ uint32_t nbr_phase(uint32_t m, int phase) {
+  return m & (phase == 0 ? kNbrCenter : (phase == 1 ? kNbrFaces : ~(kNbrCenter | kNbrFaces)));
+}
+
+__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ rec,
+                                                   const uint32_t* __restrict__ nbr, const double* __restrict__ pts,
                                                    V3<double> p, double lim2, double stop2) {
   double best = __longlong_as_double(0x7ff0000000000000ll);
   if (g.dims[0] == 0) return best;
   const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
   const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
   const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
-  if (!occupancy_maybe_near(g, occ, cx, cy, cz)) return best;
-  const double q = g.h * (1.0 / 255.0);
-  for (int ix = 0; ix < 3; ++ix)
-  for (int iy = 0; iy < 3; ++iy)
-  for (int iz = 0; iz < 3; ++iz) {
-    const int x = cx + nbr_delta(ix), y = cy + nbr_delta(iy), z = cz + nbr_delta(iz);
-    if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
-    const uint4 rec = cells[(x * g.dims[1] + y) * g.dims[2] + z];
-    if (rec.y == 0) continue;
-    const double c0x = g.origin[0] + x * g.h, c0y = g.origin[1] + y * g.h, c0z = g.origin[2] + z * g.h;
-    const double gx = fmax(fmax(c0x + (rec.z & 255u) * q - p.x, p.x - (c0x + (rec.w & 255u) * q)), 0.0);
-    const double gy = fmax(fmax(c0y + ((rec.z >> 8) & 255u) * q - p.y, p.y - (c0y + ((rec.w >> 8) & 255u) * q)), 0.0);
-    const double gz =
-        fmax(fmax(c0z + ((rec.z >> 16) & 255u) * q - p.z, p.z - (c0z + ((rec.w >> 16) & 255u) * q)), 0.0);
-    const double bd2 = gx * gx + gy * gy + gz * gz;
-    if (bd2 > fmin(best, lim2) * (1.0 + 1e-12)) continue;
-    for (uint32_t k = rec.x; k < rec.x + rec.y; ++k) {
-      const V3<double> qq{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]};
-      const double d2 = sqnorm(p - qq);
-      best = d2 < best ? d2 : best;
+  const uint32_t m = nbr_mask(g, nbr, cx, cy, cz);
+  if (!m) return best;
+  const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
+  const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
+  for (int phase = 0; phase < 3; ++phase) {
+    uint32_t mm = nbr_phase(m, phase);
+    while (mm) {
+      const int b = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int c = cbase + nbr_offset(b, d12, d2);
+      const uint4 ra = rec[2 * c], rb = rec[2 * c + 1];
+      const V3<double> lo{__uint_as_float(ra.z), __uint_as_float(ra.w), __uint_as_float(rb.x)};
+      const V3<double> hi{__uint_as_float(rb.y), __uint_as_float(rb.z), __uint_as_float(rb.w)};
+      const V3<double> gap{fmax(fmax(lo.x - p.x, p.x - hi.x), 0.0), fmax(fmax(lo.y - p.y, p.y - hi.y), 0.0),
+                           fmax(fmax(lo.z - p.z, p.z - hi.z), 0.0)};
+      const double bd2 = sqnorm(gap);
+      if (bd2 > fmin(best, lim2) * (1.0 + 1e-12)) continue;
+      for (uint32_t k = ra.x; k < ra.x + ra.y; ++k) {
+        const V3<double> qq{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]};
+        const double dd = sqnorm(p - qq);
+        best = dd < best ? dd : best;
+      }
+      if (best < stop2) return best;
     }
-    if (best < stop2) return best;
   }
   return best;
 }
 
-__device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4* __restrict__ cells,
-                                                 const uint32_t* __restrict__ occ, const float4* __restrict__ pts,
+__device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4* __restrict__ rec,
+                                                 const uint32_t* __restrict__ nbr, const float4* __restrict__ pts,
                                                  V3<float> p, float lim2, float stop2) {
   float best = __int_as_float(0x7f800000);
   if (g.dims[0] == 0) return best;
-  const float fx = (p.x - g.origin_f[0]) * g.inv_h_f;
-  const float fy = (p.y - g.origin_f[1]) * g.inv_h_f;
-  const float fz = (p.z - g.origin_f[2]) * g.inv_h_f;
-  const int cx = __float2int_rd(fx), cy = __float2int_rd(fy), cz = __float2int_rd(fz);
+  const int cx = __float2int_rd((p.x - g.origin_f[0]) * g.inv_h_f);
+  const int cy = __float2int_rd((p.y - g.origin_f[1]) * g.inv_h_f);
+  const int cz = __float2int_rd((p.z - g.origin_f[2]) * g.inv_h_f);
   AMPPI_STAT(0, 1);
-  if (!occupancy_maybe_near(g, occ, cx, cy, cz)) return best;
+  const uint32_t m = nbr_mask(g, nbr, cx, cy, cz);
+  if (!m) return best;
   AMPPI_STAT(1, 1);
-  // p relative to the query cell's corner, in box quanta (1/255 cell)
-  const float rx = (fx - static_cast<float>(cx)) * 255.f, ry = (fy - static_cast<float>(cy)) * 255.f,
-              rz = (fz - static_cast<float>(cz)) * 255.f;
-  const float q2 = g.h_f * g.h_f * (1.f / (255.f * 255.f));
-  const float lim = lim2 / q2;  // thresholds in quanta^2
-  for (int ix = 0; ix < 3; ++ix)
-  for (int iy = 0; iy < 3; ++iy)
-  for (int iz = 0; iz < 3; ++iz) {
-    const int ox = nbr_delta(ix), oy = nbr_delta(iy), oz = nbr_delta(iz);
-    const int x = cx + ox, y = cy + oy, z = cz + oz;
-    if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
-    const uint4 rec = __ldg(cells + (x * g.dims[1] + y) * g.dims[2] + z);
-    AMPPI_STAT(2, 1);
-    if (rec.y == 0) continue;
-    // box in quanta relative to the query cell's corner (+-1 quantum of slack)
-    const float bx0 = static_cast<float>(ox * 255 + static_cast<int>(rec.z & 255u)) - 1.f;
-    const float bx1 = static_cast<float>(ox * 255 + static_cast<int>(rec.w & 255u)) + 1.f;
-    const float by0 = static_cast<float>(oy * 255 + static_cast<int>((rec.z >> 8) & 255u)) - 1.f;
-    const float by1 = static_cast<float>(oy * 255 + static_cast<int>((rec.w >> 8) & 255u)) + 1.f;
-    const float bz0 = static_cast<float>(oz * 255 + static_cast<int>((rec.z >> 16) & 255u)) - 1.f;
-    const float bz1 = static_cast<float>(oz * 255 + static_cast<int>((rec.w >> 16) & 255u)) + 1.f;
-    const float gx = fmaxf(fmaxf(bx0 - rx, rx - bx1), 0.f);
-    const float gy = fmaxf(fmaxf(by0 - ry, ry - by1), 0.f);
-    const float gz = fmaxf(fmaxf(bz0 - rz, rz - bz1), 0.f);
-    const float bd2 = gx * gx + gy * gy + gz * gz;
-    if (bd2 >= fminf(best / q2, lim)) continue;
-    AMPPI_STAT(3, 1);
-    AMPPI_STAT(4, rec.y);
-    for (uint32_t k = rec.x; k < rec.x + rec.y; ++k) {
-      const float4 qq = __ldg(pts + k);
-      const float dx = p.x - qq.x, dy = p.y - qq.y, dz = p.z - qq.z;
-      best = fminf(best, dx * dx + dy * dy + dz * dz);
+  const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
+  const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
+#pragma unroll 1
+  for (int phase = 0; phase < 3; ++phase) {
+    uint32_t mm = nbr_phase(m, phase);
+    while (mm) {
+      const int b = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int c = cbase + nbr_offset(b, d12, d2);
+      const uint4 ra = __ldg(rec + 2 * c), rb = __ldg(rec + 2 * c + 1);
+      AMPPI_STAT(2, 1);
+      const V3<float> gap{fmaxf(fmaxf(__uint_as_float(ra.z) - p.x, p.x - __uint_as_float(rb.y)), 0.f),
+                          fmaxf(fmaxf(__uint_as_float(ra.w) - p.y, p.y - __uint_as_float(rb.z)), 0.f),
+                          fmaxf(fmaxf(__uint_as_float(rb.x) - p.z, p.z - __uint_as_float(rb.w)), 0.f)};
+      if (sqnorm(gap) >= fminf(best, lim2)) continue;
+      AMPPI_STAT(3, 1);
+      AMPPI_STAT(4, ra.y);
+      for (uint32_t k = ra.x; k < ra.x + ra.y; ++k) {
+        const float4 qq = __ldg(pts + k);
+        best = fminf(best, sqnorm(V3<float>{p.x - qq.x, p.y - qq.y, p.z - qq.z}));
+      }
+      if (best < stop2) return best;
     }
-    if (best < stop2) return best;
   }
   return best;
 }

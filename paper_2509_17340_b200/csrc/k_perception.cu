@@ -173,7 +173,7 @@ constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 struct FinalizeSmem {
   double rng[kCells];  // also the u64 range-bits table during fused keying, and
   uint32_t idx[kCells];  // (rng..idx, 86 KB) the sort keys / values of the grid build
-  uint32_t occ[kOccWords];
+  uint32_t rows[kGridAxis * kGridAxis];  // non-empty grid cells: bit z of row (x, y)
   uint32_t warp_sums[kFinalizeThreads / 32];
   double bbox_lo[kFinalizeThreads / 32][3];
   double bbox_hi[kFinalizeThreads / 32][3];
@@ -220,7 +220,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   const int tid = threadIdx.x;
   const int64_t cell_base = static_cast<int64_t>(s) * kCells;
   const int64_t pt_base = in.offsets[s];
-  for (int w = tid; w < kOccWords; w += blockDim.x) sm.occ[w] = 0u;
+  for (int w = tid; w < kGridAxis * kGridAxis; w += blockDim.x) sm.rows[w] = 0u;
   if (P.ranges)
     for (int f = tid; f < kCells; f += blockDim.x) {
       P.ranges[cell_base + f] = sm.rng[f];
@@ -334,14 +334,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   }
   __syncthreads();
   const GridMeta meta = sm.meta;
-  const int ncell = meta.dims[0] * meta.dims[1] * meta.dims[2];
-  uint32_t* __restrict__ gstart = P.grid_start + static_cast<int64_t>(s) * (kGridCells + 1);
-  uint32_t* __restrict__ gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
-  if (n_pts == 0) {
-    for (int w = tid; w < kOccWords; w += blockDim.x) gocc[w] = 0u;
-    if (tid == 0) gstart[0] = 0u;
-    return;
-  }
+  if (n_pts == 0) return;  // dims = 0: every query returns +inf
 
   // collision grid: sort the filtered points by (cell, Morton code of the
   // 1/8-cell sub-position) with a block bitonic sort in shared memory (the
@@ -379,7 +372,6 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     keys[k] = key;
     vals[k] = static_cast<uint16_t>(k);
   }
-  for (int w = tid; w < kOccWords; w += blockDim.x) sm.occ[w] = 0u;
   __syncthreads();
   for (uint32_t size = 2; size <= n2; size <<= 1)
     for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
@@ -398,13 +390,11 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       }
       __syncthreads();
     }
-  // scatter into sorted order; cell ranges from the key boundaries; dilated
-  // occupancy over the padded (dims+2)^3 lattice
+  // scatter into sorted order; per non-empty cell its record (point range and
+  // float box rounded outward from FP64) and its bit in the row table
   double* __restrict__ gp64 = P.grid_pts64 + cell_base * 3;
   float4* __restrict__ gp32 = P.grid_pts32 + cell_base;
-  uint4* __restrict__ gcell = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
-  for (int c = tid; c < ncell; c += blockDim.x) gcell[c] = make_uint4(0u, 0u, 0u, 0u);
-  __syncthreads();
+  uint4* __restrict__ grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
   for (uint32_t i = tid; i < n_pts; i += blockDim.x) {
     const uint32_t k = vals[i];
     const double x = filt[3 * k], y = filt[3 * k + 1], z = filt[3 * k + 2];
@@ -414,49 +404,47 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     gp32[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.f);
     const uint32_t c = keys[i] >> 9;
     if (i == 0 || (keys[i - 1] >> 9) != c) {  // first point of cell c
+      double blo[3] = {x, y, z}, bhi[3] = {x, y, z};
       uint32_t e = i + 1;
-      while (e < n_pts && (keys[e] >> 9) == c) ++e;
-      gcell[c].x = i;
-      gcell[c].y = e - i;
+      for (; e < n_pts && (keys[e] >> 9) == c; ++e) {
+        const uint32_t ke = vals[e];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          blo[a] = fmin(blo[a], filt[3 * ke + a]);
+          bhi[a] = fmax(bhi[a], filt[3 * ke + a]);
+        }
+      }
+      grec[2 * c] = make_uint4(i, e - i, __float_as_uint(__double2float_rd(blo[0])),
+                               __float_as_uint(__double2float_rd(blo[1])));
+      grec[2 * c + 1] = make_uint4(__float_as_uint(__double2float_rd(blo[2])), __float_as_uint(__double2float_ru(bhi[0])),
+                                   __float_as_uint(__double2float_ru(bhi[1])), __float_as_uint(__double2float_ru(bhi[2])));
       const int cz = static_cast<int>(c % meta.dims[2]);
-      const int cy = static_cast<int>((c / meta.dims[2]) % meta.dims[1]);
-      const int cx = static_cast<int>(c / (meta.dims[2] * meta.dims[1]));
-      const int py = meta.dims[1] + 2, pz = meta.dims[2] + 2;
-      for (int dx = 0; dx < 3; ++dx)
-        for (int dy = 0; dy < 3; ++dy)
-          for (int dz = 0; dz < 3; ++dz) {
-            const int oc = ((cx + dx) * py + (cy + dy)) * pz + (cz + dz);
-            atomicOr(&sm.occ[oc >> 5], 1u << (oc & 31));
-          }
+      const int cxy = static_cast<int>(c / meta.dims[2]);  // x * dims[1] + y
+      atomicOr(&sm.rows[cxy], 1u << cz);
     }
   }
   __syncthreads();
-  for (int w = tid; w < kOccWords; w += blockDim.x) gocc[w] = sm.occ[w];
-  // per-cell point boxes relative to the cell corner, quantised outward to
-  // h/255 with one extra quantum of slack
-  const double quanta = 255.0 * meta.inv_h;
-  for (int c = tid; c < ncell; c += blockDim.x) {
-    const uint4 rec = gcell[c];
-    if (rec.y == 0) continue;
-    const int cz = c % meta.dims[2], cy = (c / meta.dims[2]) % meta.dims[1], cx = c / (meta.dims[2] * meta.dims[1]);
-    const int cc[3] = {cx, cy, cz};
-    double blo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, bhi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
-    for (uint32_t k = rec.x; k < rec.x + rec.y; ++k)
-      for (int a = 0; a < 3; ++a) {
-        blo[a] = fmin(blo[a], gp64[3 * k + a]);
-        bhi[a] = fmax(bhi[a], gp64[3 * k + a]);
+  // neighbour masks over the padded lattice: bit i*9+j*3+k of padded cell
+  // (x, y, z) <-> grid cell (x-2+i, y-2+j, z-2+k) is non-empty
+  uint32_t* __restrict__ gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  const int p1 = meta.dims[1] + 2, p2 = meta.dims[2] + 2;
+  const int npad = (meta.dims[0] + 2) * p1 * p2;
+  for (int c = tid; c < npad; c += blockDim.x) {
+    const int z = c % p2, y = (c / p2) % p1, x = c / (p2 * p1);
+    uint32_t m = 0u;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int ux = x - 2 + i;
+      if (ux < 0 || ux >= meta.dims[0]) continue;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int uy = y - 2 + j;
+        if (uy < 0 || uy >= meta.dims[1]) continue;
+        const uint32_t r = sm.rows[ux * meta.dims[1] + uy] << 2;
+        m |= ((r >> z) & 7u) << (i * 9 + j * 3);
       }
-    uint32_t ql = 0u, qh = 0u;
-    for (int a = 0; a < 3; ++a) {
-      const double corner = meta.origin[a] + cc[a] * meta.h;
-      double fl = floor((blo[a] - corner) * quanta) - 1.0;
-      double fh = ceil((bhi[a] - corner) * quanta) + 1.0;
-      fl = fl < 0.0 ? 0.0 : (fl > 255.0 ? 255.0 : fl);
-      fh = fh < 0.0 ? 0.0 : (fh > 255.0 ? 255.0 : fh);
-      ql |= static_cast<uint32_t>(fl) << (8 * a);
-      qh |= static_cast<uint32_t>(fh) << (8 * a);
     }
-    gcell[c] = make_uint4(rec.x, rec.y, ql, qh);
+    gnbr[c] = m;
   }
 }
 

@@ -81,9 +81,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   env.cdmin = static_cast<float>(cfg.col_d_min);
   env.cdmax = static_cast<float>(cfg.col_d_max);
   env.grid = P.grid[s];
-  env.gcells = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
 
-  env.gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
+  env.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
   env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   env.has_guide = true;
   env.abort_above = s_bound;
@@ -186,9 +186,9 @@ __global__ void __launch_bounds__(128) k_stage1_col32(Perception P, Plan pl, Dev
   if (!isfinite(base)) return;  // invalid rollout or dead instance
   const int s = static_cast<int>(r / (static_cast<int64_t>(cfg.M) * cfg.K));
   const GridMeta g = P.grid[s];
-  const uint4* cells = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  const uint4* cells = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
 
-  const uint32_t* occ = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
+  const uint32_t* occ = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
   const float4* pts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   const float cs = static_cast<float>(cfg.col_scale), ca = static_cast<float>(cfg.col_slope);
   const float dmin = static_cast<float>(cfg.col_d_min), dmax = static_cast<float>(cfg.col_d_max);

@@ -248,9 +248,9 @@ __device__ __forceinline__ RolloutEnv<double> make_env64(const BatchIn& in, cons
   e.cdmin = cfg.col_d_min;
   e.cdmax = cfg.col_d_max;
   e.grid = P.grid[s];
-  e.gcells = P.grid_cell + static_cast<int64_t>(s) * kGridCells;
+  e.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
 
-  e.gocc = P.grid_occ + static_cast<int64_t>(s) * kOccWords;
+  e.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
   e.gpts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
   e.has_guide = true;
   e.abort_above = __longlong_as_double(0x7ff0000000000000ll);

@@ -18,10 +18,17 @@ constexpr double kMinPointRange = 0.05;
 constexpr double kHorizonReach = 25.0;
 
 // Collision grid: at most kGridAxis cells per axis, cell size >= d_max.
+// Every cell owns a 32-byte record (two uint4: {start, count, lo.x, lo.y},
+// {lo.z, hi.x, hi.y, hi.z}; the float box holds the cell's points, rounded
+// outward from FP64).  The padded lattice (dims+2)^3 holds, per cell, the
+// 27-bit mask of its non-empty neighbours (bit i*9+j*3+k <-> offset
+// (i-1, j-1, k-1)); mask 0 = no point within one cell.
 constexpr int kGridAxis = 24;
 constexpr int kGridCells = kGridAxis * kGridAxis * kGridAxis;
-constexpr int kOccAxis = kGridAxis + 2;
-constexpr int kOccWords = (kOccAxis * kOccAxis * kOccAxis + 31) / 32;
+constexpr int kPadAxis = kGridAxis + 2;
+constexpr int kPadCells = kPadAxis * kPadAxis * kPadAxis;
+constexpr uint32_t kNbrCenter = 1u << 13;
+constexpr uint32_t kNbrFaces = (1u << 4) | (1u << 10) | (1u << 12) | (1u << 14) | (1u << 16) | (1u << 22);
 
 constexpr uint64_t kEmptyCell = 0xFFFFFFFFFFFFFFFFull;  // > bits of any finite positive double
 
@@ -87,10 +94,8 @@ struct Perception {
   double* safe_point;          // [S*600]
   int32_t* n_filtered;         // [S]
   GridMeta* grid;              // [S]
-  uint32_t* grid_start;        // [S*(kGridCells+1)] (build scratch)
-  uint4* grid_cell;            // [S*kGridCells] {start, count, box lo, box hi}: the cell's sorted
-                               // points and their box quantised outward to h/255 (cell corner)
-  uint32_t* grid_occ;          // [S*kOccWords]
+  uint4* grid_rec;             // [S*kGridCells*2] cell records (written for non-empty cells only)
+  uint32_t* grid_nbr;          // [S*kPadCells] neighbour masks over the padded lattice
   double* grid_pts64;          // [S*7200*3] sorted by grid cell
   float4* grid_pts32;          // [S*7200]
 };

@@ -35,8 +35,8 @@ struct RolloutEnv<double> {
   double q_p, q_v, q_q;
   double cs, ca, cdmin, cdmax;
   GridMeta grid;
-  const uint4* gcells;
-  const uint32_t* gocc;
+  const uint4* grec;
+  const uint32_t* gnbr;
   const double* gpts;
   bool has_guide;
   double abort_above;
@@ -47,7 +47,7 @@ struct RolloutEnv<double> {
   __device__ __forceinline__ double unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ double attitude(Q4<double> q) const { return attitude_err_exact(q, gt); }
   __device__ __forceinline__ double collision(V3<double> p) const {
-    const double d2 = nearest_sq_exact(grid, gcells, gocc, gpts, p, cdmax * cdmax, cdmin * cdmin);
+    const double d2 = nearest_sq_exact(grid, grec, gnbr, gpts, p, cdmax * cdmax, cdmin * cdmin);
     return collision_term(sqrt(d2), cs, ca, cdmin, cdmax);
   }
 };
@@ -63,8 +63,8 @@ struct RolloutEnv<float> {
   float q_p, q_v, q_q;
   float cs, ca, cdmin, cdmax;
   GridMeta grid;
-  const uint4* gcells;
-  const uint32_t* gocc;
+  const uint4* grec;
+  const uint32_t* gnbr;
   const float4* gpts;
   bool has_guide;
   float abort_above;
@@ -77,7 +77,7 @@ struct RolloutEnv<float> {
   __device__ __forceinline__ float unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ float attitude(Q4<float> q) const { return attitude_err_fast(q, qg); }
   __device__ __forceinline__ float collision(V3<float> p) const {
-    const float d2 = nearest_sq_fast(grid, gcells, gocc, gpts, p, cdmax * cdmax * 1.0001f, cdmin * cdmin);
+    const float d2 = nearest_sq_fast(grid, grec, gnbr, gpts, p, cdmax * cdmax * 1.0001f, cdmin * cdmin);
     return collision_term(sqrtf(d2), cs, ca, cdmin, cdmax);
   }
 };
