@@ -353,6 +353,8 @@ int create_impl(amppi_ctx* ctx) {
   P.grid_rec = static_cast<uint4*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kPadCells * sizeof(uint32_t)));
   P.grid_nbr = static_cast<uint32_t*>(p);
+  CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 2 * sizeof(uint4)));
+  P.grid_leaf = static_cast<uint4*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kCells * 3 * sizeof(double)));
   P.grid_pts64 = static_cast<double*>(p);
   CK(A.alloc(&p, static_cast<size_t>(S) * kCells * sizeof(float4)));

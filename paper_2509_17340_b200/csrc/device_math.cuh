@@ -17,9 +17,13 @@
 namespace amppi_dev {
 
 #ifdef AMPPI_STATS
-// Query statistics (stats builds only): queries, queries past the occupancy
-// bit, cell records tested, cells scanned, points scanned.
-__device__ unsigned long long g_query_stats[5];
+// Query statistics (stats builds only): [0] queries, [1] queries with a
+// non-empty neighbourhood, [2] cell records tested, [3] cells scanned,
+// [4] points scanned, [5]/[6] queries ending with / without a point within
+// reach, [7] points scanned by queries without one; [8 + j] live screening
+// lanes at step j.
+constexpr int kStatSlots = 8 + 64;
+__device__ unsigned long long g_query_stats[kStatSlots];
 #define AMPPI_STAT(i, v) atomicAdd(&g_query_stats[i], static_cast<unsigned long long>(v))
 #else
 #define AMPPI_STAT(i, v) ((void)0)
@@ -368,10 +372,16 @@ __device__ __forceinline__ uint32_t nbr_phase(uint32_t m, int phase) {
 }
 
 __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ rec,
-                                                   const uint32_t* __restrict__ nbr, const double* __restrict__ pts,
-                                                   V3<double> p, double lim2, double stop2) {
+                                                   const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
+                                                   const double* __restrict__ pts, V3<double> p, double lim2,
+                                                   double stop2, uint32_t* hint) {
   double best = __longlong_as_double(0x7ff0000000000000ll);
   if (g.dims[0] == 0) return best;
+  uint32_t bi = *hint;
+  if (bi != kNoHint) {
+    best = sqnorm(p - V3<double>{pts[3 * bi], pts[3 * bi + 1], pts[3 * bi + 2]});
+    if (best < stop2) return best;
+  }
   const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
   const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
   const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
@@ -379,6 +389,15 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
   if (!m) return best;
   const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
   const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
+  // box lower bounds in the same arithmetic as the point distances (sqnorm of
+  // a difference), so box distance <= point distance; the 1e-12 slack only
+  // guards the lim2 comparison
+  auto box_d2 = [&](uint32_t lx, uint32_t ly, uint32_t lz, uint32_t hx, uint32_t hy, uint32_t hz) {
+    const V3<double> lo{__uint_as_float(lx), __uint_as_float(ly), __uint_as_float(lz)};
+    const V3<double> hi{__uint_as_float(hx), __uint_as_float(hy), __uint_as_float(hz)};
+    return sqnorm(V3<double>{fmax(fmax(lo.x - p.x, p.x - hi.x), 0.0), fmax(fmax(lo.y - p.y, p.y - hi.y), 0.0),
+                             fmax(fmax(lo.z - p.z, p.z - hi.z), 0.0)});
+  };
   for (int phase = 0; phase < 3; ++phase) {
     uint32_t mm = nbr_phase(m, phase);
     while (mm) {
@@ -386,28 +405,53 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
       mm &= mm - 1;
       const int c = cbase + nbr_offset(b, d12, d2);
       const uint4 ra = rec[2 * c], rb = rec[2 * c + 1];
-      const V3<double> lo{__uint_as_float(ra.z), __uint_as_float(ra.w), __uint_as_float(rb.x)};
-      const V3<double> hi{__uint_as_float(rb.y), __uint_as_float(rb.z), __uint_as_float(rb.w)};
-      const V3<double> gap{fmax(fmax(lo.x - p.x, p.x - hi.x), 0.0), fmax(fmax(lo.y - p.y, p.y - hi.y), 0.0),
-                           fmax(fmax(lo.z - p.z, p.z - hi.z), 0.0)};
-      const double bd2 = sqnorm(gap);
-      if (bd2 > fmin(best, lim2) * (1.0 + 1e-12)) continue;
-      for (uint32_t k = ra.x; k < ra.x + ra.y; ++k) {
-        const V3<double> qq{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]};
-        const double dd = sqnorm(p - qq);
-        best = dd < best ? dd : best;
+      if (box_d2(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
+      const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
+      const uint4* lf = leaves + 2 * ra.y;
+      for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
+        const uint4 la = lf[0], lb = lf[1];
+        if (box_d2(la.x, la.y, la.z, lb.x, lb.y, lb.z) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
+        const uint32_t te = min(t + kLeafSize, k1);
+        for (uint32_t k = t; k < te; ++k) {
+          const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
+          if (dd < best) {
+            best = dd;
+            bi = k;
+          }
+        }
+        if (best < stop2) {
+          *hint = bi;
+          return best;
+        }
       }
-      if (best < stop2) return best;
     }
   }
+  *hint = bi;
   return best;
 }
 
+// FP32 screening query: as nearest_sq_exact, plus a second branch-and-bound
+// level over each scanned cell's 16-point leaves (float leaf boxes).  Returns
+// the exact squared distance when it lies in [stop2, lim2); any value below
+// stop2 once a point closer than sqrt(stop2) is found (with stop2 = lim2 this
+// is an existence test for a point within reach); >= lim2 (or +inf) when no
+// point is closer than sqrt(lim2).  *hint (a point index, kNoHint for none)
+// seeds the search with that point's distance -- an upper bound on the
+// minimum, so every box at least that far is pruned from the start -- and
+// receives the nearest point found (the previous step's nearest point is a
+// good seed for the next step of the same rollout).
 __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4* __restrict__ rec,
-                                                 const uint32_t* __restrict__ nbr, const float4* __restrict__ pts,
-                                                 V3<float> p, float lim2, float stop2) {
+                                                 const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
+                                                 const float4* __restrict__ pts, V3<float> p, float lim2, float stop2,
+                                                 uint32_t* hint) {
   float best = __int_as_float(0x7f800000);
   if (g.dims[0] == 0) return best;
+  uint32_t bi = *hint;
+  if (bi != kNoHint) {
+    const float4 qq = __ldg(pts + bi);
+    best = sqnorm(V3<float>{p.x - qq.x, p.y - qq.y, p.z - qq.z});
+    if (best < stop2) return best;
+  }
   const int cx = __float2int_rd((p.x - g.origin_f[0]) * g.inv_h_f);
   const int cy = __float2int_rd((p.y - g.origin_f[1]) * g.inv_h_f);
   const int cz = __float2int_rd((p.z - g.origin_f[2]) * g.inv_h_f);
@@ -415,6 +459,12 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
   const uint32_t m = nbr_mask(g, nbr, cx, cy, cz);
   if (!m) return best;
   AMPPI_STAT(1, 1);
+#ifdef AMPPI_STATS
+  uint32_t q_scanned = 0;
+#define AMPPI_QEND(v) (AMPPI_STAT((v) < lim2 ? 5 : 6, 1), AMPPI_STAT(7, (v) < lim2 ? 0u : q_scanned), (v))
+#else
+#define AMPPI_QEND(v) (v)
+#endif
   const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
   const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
 #pragma unroll 1
@@ -431,15 +481,37 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
                           fmaxf(fmaxf(__uint_as_float(rb.x) - p.z, p.z - __uint_as_float(rb.w)), 0.f)};
       if (sqnorm(gap) >= fminf(best, lim2)) continue;
       AMPPI_STAT(3, 1);
-      AMPPI_STAT(4, ra.y);
-      for (uint32_t k = ra.x; k < ra.x + ra.y; ++k) {
-        const float4 qq = __ldg(pts + k);
-        best = fminf(best, sqnorm(V3<float>{p.x - qq.x, p.y - qq.y, p.z - qq.z}));
+      const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
+      const uint4* lf = leaves + 2 * ra.y;
+      for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
+        const uint4 la = __ldg(lf), lb = __ldg(lf + 1);
+        const V3<float> lg{fmaxf(fmaxf(__uint_as_float(la.x) - p.x, p.x - __uint_as_float(lb.x)), 0.f),
+                           fmaxf(fmaxf(__uint_as_float(la.y) - p.y, p.y - __uint_as_float(lb.y)), 0.f),
+                           fmaxf(fmaxf(__uint_as_float(la.z) - p.z, p.z - __uint_as_float(lb.z)), 0.f)};
+        if (sqnorm(lg) >= fminf(best, lim2)) continue;
+        const uint32_t te = min(t + kLeafSize, k1);
+        AMPPI_STAT(4, te - t);
+#ifdef AMPPI_STATS
+        q_scanned += te - t;
+#endif
+        for (uint32_t u = t; u < te; ++u) {
+          const float4 qq = __ldg(pts + u);
+          const float dd = sqnorm(V3<float>{p.x - qq.x, p.y - qq.y, p.z - qq.z});
+          if (dd < best) {
+            best = dd;
+            bi = u;
+          }
+        }
+        if (best < stop2) {
+          *hint = bi;
+          return AMPPI_QEND(best);
+        }
       }
-      if (best < stop2) return best;
     }
   }
-  return best;
+  *hint = bi;
+  return AMPPI_QEND(best);
+#undef AMPPI_QEND
 }
 
 }  // namespace amppi_dev

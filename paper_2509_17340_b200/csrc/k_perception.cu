@@ -390,11 +390,15 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       }
       __syncthreads();
     }
-  // scatter into sorted order; per non-empty cell its record (point range and
-  // float box rounded outward from FP64) and its bit in the row table
+  // scatter into sorted order and flag leaf starts: every cell's points form
+  // leaves of kLeafSize consecutive (Morton-ordered) points
   double* __restrict__ gp64 = P.grid_pts64 + cell_base * 3;
   float4* __restrict__ gp32 = P.grid_pts32 + cell_base;
   uint4* __restrict__ grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+  uint4* __restrict__ gleaf = P.grid_leaf + cell_base * 2;
+  uint8_t* lflag = reinterpret_cast<uint8_t*>(vals + kCellsPow2);  // [8192] (inside rng, past keys/vals)
+  for (uint32_t i = tid; i < kCellsPow2; i += blockDim.x) lflag[i] = 0;
+  __syncthreads();
   for (uint32_t i = tid; i < n_pts; i += blockDim.x) {
     const uint32_t k = vals[i];
     const double x = filt[3 * k], y = filt[3 * k + 1], z = filt[3 * k + 2];
@@ -404,24 +408,53 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     gp32[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.f);
     const uint32_t c = keys[i] >> 9;
     if (i == 0 || (keys[i - 1] >> 9) != c) {  // first point of cell c
-      double blo[3] = {x, y, z}, bhi[3] = {x, y, z};
       uint32_t e = i + 1;
-      for (; e < n_pts && (keys[e] >> 9) == c; ++e) {
-        const uint32_t ke = vals[e];
+      while (e < n_pts && (keys[e] >> 9) == c) ++e;
+      for (uint32_t t = i; t < e; t += kLeafSize) lflag[t] = 1;
+      atomicOr(&sm.rows[c / meta.dims[2]], 1u << (c % meta.dims[2]));  // row x*dims[1]+y, bit z
+    }
+  }
+  __syncthreads();
+  // leaf ids = prefix count of leaf starts (contiguous 16-point chunks per thread)
+  constexpr uint32_t kPerThread = kCellsPow2 / kFinalizeThreads;
+  static_assert(kPerThread * kFinalizeThreads == kCellsPow2, "chunking");
+  const uint32_t i0 = tid * kPerThread;
+  uint32_t n_leaf_starts = 0;
+  for (uint32_t i = i0; i < i0 + kPerThread; ++i) n_leaf_starts += lflag[i];
+  uint32_t leaf = block_exclusive_scan(n_leaf_starts, sm.warp_sums, &sm.total);
+  for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
+    if (!lflag[i]) continue;
+    const uint32_t c = keys[i] >> 9;
+    double llo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, lhi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    uint32_t t = i;
+    do {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        llo[a] = fmin(llo[a], gp64[3 * t + a]);
+        lhi[a] = fmax(lhi[a], gp64[3 * t + a]);
+      }
+      ++t;
+    } while (t < n_pts && !lflag[t]);
+    gleaf[2 * leaf] = make_uint4(__float_as_uint(__double2float_rd(llo[0])), __float_as_uint(__double2float_rd(llo[1])),
+                                 __float_as_uint(__double2float_rd(llo[2])), 0u);
+    gleaf[2 * leaf + 1] = make_uint4(__float_as_uint(__double2float_ru(lhi[0])),
+                                     __float_as_uint(__double2float_ru(lhi[1])),
+                                     __float_as_uint(__double2float_ru(lhi[2])), 0u);
+    if (i == 0 || (keys[i - 1] >> 9) != c) {  // cell record: points, first leaf, float box
+      uint32_t e = i + 1;
+      double blo[3] = {gp64[3 * i], gp64[3 * i + 1], gp64[3 * i + 2]}, bhi[3] = {blo[0], blo[1], blo[2]};
+      for (; e < n_pts && (keys[e] >> 9) == c; ++e)
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          blo[a] = fmin(blo[a], filt[3 * ke + a]);
-          bhi[a] = fmax(bhi[a], filt[3 * ke + a]);
+          blo[a] = fmin(blo[a], gp64[3 * e + a]);
+          bhi[a] = fmax(bhi[a], gp64[3 * e + a]);
         }
-      }
-      grec[2 * c] = make_uint4(i, e - i, __float_as_uint(__double2float_rd(blo[0])),
+      grec[2 * c] = make_uint4(i | ((e - i) << 16), leaf, __float_as_uint(__double2float_rd(blo[0])),
                                __float_as_uint(__double2float_rd(blo[1])));
       grec[2 * c + 1] = make_uint4(__float_as_uint(__double2float_rd(blo[2])), __float_as_uint(__double2float_ru(bhi[0])),
                                    __float_as_uint(__double2float_ru(bhi[1])), __float_as_uint(__double2float_ru(bhi[2])));
-      const int cz = static_cast<int>(c % meta.dims[2]);
-      const int cxy = static_cast<int>(c / meta.dims[2]);  // x * dims[1] + y
-      atomicOr(&sm.rows[cxy], 1u << cz);
     }
+    ++leaf;
   }
   __syncthreads();
   // neighbour masks over the padded lattice: bit i*9+j*3+k of padded cell

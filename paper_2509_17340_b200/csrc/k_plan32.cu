@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 
+
 #include "kernels.h"
 #include "rollout.cuh"
 
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
 
   env.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  env.gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
   env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   env.has_guide = true;
   env.abort_above = s_bound;
@@ -112,6 +114,219 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   *out = cs.aborted ? 3.4028234663852886e38f
                     : cs.valid ? stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd)
                                : __int_as_float(0x7f800000);
+}
+
+// One screening step j of a rollout (the loop body of rollout_costs<float>):
+// costs on states[j], perturbed clamped control, control costs, the
+// partial-cost bound, RK4.  Returns 0 (continue), 1 (aborted), 2 (invalid).
+// The collision query runs last and knows the partial cost, so it only has
+// to find one point inside the radius whose collision term would exhaust the
+// remaining budget (then the sample aborts); otherwise it returns the exact
+// distance.  Same sums in the same order as rollout_costs for every sample
+// that is not aborted.
+template <typename Pert>
+__device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, float (&up)[4], int j,
+                                           const RolloutEnv<float>& env, const Pert& pert) {
+  const Dyn<float>& dy = env.dyn;
+  const int N = env.N;
+  AMPPI_STAT(8 + j, 1);
+  s.trk = s.trk + norm3(x.p - env.guide_at(j));
+  s.vn = s.vn + sqnorm(x.v);
+  s.goal = s.goal + env.q_p * norm3(x.p - env.pg);
+  s.goal = s.goal + env.q_v * norm3(x.v - env.vg);
+  s.goal = s.goal + env.q_q * env.attitude(x.q);
+  float d[4];
+  pert(j, d);
+  const float u0 = clampv(env.unom_at(j, 0) + d[0], dy.tmin, dy.tmax);
+  const float u1 = clampv(env.unom_at(j, 1) + d[1], -dy.wxy, dy.wxy);
+  const float u2 = clampv(env.unom_at(j, 2) + d[2], -dy.wxy, dy.wxy);
+  const float u3 = clampv(env.unom_at(j, 3) + d[3], -dy.wz, dy.wz);
+  if (j + 1 < N) {
+    s.mag = s.mag + (((u0 * u0 + u1 * u1) + u2 * u2) + u3 * u3);
+    if (j >= 1) {
+      const float e0 = u0 - up[0], e1 = u1 - up[1], e2 = u2 - up[2], e3 = u3 - up[3];
+      s.rate = s.rate + (((e0 * e0 + e1 * e1) + e2 * e2) + e3 * e3);
+    }
+  }
+  up[0] = u0; up[1] = u1; up[2] = u2; up[3] = u3;
+  const float part =
+      ((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col);
+  if (part > env.abort_above) return 1;
+  // Abort radius: a point closer than d_thr adds more than the remaining
+  // budget (C exp(-a (d_thr - d_min)) = budget e^0.001), so finding one ends
+  // the sample; otherwise the query returns the exact distance (>= d_thr).
+  const float lim2 = env.cdmax * env.cdmax * 1.0001f;
+  float stop2 = env.cdmin * env.cdmin;
+  bool abortable = false;
+  const float budget = env.abort_above - part;
+  if (budget < env.cs) {
+    float d_thr = env.cdmin + (__logf(env.cs / budget) - 1e-3f) / env.ca;
+    d_thr = fminf(d_thr, env.cdmax * 0.9999995f);  // d2 < d_thr^2 => sqrtf(d2) < d_max
+    if (d_thr > env.cdmin) {
+      stop2 = d_thr * d_thr;
+      abortable = true;
+    }
+  }
+  const float d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, lim2, stop2, &env.hint);
+  if (abortable && d2 < stop2) return 1;
+  s.col = s.col + collision_term(sqrtf(d2), env.cs, env.ca, env.cdmin, env.cdmax);
+  if (((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col) >
+      env.abort_above)
+    return 1;
+  const St<float> nx = rk4_normalized(x, u0, V3<float>{u1, u2, u3}, dy);
+  if (!state_finite(nx)) return 2;
+  x = nx;
+  return 0;
+}
+
+// Main screening pass with lane compaction: samples [k1, K) of one instance
+// per CTA, stepped in lockstep; every kCompact steps the live samples (not
+// yet past the abort bound) are packed into the lowest threads through shared
+// memory, so warps whose lanes all aborted stop issuing.  Same per-sample
+// arithmetic as k_stage1_f32 mode 2.
+constexpr int kScreenThreads = 128;
+constexpr int kStateWords = 21;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint
+
+template <int kMinBlocks, int kCompact>
+__global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
+    k_stage1_f32c(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter, int k1) {
+  __shared__ float s_unom[4 * kMaxN];
+  __shared__ float4 s_guide[kMaxN];
+  __shared__ float s_bound;
+  __shared__ float s_state[kStateWords][kScreenThreads];
+  __shared__ int s_k[kScreenThreads];
+  __shared__ int s_wcount[2][kScreenThreads / 32];
+  const int k_n = cfg.K - k1;
+  const int tiles = (k_n + kScreenThreads - 1) / kScreenThreads;
+  int b = blockIdx.x;
+  const int tile = b % tiles;
+  b /= tiles;
+  const int m = b % cfg.M;
+  const int s = b / cfg.M;
+  const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
+  const int N = cfg.N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* __restrict__ out = pl.cost32 + smi * cfg.K;
+  if (!pl.alive[smi]) {
+    const int k = k1 + tile * kScreenThreads + tid;
+    if (k < cfg.K) out[k] = __int_as_float(0x7f800000);
+    return;
+  }
+  for (int i = tid; i < 4 * N; i += kScreenThreads) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
+  for (int i = tid; i < N; i += kScreenThreads) s_guide[i] = pl.guide32[smi * N + i];
+  if (tid < 32) {
+    float u = __int_as_float(0x7f800000);
+    for (int k = tid; k < k1; k += 32) u = fminf(u, out[k]);
+    for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
+    if (tid == 0) {
+      const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
+      s_bound = u < 3.0e38f ? u + 2.0f * window : __int_as_float(0x7f800000);
+    }
+  }
+  __syncthreads();
+  RolloutEnv<float> env;
+  env.unom = s_unom;
+  env.guide = s_guide;
+  env.N = N;
+  env.dyn = make_dyn<float>(cfg);
+  const double* gl = in.goals + 10 * s;
+  env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
+  env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
+  env.q_p = static_cast<float>(cfg.q_p);
+  env.q_v = static_cast<float>(cfg.q_v);
+  env.q_q = static_cast<float>(cfg.q_q);
+  env.cs = static_cast<float>(cfg.col_scale);
+  env.ca = static_cast<float>(cfg.col_slope);
+  env.cdmin = static_cast<float>(cfg.col_d_min);
+  env.cdmax = static_cast<float>(cfg.col_d_max);
+  env.grid = P.grid[s];
+  env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+  env.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  env.gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
+  env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
+  env.has_guide = true;
+  env.abort_above = s_bound;
+  env.wq_track = static_cast<float>(cfg.q_track);
+  env.wq_vnorm = static_cast<float>(cfg.q_vnorm);
+  env.wq_c = static_cast<float>(cfg.q_c);
+  env.wq_cd = static_cast<float>(cfg.q_c_delta);
+
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  const uint64_t seed = in.seeds[s];
+  PertRngF pr{0ull, static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
+              static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
+  int k = k1 + tile * kScreenThreads + tid;
+  bool live = k < cfg.K;
+  pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
+  const double* xs = in.states + 10 * s;
+  St<float> x;
+  x.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
+  x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
+  CostSums<float> cs{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, true, false};
+  float up[4] = {0.f, 0.f, 0.f, 0.f};
+  int round = 0;
+  for (int j0 = 0; j0 < N; j0 += kCompact, ++round) {
+    const int j1 = min(j0 + kCompact, N);
+    if (live) {
+      for (int j = j0; j < j1; ++j) {
+        const int st = screen_step(x, cs, up, j, env, pr);
+        if (st) {
+          out[k] = st == 1 ? 3.4028234663852886e38f : __int_as_float(0x7f800000);
+          live = false;
+          break;
+        }
+      }
+    }
+    if (j1 >= N) break;
+    const unsigned bal = __ballot_sync(0xffffffffu, live);
+    int* wc = s_wcount[round & 1];
+    if (lane == 0) wc[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0, live_warps = 0;
+#pragma unroll
+    for (int w = 0; w < kScreenThreads / 32; ++w) {
+      const int c = wc[w];
+      before += w < warp ? c : 0;
+      total += c;
+      live_warps += c > 0;
+    }
+    if (total == 0) return;
+    if ((total + 31) / 32 < live_warps) {  // packing retires at least one warp
+      if (live) {
+        const int slot = before + __popc(bal & ((1u << lane) - 1u));
+        float* st = &s_state[0][slot];
+        st[0 * kScreenThreads] = x.p.x; st[1 * kScreenThreads] = x.p.y; st[2 * kScreenThreads] = x.p.z;
+        st[3 * kScreenThreads] = x.q.w; st[4 * kScreenThreads] = x.q.x; st[5 * kScreenThreads] = x.q.y;
+        st[6 * kScreenThreads] = x.q.z;
+        st[7 * kScreenThreads] = x.v.x; st[8 * kScreenThreads] = x.v.y; st[9 * kScreenThreads] = x.v.z;
+        st[10 * kScreenThreads] = cs.trk; st[11 * kScreenThreads] = cs.vn; st[12 * kScreenThreads] = cs.mag;
+        st[13 * kScreenThreads] = cs.rate; st[14 * kScreenThreads] = cs.goal; st[15 * kScreenThreads] = cs.col;
+        st[16 * kScreenThreads] = up[0]; st[17 * kScreenThreads] = up[1]; st[18 * kScreenThreads] = up[2];
+        st[19 * kScreenThreads] = up[3];
+        st[20 * kScreenThreads] = __uint_as_float(env.hint);
+        s_k[slot] = k;
+      }
+      __syncthreads();
+      live = tid < total;
+      if (live) {
+        const float* st = &s_state[0][tid];
+        x.p = {st[0 * kScreenThreads], st[1 * kScreenThreads], st[2 * kScreenThreads]};
+        x.q = {st[3 * kScreenThreads], st[4 * kScreenThreads], st[5 * kScreenThreads], st[6 * kScreenThreads]};
+        x.v = {st[7 * kScreenThreads], st[8 * kScreenThreads], st[9 * kScreenThreads]};
+        cs.trk = st[10 * kScreenThreads]; cs.vn = st[11 * kScreenThreads]; cs.mag = st[12 * kScreenThreads];
+        cs.rate = st[13 * kScreenThreads]; cs.goal = st[14 * kScreenThreads]; cs.col = st[15 * kScreenThreads];
+        up[0] = st[16 * kScreenThreads]; up[1] = st[17 * kScreenThreads]; up[2] = st[18 * kScreenThreads];
+        up[3] = st[19 * kScreenThreads];
+        env.hint = __float_as_uint(st[20 * kScreenThreads]);
+        k = s_k[tid];
+        pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
+      }
+      __syncthreads();
+    }
+  }
+  if (live) out[k] = stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd);
 }
 
 // Latency path, pass 1: one thread per rollout, everything but collision;
@@ -196,7 +411,9 @@ __global__ void __launch_bounds__(128) k_stage1_col32(Perception P, Plan pl, Dev
   float col = 0.f;
   for (int j = lane; j < cfg.N; j += 32) {
     const V3<float> p{pos[4 * j], pos[4 * j + 1], pos[4 * j + 2]};
-    const float d2 = nearest_sq_fast(g, cells, occ, pts, p, dmax * dmax * 1.0001f, dmin * dmin);
+    uint32_t hint = kNoHint;
+    const float d2 = nearest_sq_fast(g, cells, occ, P.grid_leaf + static_cast<int64_t>(s) * kCells * 2, pts, p,
+                                     dmax * dmax * 1.0001f, dmin * dmin, &hint);
     col += collision_term(sqrtf(d2), cs, ca, dmin, dmax);
   }
   for (int o = 16; o > 0; o >>= 1) col += __shfl_xor_sync(0xffffffffu, col, o);
@@ -236,17 +453,31 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     TimedRegion t(timer, "k_stage1_f32_bound", st);
     kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
   }
-  const int tiles = (cfg.K - k1 + 127) / 128;
+  const int tiles = (cfg.K - k1 + kScreenThreads - 1) / kScreenThreads;
   TimedRegion t(timer, "k_stage1_f32", st);
-  kern<<<static_cast<unsigned>(SM * tiles), 128, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
+  static const char* cmp = std::getenv("AMPPI_COMPACT");  // experiment switch: compaction interval (0 = off)
+  const int every = cmp ? std::atoi(cmp) : 3;
+  if (in.injected || every <= 0) {
+    kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
+  } else if (every == 1) {
+    k_stage1_f32c<8, 1><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  } else if (every == 2) {
+    k_stage1_f32c<8, 2><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  } else if (every <= 3) {
+    k_stage1_f32c<8, 3><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  } else if (every <= 5) {
+    k_stage1_f32c<8, 5><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  } else {
+    k_stage1_f32c<8, 8><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  }
   return cudaGetLastError();
 }
 
 #ifdef AMPPI_STATS
-extern "C" int amppi_query_stats(unsigned long long* out5, int reset) {
-  cudaMemcpyFromSymbol(out5, g_query_stats, sizeof(unsigned long long) * 5);
+extern "C" int amppi_query_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_query_stats, sizeof(unsigned long long) * kStatSlots);
   if (reset) {
-    unsigned long long z[5] = {0, 0, 0, 0, 0};
+    unsigned long long z[kStatSlots] = {};
     cudaMemcpyToSymbol(g_query_stats, z, sizeof(z));
   }
   return 0;

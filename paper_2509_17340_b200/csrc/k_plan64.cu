@@ -251,6 +251,7 @@ __device__ __forceinline__ RolloutEnv<double> make_env64(const BatchIn& in, cons
   e.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
 
   e.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  e.gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
   e.gpts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
   e.has_guide = true;
   e.abort_above = __longlong_as_double(0x7ff0000000000000ll);

@@ -18,12 +18,16 @@ constexpr double kMinPointRange = 0.05;
 constexpr double kHorizonReach = 25.0;
 
 // Collision grid: at most kGridAxis cells per axis, cell size >= d_max.
-// Every cell owns a 32-byte record (two uint4: {start, count, lo.x, lo.y},
-// {lo.z, hi.x, hi.y, hi.z}; the float box holds the cell's points, rounded
-// outward from FP64).  The padded lattice (dims+2)^3 holds, per cell, the
+// Every cell owns a 32-byte record (two uint4: {start | count << 16, first
+// leaf, lo.x, lo.y}, {lo.z, hi.x, hi.y, hi.z}; the float box holds the cell's
+// points, rounded outward from FP64).  A cell's points (sorted by Morton code
+// of the 1/8-cell sub-position) form leaves of kLeafSize consecutive points;
+// a leaf box is {lo.xyz, -}, {hi.xyz, -} in float (outward-rounded).  The padded lattice (dims+2)^3 holds, per cell, the
 // 27-bit mask of its non-empty neighbours (bit i*9+j*3+k <-> offset
 // (i-1, j-1, k-1)); mask 0 = no point within one cell.
 constexpr int kGridAxis = 24;
+constexpr uint32_t kLeafSize = 16;
+constexpr uint32_t kNoHint = 0xFFFFFFFFu;
 constexpr int kGridCells = kGridAxis * kGridAxis * kGridAxis;
 constexpr int kPadAxis = kGridAxis + 2;
 constexpr int kPadCells = kPadAxis * kPadAxis * kPadAxis;
@@ -96,6 +100,7 @@ struct Perception {
   GridMeta* grid;              // [S]
   uint4* grid_rec;             // [S*kGridCells*2] cell records (written for non-empty cells only)
   uint32_t* grid_nbr;          // [S*kPadCells] neighbour masks over the padded lattice
+  uint4* grid_leaf;            // [S*7200*2] leaf boxes
   double* grid_pts64;          // [S*7200*3] sorted by grid cell
   float4* grid_pts32;          // [S*7200]
 };

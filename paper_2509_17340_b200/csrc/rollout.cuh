@@ -37,9 +37,11 @@ struct RolloutEnv<double> {
   GridMeta grid;
   const uint4* grec;
   const uint32_t* gnbr;
+  const uint4* gleaf;
   const double* gpts;
   bool has_guide;
   double abort_above;
+  mutable uint32_t hint = kNoHint;  // nearest point of the previous query (per rollout)
 
   __device__ __forceinline__ V3<double> guide_at(int j) const {
     return {guide[3 * j], guide[3 * j + 1], guide[3 * j + 2]};
@@ -47,7 +49,7 @@ struct RolloutEnv<double> {
   __device__ __forceinline__ double unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ double attitude(Q4<double> q) const { return attitude_err_exact(q, gt); }
   __device__ __forceinline__ double collision(V3<double> p) const {
-    const double d2 = nearest_sq_exact(grid, grec, gnbr, gpts, p, cdmax * cdmax, cdmin * cdmin);
+    const double d2 = nearest_sq_exact(grid, grec, gnbr, gleaf, gpts, p, cdmax * cdmax, cdmin * cdmin, &hint);
     return collision_term(sqrt(d2), cs, ca, cdmin, cdmax);
   }
 };
@@ -65,10 +67,12 @@ struct RolloutEnv<float> {
   GridMeta grid;
   const uint4* grec;
   const uint32_t* gnbr;
+  const uint4* gleaf;
   const float4* gpts;
   bool has_guide;
   float abort_above;
   float wq_track, wq_vnorm, wq_c, wq_cd;  // stage-I weights for the partial-cost bound
+  mutable uint32_t hint = kNoHint;        // nearest point of the previous query (per rollout)
 
   __device__ __forceinline__ V3<float> guide_at(int j) const {
     const float4 g = guide[j];
@@ -77,7 +81,7 @@ struct RolloutEnv<float> {
   __device__ __forceinline__ float unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ float attitude(Q4<float> q) const { return attitude_err_fast(q, qg); }
   __device__ __forceinline__ float collision(V3<float> p) const {
-    const float d2 = nearest_sq_fast(grid, grec, gnbr, gpts, p, cdmax * cdmax * 1.0001f, cdmin * cdmin);
+    const float d2 = nearest_sq_fast(grid, grec, gnbr, gleaf, gpts, p, cdmax * cdmax * 1.0001f, cdmin * cdmin, &hint);
     return collision_term(sqrtf(d2), cs, ca, cdmin, cdmax);
   }
 };

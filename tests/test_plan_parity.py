@@ -230,3 +230,12 @@ def test_large_ensemble_shape(oracle):
     cfg = make_cfg(8, 8, K=512, N=50)
     cloud, pose = forest_cycle_inputs(oracle, frames=20)
     run_case(oracle, cfg, cloud, pose, pose, goal_target=(45, 0, 2), cycle=4, seed=9, f64=False)
+
+
+def test_throughput_screening_path(oracle):
+    """S*M*K >= 148*128*4 with K > 64 selects the bounded, lane-compacted FP32
+    screening (k_stage1_f32_bound + k_stage1_f32c); per-sample costs checked."""
+    cfg = make_cfg(8, 8, K=2048, N=30)
+    cloud, pose = forest_cycle_inputs(oracle, frames=20)
+    prev = np.tile(np.array([9.81, 0.1, -0.05, 0.02]), (30, 1))
+    run_case(oracle, cfg, cloud, pose, pose, goal_target=(45, 0, 2), previous=prev, cycle=7, seed=3, f64=False)
