@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
 // ---------------------------------------------------------------------------
 // finalize body
 // ---------------------------------------------------------------------------
-constexpr int kFinalizeThreads = 512;
+constexpr int kFinalizeThreads = 256;
 constexpr int kChunk = (kCells + kFinalizeThreads - 1) / kFinalizeThreads;  // 15
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 
@@ -180,6 +180,7 @@ struct FinalizeSmem {
   GridMeta meta;
   PoseFrame pose;
   uint32_t total;
+  uint32_t n_cand;
 };
 
 // Block-wide exclusive scan of one value per thread; returns the prefix and
@@ -421,10 +422,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   const uint32_t i0 = tid * kPerThread;
   uint32_t n_leaf_starts = 0;
   for (uint32_t i = i0; i < i0 + kPerThread; ++i) n_leaf_starts += lflag[i];
-  uint32_t leaf = block_exclusive_scan(n_leaf_starts, sm.warp_sums, &sm.total);
+  const uint32_t leaf0 = block_exclusive_scan(n_leaf_starts, sm.warp_sums, &sm.total);
+  uint32_t leaf = leaf0;
   for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
     if (!lflag[i]) continue;
-    const uint32_t c = keys[i] >> 9;
     double llo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, lhi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
     uint32_t t = i;
     do {
@@ -440,19 +441,28 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     gleaf[2 * leaf + 1] = make_uint4(__float_as_uint(__double2float_ru(lhi[0])),
                                      __float_as_uint(__double2float_ru(lhi[1])),
                                      __float_as_uint(__double2float_ru(lhi[2])), 0u);
-    if (i == 0 || (keys[i - 1] >> 9) != c) {  // cell record: points, first leaf, float box
+    ++leaf;
+  }
+  __syncthreads();
+  // cell records: point range, first leaf, box = union of the leaf boxes
+  leaf = leaf0;
+  for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
+    if (!lflag[i]) continue;
+    const uint32_t c = keys[i] >> 9;
+    if (i == 0 || (keys[i - 1] >> 9) != c) {
       uint32_t e = i + 1;
-      double blo[3] = {gp64[3 * i], gp64[3 * i + 1], gp64[3 * i + 2]}, bhi[3] = {blo[0], blo[1], blo[2]};
-      for (; e < n_pts && (keys[e] >> 9) == c; ++e)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          blo[a] = fmin(blo[a], gp64[3 * e + a]);
-          bhi[a] = fmax(bhi[a], gp64[3 * e + a]);
-        }
-      grec[2 * c] = make_uint4(i | ((e - i) << 16), leaf, __float_as_uint(__double2float_rd(blo[0])),
-                               __float_as_uint(__double2float_rd(blo[1])));
-      grec[2 * c + 1] = make_uint4(__float_as_uint(__double2float_rd(blo[2])), __float_as_uint(__double2float_ru(bhi[0])),
-                                   __float_as_uint(__double2float_ru(bhi[1])), __float_as_uint(__double2float_ru(bhi[2])));
+      while (e < n_pts && (keys[e] >> 9) == c) ++e;
+      float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+      for (uint32_t l = leaf; l < leaf + (e - i + kLeafSize - 1) / kLeafSize; ++l) {
+        const uint4 la = gleaf[2 * l], lb = gleaf[2 * l + 1];
+        lo[0] = fminf(lo[0], __uint_as_float(la.x)); lo[1] = fminf(lo[1], __uint_as_float(la.y));
+        lo[2] = fminf(lo[2], __uint_as_float(la.z));
+        hi[0] = fmaxf(hi[0], __uint_as_float(lb.x)); hi[1] = fmaxf(hi[1], __uint_as_float(lb.y));
+        hi[2] = fmaxf(hi[2], __uint_as_float(lb.z));
+      }
+      grec[2 * c] = make_uint4(i | ((e - i) << 16), leaf, __float_as_uint(lo[0]), __float_as_uint(lo[1]));
+      grec[2 * c + 1] = make_uint4(__float_as_uint(lo[2]), __float_as_uint(hi[0]), __float_as_uint(hi[1]),
+                                   __float_as_uint(hi[2]));
     }
     ++leaf;
   }
@@ -482,7 +492,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
 }
 
 // Global schedule, last step: tables from K1/K1b (reset for the next cycle).
-__global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
+__global__ void __launch_bounds__(kFinalizeThreads, 2) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
   const int s = blockIdx.x;
@@ -501,7 +511,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_finalize_scene(BatchIn 
 }
 
 // Fused schedule: one CTA per scene, per-cell minimum in shared memory.
-__global__ void __launch_bounds__(kFinalizeThreads, 1) k_snapshot_scene(BatchIn in, Perception P, DevConfig cfg) {
+__global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn in, Perception P, DevConfig cfg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
   unsigned long long* cell_bits = reinterpret_cast<unsigned long long*>(sm.rng);
@@ -516,19 +526,39 @@ __global__ void __launch_bounds__(kFinalizeThreads, 1) k_snapshot_scene(BatchIn 
   const PoseFrame pose = sm.pose;
   const int64_t b = in.offsets[s], e = in.offsets[s + 1];
   const double r_max = in.r_max;
-  // pass A: minimum range bits per cell
-  for (int64_t g = b + tid; g < e; g += blockDim.x) {
-    int f;
-    uint64_t bits;
-    if (key_point(pose, load_point(in, g), r_max, f, bits)) atomicMin(cell_bits + f, bits);
+  // pass A: minimum range bits per cell; a point that was <= the running
+  // minimum when it arrived may be the final minimum and is logged (cell,
+  // index) for the tie-break -- typically a third of the points
+  uint32_t* __restrict__ log = reinterpret_cast<uint32_t*>(P.cand) + b;  // [points of this scene]
+  if (tid == 0) sm.n_cand = 0u;
+  __syncthreads();
+  const int lane = tid & 31;
+  for (int64_t g0 = b; g0 < e; g0 += blockDim.x) {
+    const int64_t g = g0 + tid;
+    int f = 0;
+    uint64_t bits = 0;
+    bool cand = false;
+    if (g < e && key_point(pose, load_point(in, g), r_max, f, bits))
+      cand = atomicMin(cell_bits + f, bits) >= bits;
+    const unsigned want = __ballot_sync(0xffffffffu, cand);
+    if (want) {
+      uint32_t base = 0;
+      if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
+      base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
+      if (cand) log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
+    }
   }
   __syncthreads();
-  // pass B: lowest point index among the points at the minimum
-  for (int64_t g = b + tid; g < e; g += blockDim.x) {
-    int f;
-    uint64_t bits;
-    if (key_point(pose, load_point(in, g), r_max, f, bits) && cell_bits[f] == bits)
-      atomicMin(sm.idx + f, static_cast<uint32_t>(g - b));
+  // pass B: lowest point index among the logged points at the minimum
+  // ("strict <, first point wins", perception.cpp:80-86)
+  const uint32_t n_cand = sm.n_cand;
+  for (uint32_t c = tid; c < n_cand; c += blockDim.x) {
+    const uint32_t en = log[c];
+    const int f = static_cast<int>(en >> 16);
+    const uint32_t idx = en & 0xFFFFu;
+    const V3<double> p = to_body(pose, load_point(in, b + idx));
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(sqrt(sqnorm(p))));
+    if (cell_bits[f] == bits) atomicMin(sm.idx + f, idx);
   }
   __syncthreads();
   for (int f = tid; f < kCells; f += blockDim.x) {
