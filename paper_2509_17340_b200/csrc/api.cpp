@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -133,6 +134,8 @@ struct amppi_ctx {
   DevConfig dc{};
   cudaStream_t stream{nullptr};
   bool own_stream{false};
+  cudaStream_t copy_stream{nullptr};  // host->device point copies overlapped with planning
+  std::vector<cudaEvent_t> chunk_ready;
   std::string err;
   int S_cap{1};
   int64_t P_cap{0};
@@ -286,6 +289,7 @@ int create_impl(amppi_ctx* ctx) {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->own_stream = true;
   }
+  CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   CK(init_kernel_attributes());
   Arena& A = ctx->arena;
   // inputs (device + pinned mirror with identical layout)
@@ -388,7 +392,12 @@ int create_impl(amppi_ctx* ctx) {
   CK(A.alloc(&p, SM * K * sizeof(double)));
   pl.cost64 = static_cast<double*>(p);
   {
-    const size_t jobs = std::max<size_t>(SM, static_cast<size_t>(kLatencyRollouts));
+    // deferred-collision rollouts: stage II (S*M) and the split FP64 refine
+    // (~4 support samples per instance; more spill to the fused k_refine)
+    const size_t jobs = std::max<size_t>(4 * SM, static_cast<size_t>(kLatencyRollouts));
+    pl.pos_cap = static_cast<int64_t>(jobs);
+    if (const char* f = std::getenv("AMPPI_REFINE_SPLIT_CAP"))  // tests: force the fused-refine overflow path
+      pl.pos_cap = std::max<int64_t>(0, std::min<int64_t>(pl.pos_cap, std::atoll(f)));
     CK(A.alloc(&p, static_cast<size_t>(kLatencyRollouts) * N * 4 * sizeof(float)));
     pl.pos32 = static_cast<float*>(p);
     CK(A.alloc(&p, jobs * N * 4 * sizeof(double)));
@@ -436,14 +445,48 @@ BatchIn batch_from_block(amppi_ctx* ctx, int S, double r_max, bool f64_points) {
   return in;
 }
 
+// The plan arrays of scenes [s0, ...): a chunk of a batch planned on its own
+// writes its per-scene results at their batch position (perception and
+// per-iteration scratch are consumed within the chunk and are reused).
+Plan shift_plan(const Plan& p, int64_t s0, const DevConfig& c) {
+  const int64_t sm = s0 * c.M;
+  Plan q = p;
+  q.anchor_init += sm * 3;
+  q.anchor_ref += sm * 3;
+  q.anchor_dir += sm * 3;
+  q.anchor_range += sm;
+  q.anchor_ij += sm * 2;
+  q.guide_coef += sm * 18;
+  q.guide64 += sm * c.N * 3;
+  q.guide32 += sm * c.N;
+  q.nominal += sm * c.N * 4;
+  q.cost32 += sm * c.K;
+  q.cost64 += sm * c.K;
+  q.alive += sm;
+  q.stage1 += sm;
+  q.stage2 += sm;
+  q.ess += sm;
+  q.valid += sm;
+  q.breakdown += sm * 5;
+  q.n_support += sm;
+  q.done += s0;
+  q.winner += s0;
+  q.status += s0;
+  q.control += s0 * 4;
+  if (q.winner_states) q.winner_states += s0 * (c.N + 1) * 10;
+  if (q.winner_controls) q.winner_controls += s0 * c.N * 4;
+  return q;
+}
+
 int run_cycle(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, bool do_snapshot, bool do_plan,
-              bool winner_rollout) {
+              bool winner_rollout, int64_t s0 = 0) {
   if (do_snapshot) {
     cudaError_t e = launch_snapshot(in, ctx->P, ctx->dc, max_pts_scene, ctx->stream, &ctx->timer);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_snapshot");
   }
   if (do_plan) {
-    cudaError_t e = launch_plan_impl(in, ctx->P, ctx->pl, ctx->dc, ctx->opt.precision, winner_rollout, ctx->cand_k,
+    const Plan pl = s0 ? shift_plan(ctx->pl, s0, ctx->dc) : ctx->pl;
+    cudaError_t e = launch_plan_impl(in, ctx->P, pl, ctx->dc, ctx->opt.precision, winner_rollout, ctx->cand_k,
                                      ctx->cand_s, ctx->cand_w, ctx->pairs, ctx->pair_count, ctx->stream, &ctx->timer);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_plan");
   }
@@ -558,6 +601,8 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->h_in) cudaFreeHost(ctx->h_in);
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (cudaEvent_t e : ctx->chunk_ready) cudaEventDestroy(e);
   delete ctx;
   return AMPPI_OK;
 }
@@ -741,9 +786,6 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   for (int s = 0; s < S; ++s) max_scene = std::max(max_scene, in->point_offsets[s + 1] - in->point_offsets[s]);
   // inputs: points straight from the caller's buffer, per-scene arrays via the
   // pinned block
-  if (total > 0)
-    CK(cudaMemcpyAsync(ctx->d_xyz, in->xyz, static_cast<size_t>(total) * 3 * sizeof(float), cudaMemcpyHostToDevice,
-                       ctx->stream));
   InputBlock& h = ctx->hin;
   std::memcpy(h.poses, in->poses, static_cast<size_t>(S) * 10 * sizeof(double));
   std::memcpy(h.states, in->states, static_cast<size_t>(S) * 10 * sizeof(double));
@@ -756,9 +798,73 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   for (int s = 0; s < S; ++s) h.prev_len[s] = in->previous ? (in->previous_len ? in->previous_len[s] : N) : 0;
   const size_t span = static_cast<size_t>(reinterpret_cast<unsigned char*>(h.prev_len + ctx->S_cap) -
                                           reinterpret_cast<unsigned char*>(h.poses));
-  CK(cudaMemcpyAsync(ctx->din.poses, h.poses, span, cudaMemcpyHostToDevice, ctx->stream));
-  BatchIn bin = batch_from_block(ctx, S, in->r_max, false);
-  if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
+  // Pipeline: the points of chunk c+1 cross PCIe on the copy stream while
+  // chunk c is planned.  Chunks are whole scenes (>= 2 fused-snapshot waves);
+  // results land at each scene's batch position.
+  // Chunks cost ~1.5 ms of extra kernel tails each, so keep them large: ~24M
+  // points (3 for C5's 73M), at most 4.
+  int chunks = static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, (total + (12 << 20)) / (24 << 20))));
+  chunks = std::max(1, std::min(chunks, S / 296));
+  if (const char* f = std::getenv("AMPPI_PIPELINE_CHUNKS")) chunks = std::max(1, std::min(S, std::atoi(f)));  // tests
+  while (static_cast<int>(ctx->chunk_ready.size()) < chunks) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->chunk_ready.push_back(ev);
+  }
+  // the copy stream must not overwrite inputs a previous call is still using;
+  // the per-scene block goes first on the copy stream (H2D copies share the
+  // copy engine in issue order, so it must not queue behind the points)
+  CK(cudaEventRecord(ctx->chunk_ready[0], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ready[0], 0));
+  CK(cudaMemcpyAsync(ctx->din.poses, h.poses, span, cudaMemcpyHostToDevice, ctx->copy_stream));
+  static const bool trace = std::getenv("AMPPI_PIPELINE_TRACE") != nullptr;  // diagnostics
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  tmark(ctx->copy_stream);
+  for (int c = 0; c < chunks; ++c) {
+    const int s0 = static_cast<int>(static_cast<int64_t>(S) * c / chunks);
+    const int s1 = static_cast<int>(static_cast<int64_t>(S) * (c + 1) / chunks);
+    const int64_t p0 = in->point_offsets[s0], p1 = in->point_offsets[s1];
+    if (p1 > p0)
+      CK(cudaMemcpyAsync(ctx->d_xyz + 3 * p0, in->xyz + 3 * p0, static_cast<size_t>(p1 - p0) * 3 * sizeof(float),
+                         cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->chunk_ready[c], ctx->copy_stream));
+    tmark(ctx->copy_stream);
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ready[c], 0));
+    int64_t max_chunk_scene = 0;
+    for (int s = s0; s < s1; ++s)
+      max_chunk_scene = std::max(max_chunk_scene, in->point_offsets[s + 1] - in->point_offsets[s]);
+    BatchIn bin = batch_from_block(ctx, s1 - s0, in->r_max, false);
+    bin.offsets += s0;
+    bin.poses += 10 * s0;
+    bin.states += 10 * s0;
+    bin.goals += 10 * s0;
+    bin.prev += static_cast<int64_t>(s0) * N * 4;
+    bin.prev_len += s0;
+    bin.last_applied += 4 * s0;
+    bin.cycles += s0;
+    bin.seeds += s0;
+    if (int rc = run_cycle(ctx, bin, max_chunk_scene, true, true, false, s0); rc != AMPPI_OK) return rc;
+    tmark(ctx->stream);
+  }
+  if (trace) {
+    cudaDeviceSynchronize();
+    std::fprintf(stderr, "pipeline %d chunks:", chunks);
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      std::fprintf(stderr, " %.2f", ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
+  (void)max_scene;
   return batch_outputs_gather(ctx, S, out, false);
 }
 

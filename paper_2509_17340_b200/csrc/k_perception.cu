@@ -533,19 +533,29 @@ __global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn 
   if (tid == 0) sm.n_cand = 0u;
   __syncthreads();
   const int lane = tid & 31;
-  for (int64_t g0 = b; g0 < e; g0 += blockDim.x) {
-    const int64_t g = g0 + tid;
-    int f = 0;
-    uint64_t bits = 0;
-    bool cand = false;
-    if (g < e && key_point(pose, load_point(in, g), r_max, f, bits))
-      cand = atomicMin(cell_bits + f, bits) >= bits;
-    const unsigned want = __ballot_sync(0xffffffffu, cand);
-    if (want) {
-      uint32_t base = 0;
-      if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
-      base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
-      if (cand) log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
+  constexpr int kUnroll = 4;  // loads of kUnroll points in flight per thread
+  for (int64_t g0 = b; g0 < e; g0 += kUnroll * blockDim.x) {
+    V3<double> w[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t g = g0 + u * blockDim.x + tid;
+      w[u] = g < e ? load_point(in, g) : V3<double>{0.0, 0.0, 0.0};
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t g = g0 + u * blockDim.x + tid;
+      int f = 0;
+      uint64_t bits = 0;
+      bool cand = false;
+      if (g < e && key_point(pose, w[u], r_max, f, bits)) cand = atomicMin(cell_bits + f, bits) >= bits;
+      const unsigned want = __ballot_sync(0xffffffffu, cand);
+      if (want) {
+        uint32_t base = 0;
+        if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
+        base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
+        if (cand)
+          log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
+      }
     }
   }
   __syncthreads();

@@ -448,10 +448,11 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     kern<<<static_cast<unsigned>(SM * tiles), threads, 0, st>>>(in, P, pl, cfg, iter, 0, 0);
     return cudaGetLastError();
   }
-  const int k1 = 32;
+  static const char* k1env = std::getenv("AMPPI_K1");  // experiment switch: bound-pass samples
+  const int k1 = k1env ? std::atoi(k1env) : 32;
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
-    kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
+    kern<<<static_cast<unsigned>(SM * ((k1 + 31) / 32)), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
   }
   const int tiles = (cfg.K - k1 + kScreenThreads - 1) / kScreenThreads;
   TimedRegion t(timer, "k_stage1_f32", st);

@@ -19,6 +19,8 @@
 //                       the winner (ensemble.cpp:151-168)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "cr_math.cuh"
 #include "kernels.h"
 #include "rollout.cuh"
@@ -403,11 +405,13 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
 
 // One thread per (instance, support slot) over the flattened work list:
 // full warps regardless of how the support sizes are distributed.
+// Fused FP64 re-rollout of support pairs [first, pair_count) (the pairs the
+// split traj/col kernels had no scratch for).
 __global__ void __launch_bounds__(64) k_refine(BatchIn in, Perception P, Plan pl, DevConfig cfg, UpdateScratch us,
-                                               int iter) {
+                                               int iter, unsigned long long first) {
   const unsigned long long n = *us.pair_count;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-  for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < n;
+  for (unsigned long long w = first + static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < n;
        w += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
     const uint2 pr = us.pairs[w];
     const int64_t smi = pr.x;
@@ -563,7 +567,7 @@ __global__ void __launch_bounds__(128) k_stage2_col(BatchIn in, Perception P, Pl
 // then a warp per slot for the collision terms.
 __global__ void __launch_bounds__(64) k_refine_traj(BatchIn in, Perception P, Plan pl, DevConfig cfg,
                                                     UpdateScratch us, int iter) {
-  const unsigned long long n = *us.pair_count;
+  const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
   for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < n;
        w += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
     const uint2 pr = us.pairs[w];
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(64) k_refine_traj(BatchIn in, Perception P, Pl
 __global__ void __launch_bounds__(128) k_refine_col(BatchIn in, Perception P, Plan pl, DevConfig cfg,
                                                     UpdateScratch us) {
   __shared__ double s_terms[4][64];
-  const unsigned long long n = *us.pair_count;
+  const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
   const int wid = threadIdx.x >> 5;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   for (unsigned long long w = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n;
@@ -694,19 +698,27 @@ cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan&
       k_support<<<SM, kSupportThreads, 0, st>>>(pl, cfg, us, precision);
     }
     if (precision == 32) {
+      // FP64 re-rollout of the support: trajectories first (collision
+      // deferred, positions to pos64), then one warp per rollout for the
+      // collision terms -- a rollout's latency is its trajectory, not 30
+      // sequential exact queries.  Pairs beyond pos_cap take the fused kernel.
       const int64_t total = static_cast<int64_t>(SM) * cfg.K;
-      if (total < kLatencyRollouts) {
-        const int blocks = static_cast<int>((total + 63) / 64);
-        {
-          TimedRegion t(timer, "k_refine_traj", st);
-          k_refine_traj<<<blocks, 64, 0, st>>>(in, P, pl, cfg, us, iter);
-        }
+      const int64_t jobs = std::min<int64_t>(total, pl.pos_cap);
+      {
+        TimedRegion t(timer, "k_refine_traj", st);
+        const int64_t b = (jobs + 63) / 64;
+        k_refine_traj<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+      }
+      {
         TimedRegion t(timer, "k_refine_col", st);
-        k_refine_col<<<static_cast<int>((total * 32 + 127) / 128), 128, 0, st>>>(in, P, pl, cfg, us);
-      } else {
-        const int64_t cap = (total + 63) / 64;
+        const int64_t b = (jobs * 32 + 127) / 128;
+        k_refine_col<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 128, 0, st>>>(in, P, pl, cfg, us);
+      }
+      if (total > pl.pos_cap) {
         TimedRegion t(timer, "k_refine", st);
-        k_refine<<<static_cast<int>(cap < sms * 16 ? cap : sms * 16), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+        const int64_t b = (total - pl.pos_cap + 63) / 64;
+        k_refine<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(
+            in, P, pl, cfg, us, iter, static_cast<unsigned long long>(pl.pos_cap));
       }
     }
     {

@@ -139,8 +139,9 @@ struct Plan {
   uint32_t* n_support;         // [S*M] softmin support size (diagnostics)
   // deferred-collision scratch (latency path and stage II)
   float* pos32;                // [kLatencyRollouts*N*4]
-  double* pos64;               // [max(S*M, kLatencyRollouts)*N*4]
-  TrajSums* tsum;              // [max(S*M, kLatencyRollouts)]
+  double* pos64;               // [pos_cap*N*4]
+  TrajSums* tsum;              // [pos_cap]
+  int64_t pos_cap;             // support pairs the split refine handles (pos64/tsum hold max(4*S*M, kLatencyRollouts))
   // per scene
   int32_t* done;               // [S] arrival counter (self-resetting)
   int32_t* winner;             // [S]

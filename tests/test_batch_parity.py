@@ -76,6 +76,17 @@ def test_batch_warm_start_matches_oracle(oracle, batch):
     assert _check_against_oracle(oracle, cfg, data, out, previous=first["winner_nominal"], cycle_shift=1) > S // 2
 
 
+def test_pipelined_host_batch_equals_single_chunk(batch, monkeypatch):
+    """amppi_cycle_batch overlaps chunk c+1's point upload with chunk c's
+    planning; results must not depend on the chunking."""
+    cfg, data, planner = batch
+    one = _host_call(planner, data)
+    monkeypatch.setenv("AMPPI_PIPELINE_CHUNKS", "3")
+    three = _host_call(planner, data)
+    for k in one:
+        assert np.array_equal(one[k], three[k]), k
+
+
 def test_device_entry_point_equals_host(batch):
     import torch
 

@@ -239,3 +239,25 @@ def test_throughput_screening_path(oracle):
     cloud, pose = forest_cycle_inputs(oracle, frames=20)
     prev = np.tile(np.array([9.81, 0.1, -0.05, 0.02]), (30, 1))
     run_case(oracle, cfg, cloud, pose, pose, goal_target=(45, 0, 2), previous=prev, cycle=7, seed=3, f64=False)
+
+
+def test_refine_overflow_path(oracle, monkeypatch):
+    """Support pairs beyond the split-refine scratch take the fused FP64
+    re-rollout (k_refine); forced here with a 5-pair split capacity."""
+    from paper_2509_17340_b200 import Planner
+
+    monkeypatch.setenv("AMPPI_REFINE_SPLIT_CAP", "5")
+    cfg = make_cfg(4, 2, K=256, N=30)
+    planner = Planner(cfg, precision=32, max_points=1 << 20)
+    key = (repr(cfg), 32)
+    saved = _planners.get(key)
+    _planners[key] = planner
+    try:
+        cloud, pose = forest_cycle_inputs(oracle)
+        run_case(oracle, cfg, cloud, pose, pose, goal_target=(45, 0, 2), cycle=11, seed=2, f64=False)
+    finally:
+        planner.close()
+        if saved is not None:
+            _planners[key] = saved
+        else:
+            _planners.pop(key)
