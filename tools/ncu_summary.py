@@ -76,8 +76,24 @@ def full(path):
         for m, label in METRICS:
             if m in col:
                 print(f"| {label} (`{m}`) | {r[col[m]]} {units[col[m]]} |")
-        stalls = [(h, r[i]) for h, i in col.items() if h.startswith("smsp__average_warp_latency_issue_stalled_")
-                  and h.endswith("_ratio") is False]
+        def num(k):
+            try:
+                return float(r[col[k]].replace(",", ""))
+            except (KeyError, ValueError):
+                return float("nan")
+
+        fl = (2 * num("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed")
+              + num("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed")
+              + num("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed"))
+        hz = num("gpc__cycles_elapsed.avg.per_second")
+        unit = units[col["gpc__cycles_elapsed.avg.per_second"]].lower() if "gpc__cycles_elapsed.avg.per_second" in col else ""
+        hz *= 1e9 if "ghz" in unit else (1e6 if "mhz" in unit else 1.0)
+        peak = 2 * num("sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained")
+        if fl == fl and hz == hz:
+            print(f"| executed FP32 flops (2 FFMA + FADD + FMUL) | {fl:.0f} /cycle = {fl * hz / 1e12:.2f} TFLOP/s "
+                  f"= {100 * fl / peak:.1f}% of the {peak:.0f}/cycle FFMA peak |")
+        dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+        print(f"| DRAM traffic read+write | {dram:.1f} {units[col['dram__bytes_read.sum']]} |")
         print()
 
 
