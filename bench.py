@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c4"],
+                    help="c5: batched scenes (default, the driver's line); c4: 64x8192x50 ensemble, samples "
+                         "sharded over the ranks with NCCL")
     ap.add_argument("--scenes", type=int, default=4096)
     ap.add_argument("--points", type=int, default=20000)
     ap.add_argument("--latency-cycles", type=int, default=1000)
@@ -392,9 +395,99 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_c4(args):
+    """Config C4: one forest scene, 8x8 anchors x 8192 samples x 50 steps; the
+    samples of every instance are split over the ranks (global sample index in
+    the RNG key) and merged with one all-reduce MIN + one all-gather per
+    iteration (sharding.plan_step_sharded).  value = rollout-steps/s of the
+    whole job, device time max over ranks; scaling: strong (fixed ensemble)."""
+    import numpy as np
+    import torch
+
+    from paper_2509_17340_b200 import ControlInput, GoalSpec, Planner, State
+    from paper_2509_17340_b200.sharding import TorchComm, plan_step_sharded
+    from paper_2509_17340_b200.workloads import plan_config, rollout_steps, scenes
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    import torch.distributed as dist
+
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    cfg = plan_config(m_h=8, m_v=8, K=8192, N=50)
+    one = scenes(1, points=args.points, frames=20, first=0, kinds=1, device=local)
+    planner = Planner(cfg, device=local, precision=32, max_points=1 << 16, profile=True, stream=stream.cuda_stream)
+    x = State.from_array(one["states"][0])
+    goal = GoalSpec((45.0, 0.0, 2.0), (0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0))
+    la = ControlInput(one["last"][0][0], (0.0, 0.0, 0.0))
+    snap = planner.build_snapshot(one["xyz"], x, cfg.r_max)
+    prev = None
+
+    class _Single:  # one rank: the collectives are identities
+        rank, world = 0, 1
+
+        @staticmethod
+        def allreduce_min(t):
+            pass
+
+        @staticmethod
+        def allgather(out, t):
+            out.copy_(t)
+
+    comm = TorchComm() if ws > 1 else _Single()
+
+    def step(i):
+        nonlocal prev
+        r = plan_step_sharded(planner, x, goal, snap, prev, la, 100 + i, 1, comm, want_rollout=False)
+        prev = r.per_instance[r.winner].nominal
+        return r
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    planner.kernel_times_reset()
+    sampler = ClockSampler(local)
+    sampler.start()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    kt = planner.kernel_times()
+    value = rollout_steps(cfg, 1) * args.steps / (ms / 1e3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "rollout-steps/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 screening / f64 support, update, stage II", "data": "synthetic",
+            "config": {"workload": "C4: one forest scene (GPU LiDAR, 20k points), 8x8 anchors x 8192 samples x "
+                                   "50 steps, samples sharded over the ranks (NCCL all-reduce MIN + all-gather "
+                                   "of the softmin partials per iteration); host-to-host plan_step per step",
+                       "anchors": 64, "samples": 8192, "horizon": 50, "parallelism": f"sample-sharded x{ws}"},
+            "clocks": clocks, "gpu_launches": int(sum(v[1] for v in kt.values())),
+            "kernels": {k: {"ms_total": v[0], "launches": v[1]} for k, v in sorted(kt.items())},
+        }), flush=True)
+    planner.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.impl == "b200" and args.workload == "c4":
+        run_c4(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

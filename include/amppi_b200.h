@@ -198,6 +198,25 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
 int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in_device,
                              amppi_batch_output* out_device);
 
+/* Sample-sharded plan_step (config C4): one context per GPU,
+ * each owning samples [k_begin, k_end) of every instance (the global sample
+ * index keys the perturbation stream, so the draws equal the unsharded plan).
+ * Per iteration: screen -> all-reduce MIN of local_min[M] over the shards ->
+ * partials -> all-gather of the [M * stride] partials (stride =
+ * amppi_shard_partials_stride) in shard order -> update.  Then finish, which
+ * fills *out like amppi_plan (identical on every shard).  All pointers except
+ * out are DEVICE pointers; work is enqueued on the context stream and the
+ * caller runs the collectives (e.g. NCCL) on that stream.  Replaces the inner
+ * loop of plan_step (ensemble.cpp:79-129) with the merge of DESIGN.md §6. */
+int amppi_shard_begin(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
+                      int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
+                      int32_t k_begin, int32_t k_end);
+int amppi_shard_screen(amppi_ctx* ctx, int32_t iter, float* local_min);
+int amppi_shard_partials(amppi_ctx* ctx, int32_t iter, const float* global_min, double* partials);
+int amppi_shard_update(amppi_ctx* ctx, int32_t iter, const double* all_partials, int32_t n_shards);
+int amppi_shard_finish(amppi_ctx* ctx, amppi_plan_result* out);
+int32_t amppi_shard_partials_stride(const amppi_ctx* ctx);
+
 /* Profiling: per-kernel device time accumulated since the last reset
  * (requires opt.profile = 1).  names/ms/launches are caller arrays of cap. */
 int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches,

@@ -133,6 +133,14 @@ EXPORTS = {
                                       c_uint64_p, ctypes.c_double, ctypes.c_int64, c_float_p, c_int64_p,
                                       ctypes.c_int32]),
     "amppi_probe_fp32_peak": (ctypes.c_int, [ctypes.c_int32, c_double_p, c_double_p]),
+    "amppi_shard_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(State), ctypes.POINTER(Goal), c_double_p,
+                                         ctypes.c_int32, ctypes.POINTER(Control), ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_int32, ctypes.c_int32]),
+    "amppi_shard_screen": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
+    "amppi_shard_partials": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
+    "amppi_shard_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32]),
+    "amppi_shard_finish": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PlanResult)]),
+    "amppi_shard_partials_stride": (ctypes.c_int32, [ctypes.c_void_p]),
 }
 
 _lib = None

@@ -169,6 +169,10 @@ struct amppi_ctx {
   double snap_pose[10]{};
   int64_t snap_points{0};
   KernelTimer timer;
+  // sample-sharded plan in progress (amppi_shard_*)
+  bool shard_active{false};
+  DevConfig shard_dc{};
+  BatchIn shard_in{};
 
   int fail(int code, const std::string& msg) {
     err = msg;
@@ -194,6 +198,8 @@ DevConfig to_dev(const amppi_config& c) {
   d.m_v = c.m_v;
   d.M = c.m_h * c.m_v;
   d.K = c.rollouts;
+  d.k_lo = 0;
+  d.k_hi = c.rollouts;
   d.N = c.horizon;
   d.iterations = c.iterations;
   d.lookahead = c.lookahead;
@@ -681,10 +687,15 @@ int amppi_snapshot_download(amppi_ctx* ctx, amppi_snapshot_view* v) {
   return AMPPI_OK;
 }
 
-int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
-               int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
-               const double* injected, amppi_plan_result* out) {
-  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+}  // extern "C"
+
+namespace {
+
+// plan_step inputs of the single-scene API -> device input block (+ optional
+// injected perturbations); *in receives the batch view.
+int stage_plan_inputs(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
+                      int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
+                      const double* injected, BatchIn* in_out) {
   if (!x || !goal || !last_applied) return ctx->fail(AMPPI_INVALID_ARGUMENT, "null argument");
   if (!ctx->have_snapshot) return ctx->fail(AMPPI_NO_SNAPSHOT, "amppi_plan before amppi_snapshot");
   const DevConfig& dc = ctx->dc;
@@ -714,8 +725,15 @@ int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, con
     CK(cudaMemcpyAsync(ctx->d_injected, injected, bytes, cudaMemcpyHostToDevice, ctx->stream));
     in.injected = ctx->d_injected;
   }
-  const bool want_states = out && (out->winner_states || out->winner_controls);
-  if (int rc = run_cycle(ctx, in, ctx->snap_points, false, true, want_states); rc != AMPPI_OK) return rc;
+  *in_out = in;
+  return AMPPI_OK;
+}
+
+// Results of a single-scene plan (k_gather'd block + optional arrays) ->
+// caller buffers; syncs the stream.
+int collect_plan_result(amppi_ctx* ctx, amppi_plan_result* out, bool want_states) {
+  const DevConfig& dc = ctx->dc;
+  const int M = dc.M, K = dc.K, N = dc.N;
   CK(cudaMemcpyAsync(ctx->h_res, ctx->d_res, ctx->dres.bytes, cudaMemcpyDeviceToHost, ctx->stream));
   std::vector<float> c32;
   std::vector<double> c64;
@@ -772,6 +790,86 @@ int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, con
   if (status != 0) return ctx->fail(AMPPI_PLANNING_FAILED, "planning failed");
   return AMPPI_OK;
 }
+
+}  // namespace
+
+
+extern "C" {
+
+int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
+               int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
+               const double* injected, amppi_plan_result* out) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  BatchIn in{};
+  if (int rc = stage_plan_inputs(ctx, x, goal, previous, previous_len, last_applied, cycle, seed, injected, &in);
+      rc != AMPPI_OK)
+    return rc;
+  const bool want_states = out && (out->winner_states || out->winner_controls);
+  if (int rc = run_cycle(ctx, in, ctx->snap_points, false, true, want_states); rc != AMPPI_OK) return rc;
+  return collect_plan_result(ctx, out, want_states);
+}
+
+// ---- sample-sharded plan (config C4) ----
+int amppi_shard_begin(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
+                      int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
+                      int32_t k_begin, int32_t k_end) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (ctx->opt.precision != 32) return ctx->fail(AMPPI_INVALID_ARGUMENT, "sample sharding needs precision 32");
+  if (k_begin < 0 || k_end > ctx->dc.K || k_begin >= k_end)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "sample range out of [0, rollouts)");
+  BatchIn in{};
+  if (int rc = stage_plan_inputs(ctx, x, goal, previous, previous_len, last_applied, cycle, seed, nullptr, &in);
+      rc != AMPPI_OK)
+    return rc;
+  ctx->shard_dc = ctx->dc;
+  ctx->shard_dc.k_lo = k_begin;
+  ctx->shard_dc.k_hi = k_end;
+  ctx->shard_in = in;
+  ctx->shard_active = true;
+  cudaError_t e = launch_plan_begin(in, ctx->P, ctx->pl, ctx->shard_dc, ctx->stream, &ctx->timer);
+  return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "launch_plan_begin");
+}
+
+int amppi_shard_screen(amppi_ctx* ctx, int32_t iter, float* local_min) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (!ctx->shard_active || !local_min || iter < 0 || iter >= ctx->dc.iterations)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "amppi_shard_screen: no shard plan / bad iteration");
+  cudaError_t e = launch_shard_screen(ctx->shard_in, ctx->P, ctx->pl, ctx->shard_dc, iter, local_min, ctx->stream,
+                                      &ctx->timer);
+  return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "launch_shard_screen");
+}
+
+int amppi_shard_partials(amppi_ctx* ctx, int32_t iter, const float* global_min, double* partials) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (!ctx->shard_active || !global_min || !partials || iter < 0 || iter >= ctx->dc.iterations)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "amppi_shard_partials: no shard plan / bad argument");
+  cudaError_t e = launch_shard_partials(ctx->shard_in, ctx->P, ctx->pl, ctx->shard_dc, ctx->cand_k, ctx->cand_s,
+                                        ctx->cand_w, ctx->pairs, ctx->pair_count, iter, global_min, partials,
+                                        ctx->stream, &ctx->timer);
+  return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "launch_shard_partials");
+}
+
+int amppi_shard_update(amppi_ctx* ctx, int32_t iter, const double* all_partials, int32_t n_shards) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (!ctx->shard_active || !all_partials || iter < 0 || iter >= ctx->dc.iterations || n_shards < 1 ||
+      n_shards > 64)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "amppi_shard_update: no shard plan / bad argument");
+  cudaError_t e = launch_shard_merge(ctx->shard_in, ctx->pl, ctx->shard_dc, all_partials, n_shards, ctx->stream,
+                                     &ctx->timer);
+  return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "launch_shard_merge");
+}
+
+int amppi_shard_finish(amppi_ctx* ctx, amppi_plan_result* out) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  if (!ctx->shard_active) return ctx->fail(AMPPI_INVALID_ARGUMENT, "amppi_shard_finish: no shard plan");
+  ctx->shard_active = false;
+  const bool want_states = out && (out->winner_states || out->winner_controls);
+  cudaError_t e = launch_plan_finish(ctx->shard_in, ctx->P, ctx->pl, ctx->dc, want_states, ctx->stream, &ctx->timer);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_plan_finish");
+  return collect_plan_result(ctx, out, want_states);
+}
+
+int32_t amppi_shard_partials_stride(const amppi_ctx* ctx) { return ctx ? 3 + 4 * ctx->dc.N : 0; }
 
 static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, bool device_out);
 

@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   __shared__ float s_unom[4 * kMaxN];
   __shared__ float4 s_guide[kMaxN];
   __shared__ float s_bound;
-  const int k_lo = mode == 2 ? k1 : 0;
-  const int k_n = mode == 0 ? cfg.K : (mode == 1 ? k1 : cfg.K - k1);
+  const int k_lo = mode == 2 ? cfg.k_lo + k1 : cfg.k_lo;
+  const int k_n = mode == 0 ? cfg.k_hi - cfg.k_lo : (mode == 1 ? k1 : cfg.k_hi - cfg.k_lo - k1);
   const int tiles = (k_n + blockDim.x - 1) / blockDim.x;
   int b = blockIdx.x;
   const int tile = b % tiles;
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   if (threadIdx.x < 32) {
     float u = __int_as_float(0x7f800000);
     if (mode == 2)
-      for (int k = threadIdx.x; k < k1; k += 32) u = fminf(u, pl.cost32[smi * cfg.K + k]);
+      for (int k = cfg.k_lo + threadIdx.x; k < cfg.k_lo + k1; k += 32) u = fminf(u, pl.cost32[smi * cfg.K + k]);
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (threadIdx.x == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   __shared__ float s_state[kStateWords][kScreenThreads];
   __shared__ int s_k[kScreenThreads];
   __shared__ int s_wcount[2][kScreenThreads / 32];
-  const int k_n = cfg.K - k1;
+  const int k_n = cfg.k_hi - cfg.k_lo - k1;
   const int tiles = (k_n + kScreenThreads - 1) / kScreenThreads;
   int b = blockIdx.x;
   const int tile = b % tiles;
@@ -208,15 +208,15 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* __restrict__ out = pl.cost32 + smi * cfg.K;
   if (!pl.alive[smi]) {
-    const int k = k1 + tile * kScreenThreads + tid;
-    if (k < cfg.K) out[k] = __int_as_float(0x7f800000);
+    const int k = cfg.k_lo + k1 + tile * kScreenThreads + tid;
+    if (k < cfg.k_hi) out[k] = __int_as_float(0x7f800000);
     return;
   }
   for (int i = tid; i < 4 * N; i += kScreenThreads) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
   for (int i = tid; i < N; i += kScreenThreads) s_guide[i] = pl.guide32[smi * N + i];
   if (tid < 32) {
     float u = __int_as_float(0x7f800000);
-    for (int k = tid; k < k1; k += 32) u = fminf(u, out[k]);
+    for (int k = cfg.k_lo + tid; k < cfg.k_lo + k1; k += 32) u = fminf(u, out[k]);
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (tid == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
@@ -256,8 +256,8 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   const uint64_t seed = in.seeds[s];
   PertRngF pr{0ull, static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
               static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
-  int k = k1 + tile * kScreenThreads + tid;
-  bool live = k < cfg.K;
+  int k = cfg.k_lo + k1 + tile * kScreenThreads + tid;
+  bool live = k < cfg.k_hi;
   pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
   const double* xs = in.states + 10 * s;
   St<float> x;
@@ -424,18 +424,19 @@ __global__ void __launch_bounds__(128) k_stage1_col32(Perception P, Plan pl, Dev
 
 cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
                               cudaStream_t st, KernelTimer* timer) {
-  const int64_t total = static_cast<int64_t>(in.S) * cfg.M * cfg.K;
+  const int kr = cfg.k_hi - cfg.k_lo;  // samples per instance screened here
+  const int64_t total = static_cast<int64_t>(in.S) * cfg.M * kr;
   const int64_t SM = static_cast<int64_t>(in.S) * cfg.M;
   static const char* sched = std::getenv("AMPPI_SCREEN");  // experiment switch: "single" disables the bound
   const bool single = sched && std::strcmp(sched, "single") == 0;
   // throughput mode: 64 registers (8 CTAs = 32 warps per SM, a few bytes of
   // L1-resident spill); latency mode: no cap (fastest single rollout)
   auto kern = k_stage1_f32<8>;
-  if (single || total < 148 * 128 * 4 || cfg.K <= 64) {
+  if (single || total < 148 * 128 * 4 || kr <= 64) {
     // latency mode (few rollouts): one pass, warps spread over the SMs
     const int threads = total < 148 * 128 ? 32 : 128;
-    const int tiles = (cfg.K + threads - 1) / threads;
-    if (total < kLatencyRollouts) {
+    const int tiles = (kr + threads - 1) / threads;
+    if (total < kLatencyRollouts && kr == cfg.K) {
       {
         TimedRegion t(timer, "k_stage1_traj32", st);
         k_stage1_traj32<<<static_cast<unsigned>(SM * ((cfg.K + 31) / 32)), 32, 0, st>>>(in, P, pl, cfg, iter);
@@ -454,7 +455,7 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     TimedRegion t(timer, "k_stage1_f32_bound", st);
     kern<<<static_cast<unsigned>(SM * ((k1 + 31) / 32)), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
   }
-  const int tiles = (cfg.K - k1 + kScreenThreads - 1) / kScreenThreads;
+  const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
   TimedRegion t(timer, "k_stage1_f32", st);
   static const char* cmp = std::getenv("AMPPI_COMPACT");  // experiment switch: compaction interval (0 = off)
   const int every = cmp ? std::atoi(cmp) : 3;

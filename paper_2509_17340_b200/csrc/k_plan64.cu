@@ -328,7 +328,11 @@ __device__ __forceinline__ double load_cost(const Plan& pl, int precision, int64
   return precision == 32 ? static_cast<double>(pl.cost32[i]) : pl.cost64[i];
 }
 
-__global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig cfg, UpdateScratch us, int precision) {
+// Softmin support of each instance over samples [k_lo, k_hi): every sample
+// within the window of rho, the screening minimum -- computed here, or the
+// global minimum over all sample shards when rho_ext is given.
+__global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig cfg, UpdateScratch us, int precision,
+                                                            const float* rho_ext) {
   __shared__ double s_red[kSupportThreads / 32];
   __shared__ uint32_t s_cnt[kSupportThreads / 32];
   __shared__ double s_rho;
@@ -341,18 +345,23 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
     return;
   }
   const int64_t base = smi * K;
-  double lmin = kInf;
-  for (int k = tid; k < K; k += blockDim.x) {
-    const double c = load_cost(pl, precision, base + k);
-    if (isfinite(c)) lmin = fmin(lmin, c);
-  }
-  for (int o = 16; o > 0; o >>= 1) lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
-  if (lane == 0) s_red[warp] = lmin;
-  __syncthreads();
-  if (tid == 0) {
-    double r = kInf;
-    for (int w = 0; w < kSupportThreads / 32; ++w) r = fmin(r, s_red[w]);
-    s_rho = r;
+  const int k_lo = cfg.k_lo, kr = cfg.k_hi - cfg.k_lo;
+  if (rho_ext) {
+    if (tid == 0) s_rho = static_cast<double>(rho_ext[smi]);
+  } else {
+    double lmin = kInf;
+    for (int k = k_lo + tid; k < cfg.k_hi; k += blockDim.x) {
+      const double c = load_cost(pl, precision, base + k);
+      if (isfinite(c)) lmin = fmin(lmin, c);
+    }
+    for (int o = 16; o > 0; o >>= 1) lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+    if (lane == 0) s_red[warp] = lmin;
+    __syncthreads();
+    if (tid == 0) {
+      double r = kInf;
+      for (int w = 0; w < kSupportThreads / 32; ++w) r = fmin(r, s_red[w]);
+      s_rho = r;
+    }
   }
   __syncthreads();
   const double rho_s = s_rho;
@@ -364,8 +373,8 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
     return;
   }
   const double window = precision == 32 ? 64.0 * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
-  const int per = (K + blockDim.x - 1) / blockDim.x;
-  const int k0 = min(tid * per, K), k1 = min(k0 + per, K);
+  const int per = (kr + blockDim.x - 1) / blockDim.x;
+  const int k0 = k_lo + min(tid * per, kr), k1 = min(k0 + per, cfg.k_hi);
   uint32_t mine = 0;
   for (int k = k0; k < k1; ++k) {
     const double c = load_cost(pl, precision, base + k);
@@ -500,6 +509,138 @@ __global__ void __launch_bounds__(128) k_nominal(BatchIn in, Plan pl, DevConfig 
       du = du + w * applied;
     }
     nom[jc] = clampv(u + du, lo, hi);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sample sharding (config C4).  A shard screens samples
+// [k_lo, k_hi) of every instance (global k in the RNG key, so its draws are
+// the single-GPU draws), the shards agree on the global screening minimum
+// (all-reduce MIN of k_local_min), each refines its part of the softmin
+// support and reduces it to per-instance partials, and after one all-gather
+// every shard merges the partials in shard order (k_merge) -- the same
+// nominal on every shard, so stage II and the winner are replicated.
+// Partials per instance: {m_g, eta_g, w2_g, ed_g[4N]} with e_k =
+// exp(-(S_k - m_g)/lambda), eta_g = sum e_k, w2_g = sum e_k^2, ed_g[jc] =
+// sum e_k * applied_k[jc] (mppi.cpp:70-101 split by shard).
+// ---------------------------------------------------------------------------
+__global__ void k_local_min(Plan pl, DevConfig cfg, float* out) {
+  const int64_t smi = blockIdx.x;
+  float v = __int_as_float(0x7f800000);
+  if (pl.alive[smi])
+    for (int k = cfg.k_lo + threadIdx.x; k < cfg.k_hi; k += blockDim.x) {
+      const float c = pl.cost32[smi * cfg.K + k];
+      if (isfinite(c)) v = fminf(v, c);
+    }
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (threadIdx.x == 0) out[smi] = v;
+}
+
+__global__ void __launch_bounds__(128) k_partials(BatchIn in, Plan pl, DevConfig cfg, UpdateScratch us, int iter,
+                                                 double* out) {
+  __shared__ double s_m;
+  const int64_t smi = blockIdx.x;
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  const int N = cfg.N, tid = threadIdx.x;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  double* o = out + smi * (3 + 4 * N);
+  const uint32_t n = pl.alive[smi] ? pl.n_support[smi] : 0u;
+  const int64_t base = smi * cfg.K;
+  const uint32_t* cand_k = us.cand_k + base;
+  const double* cand_s = us.cand_s + base;
+  double* cand_w = us.cand_w + base;
+  if (tid == 0) {
+    double mg = kInf;
+    for (uint32_t c = 0; c < n; ++c)
+      if (isfinite(cand_s[c])) mg = dmin(mg, cand_s[c]);
+    double eta = 0.0, w2 = 0.0;
+    if (isfinite(mg))
+      for (uint32_t c = 0; c < n; ++c) {
+        const double e = isfinite(cand_s[c]) ? exp(-(cand_s[c] - mg) / cfg.lambda) : 0.0;
+        cand_w[c] = e;
+        eta += e;
+        w2 += e * e;
+      }
+    o[0] = mg;
+    o[1] = eta;
+    o[2] = w2;
+    s_m = mg;
+  }
+  __syncthreads();
+  const bool live = isfinite(s_m);
+  const Dyn<double> dy = make_dyn<double>(cfg);
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  const double* nom = pl.nominal + smi * N * 4;
+  for (int jc = tid; jc < 4 * N; jc += blockDim.x) {
+    double ed = 0.0;
+    if (live) {
+      const int c = jc & 3;
+      const double u = nom[jc];
+      const double lo = c == 0 ? dy.tmin : (c == 3 ? -dy.wz : -dy.wxy);
+      const double hi = c == 0 ? dy.tmax : (c == 3 ? dy.wz : dy.wxy);
+      for (uint32_t ci = 0; ci < n; ++ci) {
+        const double e = cand_w[ci];
+        if (e == 0.0) continue;
+        const int k = static_cast<int>(cand_k[ci]);
+        double draw;
+        if (in.injected) {
+          draw = injected_row(in, cfg, s, iter, m, k)[jc];
+        } else {
+          const uint64_t key = stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
+          double n0, n1;
+          normal_pair(key, static_cast<uint32_t>(jc >> 1), n0, n1);
+          draw = cfg.sigma[c] * ((jc & 1) ? n1 : n0);
+        }
+        ed = ed + e * (clampv(u + draw, lo, hi) - u);
+      }
+    }
+    o[3 + jc] = ed;
+  }
+}
+
+constexpr int kMaxShards = 64;
+
+__global__ void __launch_bounds__(128) k_merge(Plan pl, DevConfig cfg, const double* parts, int n_shards) {
+  __shared__ double s_a[kMaxShards];
+  __shared__ double s_eta;
+  __shared__ int s_dead;
+  const int64_t smi = blockIdx.x;
+  const int N = cfg.N, tid = threadIdx.x, stride = 3 + 4 * N;
+  const int64_t inst = static_cast<int64_t>(gridDim.x);  // S*M
+  if (tid == 0) {
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double rho = kInf;
+    for (int g = 0; g < n_shards; ++g) rho = dmin(rho, parts[(g * inst + smi) * stride]);
+    s_dead = !isfinite(rho);
+    if (s_dead) {
+      pl.alive[smi] = 0;  // "no valid rollout" on every shard (ensemble.cpp:126)
+      pl.n_support[smi] = 0;
+    } else {
+      double eta = 0.0, w2 = 0.0;
+      for (int g = 0; g < n_shards; ++g) {
+        const double* p = parts + (g * inst + smi) * stride;
+        const double a = isfinite(p[0]) ? exp(-(p[0] - rho) / cfg.lambda) : 0.0;
+        s_a[g] = a;
+        eta += a * p[1];
+        w2 += (a * a) * p[2];
+      }
+      s_eta = eta;
+      pl.stage1[smi] = rho;
+      pl.ess[smi] = w2 > 0.0 ? (eta * eta) / w2 : 0.0;
+    }
+  }
+  __syncthreads();
+  if (s_dead) return;
+  const Dyn<double> dy = make_dyn<double>(cfg);
+  double* nom = pl.nominal + smi * N * 4;
+  for (int jc = tid; jc < 4 * N; jc += blockDim.x) {
+    const int c = jc & 3;
+    const double lo = c == 0 ? dy.tmin : (c == 3 ? -dy.wz : -dy.wxy);
+    const double hi = c == 0 ? dy.tmax : (c == 3 ? dy.wz : dy.wxy);
+    double acc = 0.0;
+    for (int g = 0; g < n_shards; ++g)
+      if (s_a[g] != 0.0) acc = acc + s_a[g] * parts[(g * inst + smi) * stride + 3 + jc];
+    nom[jc] = clampv(nom[jc] + acc / s_eta, lo, hi);
   }
 }
 
@@ -671,61 +812,62 @@ cudaError_t launch_gather(const Plan& pl, const DevConfig& cfg, int S, const Gat
   return cudaGetLastError();
 }
 
-cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
-                             int precision, bool want_winner_rollout, uint32_t* cand_k, double* cand_s, double* cand_w,
-                             uint2* pairs, unsigned long long* pair_count, cudaStream_t st, KernelTimer* timer) {
+static int device_sms() {
+  static int sms = [] {
+    int v = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return sms;
+}
+
+cudaError_t launch_plan_begin(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                              cudaStream_t st, KernelTimer* timer) {
   const int SM = in.S * cfg.M;
+  TimedRegion t(timer, "k_anchors", st);
+  k_anchors<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+  return cudaGetLastError();
+}
+
+// Support + FP64 re-rollout of the support (FP32 screening): fills cand_s.
+static void launch_support_refine(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                                  const UpdateScratch& us, int iter, const float* rho_ext, cudaStream_t st,
+                                  KernelTimer* timer) {
+  const int SM = in.S * cfg.M;
+  const int sms = device_sms();
+  cudaMemsetAsync(us.pair_count, 0, sizeof(unsigned long long), st);
   {
-    TimedRegion t(timer, "k_anchors", st);
-    k_anchors<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+    TimedRegion t(timer, "k_support", st);
+    k_support<<<SM, kSupportThreads, 0, st>>>(pl, cfg, us, 32, rho_ext);
   }
-  const UpdateScratch us{cand_k, cand_s, cand_w, pairs, pair_count};
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (int iter = 0; iter < cfg.iterations; ++iter) {
-    if (precision == 32) {
-      cudaError_t e = launch_stage1_f32(in, P, pl, cfg, iter, st, timer);
-      if (e != cudaSuccess) return e;
-    } else {
-      const int threads = 128;
-      const int tiles = (cfg.K + threads - 1) / threads;
-      TimedRegion t(timer, "k_stage1_f64", st);
-      k_stage1_f64<<<SM * tiles, threads, 4 * cfg.N * sizeof(double), st>>>(in, P, pl, cfg, iter);
-    }
-    cudaMemsetAsync(pair_count, 0, sizeof(unsigned long long), st);
-    {
-      TimedRegion t(timer, "k_support", st);
-      k_support<<<SM, kSupportThreads, 0, st>>>(pl, cfg, us, precision);
-    }
-    if (precision == 32) {
-      // FP64 re-rollout of the support: trajectories first (collision
-      // deferred, positions to pos64), then one warp per rollout for the
-      // collision terms -- a rollout's latency is its trajectory, not 30
-      // sequential exact queries.  Pairs beyond pos_cap take the fused kernel.
-      const int64_t total = static_cast<int64_t>(SM) * cfg.K;
-      const int64_t jobs = std::min<int64_t>(total, pl.pos_cap);
-      {
-        TimedRegion t(timer, "k_refine_traj", st);
-        const int64_t b = (jobs + 63) / 64;
-        k_refine_traj<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
-      }
-      {
-        TimedRegion t(timer, "k_refine_col", st);
-        const int64_t b = (jobs * 32 + 127) / 128;
-        k_refine_col<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 128, 0, st>>>(in, P, pl, cfg, us);
-      }
-      if (total > pl.pos_cap) {
-        TimedRegion t(timer, "k_refine", st);
-        const int64_t b = (total - pl.pos_cap + 63) / 64;
-        k_refine<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(
-            in, P, pl, cfg, us, iter, static_cast<unsigned long long>(pl.pos_cap));
-      }
-    }
-    {
-      TimedRegion t(timer, "k_nominal", st);
-      k_nominal<<<SM, 128, 0, st>>>(in, pl, cfg, us, iter);
-    }
+  // FP64 re-rollout of the support: trajectories first (collision deferred,
+  // positions to pos64), then one warp per rollout for the collision terms --
+  // a rollout's latency is its trajectory, not N sequential exact queries.
+  // Pairs beyond pos_cap take the fused kernel.
+  const int64_t total = static_cast<int64_t>(SM) * (cfg.k_hi - cfg.k_lo);
+  const int64_t jobs = std::min<int64_t>(total, pl.pos_cap);
+  {
+    TimedRegion t(timer, "k_refine_traj", st);
+    const int64_t b = (jobs + 63) / 64;
+    k_refine_traj<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
   }
+  {
+    TimedRegion t(timer, "k_refine_col", st);
+    const int64_t b = (jobs * 32 + 127) / 128;
+    k_refine_col<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 128, 0, st>>>(in, P, pl, cfg, us);
+  }
+  if (total > pl.pos_cap) {
+    TimedRegion t(timer, "k_refine", st);
+    const int64_t b = (total - pl.pos_cap + 63) / 64;
+    k_refine<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(
+        in, P, pl, cfg, us, iter, static_cast<unsigned long long>(pl.pos_cap));
+  }
+}
+
+cudaError_t launch_plan_finish(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                               bool want_winner_rollout, cudaStream_t st, KernelTimer* timer) {
+  const int SM = in.S * cfg.M;
   {
     TimedRegion t(timer, "k_stage2_traj", st);
     k_stage2_traj<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
@@ -742,6 +884,62 @@ cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan&
     TimedRegion t(timer, "k_winner_rollout", st);
     k_winner_rollout<<<(in.S + 31) / 32, 32, 0, st>>>(in, P, pl, cfg);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                             int precision, bool want_winner_rollout, uint32_t* cand_k, double* cand_s, double* cand_w,
+                             uint2* pairs, unsigned long long* pair_count, cudaStream_t st, KernelTimer* timer) {
+  const int SM = in.S * cfg.M;
+  if (cudaError_t e = launch_plan_begin(in, P, pl, cfg, st, timer); e != cudaSuccess) return e;
+  const UpdateScratch us{cand_k, cand_s, cand_w, pairs, pair_count};
+  for (int iter = 0; iter < cfg.iterations; ++iter) {
+    if (precision == 32) {
+      cudaError_t e = launch_stage1_f32(in, P, pl, cfg, iter, st, timer);
+      if (e != cudaSuccess) return e;
+      launch_support_refine(in, P, pl, cfg, us, iter, nullptr, st, timer);
+    } else {
+      const int threads = 128;
+      const int tiles = (cfg.K + threads - 1) / threads;
+      {
+        TimedRegion t(timer, "k_stage1_f64", st);
+        k_stage1_f64<<<SM * tiles, threads, 4 * cfg.N * sizeof(double), st>>>(in, P, pl, cfg, iter);
+      }
+      cudaMemsetAsync(pair_count, 0, sizeof(unsigned long long), st);
+      TimedRegion t(timer, "k_support", st);
+      k_support<<<SM, kSupportThreads, 0, st>>>(pl, cfg, us, precision, nullptr);
+    }
+    {
+      TimedRegion t(timer, "k_nominal", st);
+      k_nominal<<<SM, 128, 0, st>>>(in, pl, cfg, us, iter);
+    }
+  }
+  return launch_plan_finish(in, P, pl, cfg, want_winner_rollout, st, timer);
+}
+
+cudaError_t launch_shard_screen(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
+                                float* local_min, cudaStream_t st, KernelTimer* timer) {
+  if (cudaError_t e = launch_stage1_f32(in, P, pl, cfg, iter, st, timer); e != cudaSuccess) return e;
+  k_local_min<<<in.S * cfg.M, 32, 0, st>>>(pl, cfg, local_min);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_partials(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                                  uint32_t* cand_k, double* cand_s, double* cand_w, uint2* pairs,
+                                  unsigned long long* pair_count, int iter, const float* global_min, double* partials,
+                                  cudaStream_t st, KernelTimer* timer) {
+  const UpdateScratch us{cand_k, cand_s, cand_w, pairs, pair_count};
+  launch_support_refine(in, P, pl, cfg, us, iter, global_min, st, timer);
+  TimedRegion t(timer, "k_partials", st);
+  k_partials<<<in.S * cfg.M, 128, 0, st>>>(in, pl, cfg, us, iter, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_merge(const BatchIn& in, const Plan& pl, const DevConfig& cfg, const double* all_partials,
+                               int n_shards, cudaStream_t st, KernelTimer* timer) {
+  if (n_shards < 1 || n_shards > kMaxShards) return cudaErrorInvalidValue;
+  TimedRegion t(timer, "k_merge", st);
+  k_merge<<<in.S * cfg.M, 128, 0, st>>>(pl, cfg, all_partials, n_shards);
   return cudaGetLastError();
 }
 

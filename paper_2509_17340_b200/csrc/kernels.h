@@ -90,6 +90,23 @@ cudaError_t launch_plan_impl(const BatchIn& in, const Perception& P, const Plan&
                              double* cand_w, uint2* pairs, unsigned long long* pair_count, cudaStream_t st,
                              KernelTimer* timer);
 
+// Phases of launch_plan_impl, used directly by the sample-sharded plan
+// (config C4): begin (anchors, guides, warm start) ... finish (stage II,
+// selection).  Screening / partials / merge work on samples [cfg.k_lo,
+// cfg.k_hi); partials are [S*M*(3+4N)] doubles, all_partials n_shards of them.
+cudaError_t launch_plan_begin(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                              cudaStream_t st, KernelTimer* timer);
+cudaError_t launch_plan_finish(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                               bool want_winner_rollout, cudaStream_t st, KernelTimer* timer);
+cudaError_t launch_shard_screen(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
+                                float* local_min, cudaStream_t st, KernelTimer* timer);
+cudaError_t launch_shard_partials(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
+                                  uint32_t* cand_k, double* cand_s, double* cand_w, uint2* pairs,
+                                  unsigned long long* pair_count, int iter, const float* global_min, double* partials,
+                                  cudaStream_t st, KernelTimer* timer);
+cudaError_t launch_shard_merge(const BatchIn& in, const Plan& pl, const DevConfig& cfg, const double* all_partials,
+                               int n_shards, cudaStream_t st, KernelTimer* timer);
+
 // Per-scene winner outputs gathered into dense arrays (any pointer may be null).
 struct GatherOut {
   int32_t* status;

@@ -39,6 +39,7 @@ constexpr uint64_t kEmptyCell = 0xFFFFFFFFFFFFFFFFull;  // > bits of any finite 
 // Flat copy of amppi_config plus derived sizes.
 struct DevConfig {
   int m_h, m_v, M, K, N, iterations;
+  int k_lo, k_hi;  // samples [k_lo, k_hi) of every instance are screened here (sample sharding); 0, K otherwise
   double lookahead, spacing_deg, terminal_speed, min_anchor_distance;
   double lambda, sigma[4], mppi_dt;
   double q_track, q_vnorm, q_c, q_c_delta, q_p, q_v, q_q;

@@ -325,6 +325,7 @@ class Planner:
         self._gen = 0
         self.precision = precision
         self.max_scenes = max_scenes
+        self.device = device
 
     # -- lifecycle -------------------------------------------------------
     def close(self) -> None:
@@ -401,8 +402,30 @@ class Planner:
         cfg = self.cfg
         M, N, K = cfg.grid.count(), cfg.mppi.horizon, cfg.mppi.rollouts
         la = last_applied if last_applied is not None else cfg.dynamics.hover()
+        prev, prev_len = self._prev(previous)
+        bufs, r = self._result_buffers(want_rollout, want_sample_costs)
+        inj = None
+        if injected_delta is not None:
+            inj = np.ascontiguousarray(injected_delta, dtype=np.float64)
+            expect = cfg.mppi.iterations * M * K * N * 4
+            if inj.size != expect:
+                raise ValueError(f"injected_delta must hold {expect} values")
+        xs, gs, lc = x.to_c(), goal.to_c(), la.to_c()
+        rc = self.lib.amppi_plan(self._h, ctypes.byref(xs), ctypes.byref(gs),
+                                 None if prev is None else _ptr(prev, ctypes.c_double), prev_len,
+                                 ctypes.byref(lc), ctypes.c_uint64(cycle), ctypes.c_uint64(seed),
+                                 None if inj is None else _ptr(inj, ctypes.c_double), ctypes.byref(r))
+        self._check(rc)
+        return self._make_result(r, bufs)
+
+    @staticmethod
+    def _prev(previous):
         prev = None if previous is None else np.ascontiguousarray(np.asarray(previous, dtype=np.float64).reshape(-1, 4))
-        prev_len = 0 if prev is None else int(prev.shape[0])
+        return prev, (0 if prev is None else int(prev.shape[0]))
+
+    def _result_buffers(self, want_rollout: bool, want_sample_costs: bool):
+        cfg = self.cfg
+        M, N, K = cfg.grid.count(), cfg.mppi.horizon, cfg.mppi.rollouts
         bufs = {
             "stage1": np.zeros(M), "stage2": np.zeros(M), "ess": np.zeros(M), "valid": np.zeros(M, dtype=np.uint8),
             "nominal": np.zeros((M, N, 4)), "anchor_initial": np.zeros((M, 3)), "anchor_refined": np.zeros((M, 3)),
@@ -421,18 +444,10 @@ class Planner:
         if want_sample_costs:
             bufs["sample_costs"] = np.zeros((M, K))
             r.sample_costs = _ptr(bufs["sample_costs"], ctypes.c_double)
-        inj = None
-        if injected_delta is not None:
-            inj = np.ascontiguousarray(injected_delta, dtype=np.float64)
-            expect = cfg.mppi.iterations * M * K * N * 4
-            if inj.size != expect:
-                raise ValueError(f"injected_delta must hold {expect} values")
-        xs, gs, lc = x.to_c(), goal.to_c(), la.to_c()
-        rc = self.lib.amppi_plan(self._h, ctypes.byref(xs), ctypes.byref(gs),
-                                 None if prev is None else _ptr(prev, ctypes.c_double), prev_len,
-                                 ctypes.byref(lc), ctypes.c_uint64(cycle), ctypes.c_uint64(seed),
-                                 None if inj is None else _ptr(inj, ctypes.c_double), ctypes.byref(r))
-        self._check(rc)
+        return bufs, r
+
+    def _make_result(self, r, bufs) -> PlanResult:
+        M = self.cfg.grid.count()
         per = [InstanceRecord(float(bufs["stage1"][m]), float(bufs["stage2"][m]), float(bufs["ess"][m]),
                               bool(bufs["valid"][m]), bufs["nominal"][m].copy() if bufs["valid"][m] else None)
                for m in range(M)]
@@ -447,6 +462,39 @@ class Planner:
             winner_states=bufs.get("winner_states"), winner_controls=bufs.get("winner_controls"),
             sample_costs=bufs.get("sample_costs"),
         )
+
+    # -- sample-sharded plan_step (C4) -------------------------------------
+    # Phase calls of amppi_shard_* (include/amppi_b200.h); device buffers are
+    # raw CUDA pointers (e.g. torch tensor .data_ptr()) used on the planner's
+    # stream.  sharding.plan_step_sharded drives them.
+    def shard_begin(self, x: State, goal: GoalSpec, snap: PerceptionSnapshot, previous, last_applied: ControlInput,
+                    cycle: int, seed: int, k_begin: int, k_end: int) -> None:
+        if snap.planner is not self or snap.generation != self._gen:
+            raise ValueError("snapshot does not belong to this planner's current device state")
+        prev, prev_len = self._prev(previous)
+        xs, gs, lc = x.to_c(), goal.to_c(), last_applied.to_c()
+        self._check(self.lib.amppi_shard_begin(self._h, ctypes.byref(xs), ctypes.byref(gs),
+                                               None if prev is None else _ptr(prev, ctypes.c_double), prev_len,
+                                               ctypes.byref(lc), ctypes.c_uint64(cycle), ctypes.c_uint64(seed),
+                                               int(k_begin), int(k_end)))
+
+    def shard_screen(self, it: int, local_min_ptr: int) -> None:
+        self._check(self.lib.amppi_shard_screen(self._h, it, ctypes.c_void_p(local_min_ptr)))
+
+    def shard_partials(self, it: int, global_min_ptr: int, partials_ptr: int) -> None:
+        self._check(self.lib.amppi_shard_partials(self._h, it, ctypes.c_void_p(global_min_ptr),
+                                                  ctypes.c_void_p(partials_ptr)))
+
+    def shard_update(self, it: int, all_partials_ptr: int, n_shards: int) -> None:
+        self._check(self.lib.amppi_shard_update(self._h, it, ctypes.c_void_p(all_partials_ptr), n_shards))
+
+    def shard_finish(self, want_rollout: bool = True) -> PlanResult:
+        bufs, r = self._result_buffers(want_rollout, False)
+        self._check(self.lib.amppi_shard_finish(self._h, ctypes.byref(r)))
+        return self._make_result(r, bufs)
+
+    def shard_partials_stride(self) -> int:
+        return int(self.lib.amppi_shard_partials_stride(self._h))
 
     # -- batched scenes (C5) ---------------------------------------------
     def cycle_batch(self, offsets: np.ndarray, xyz: np.ndarray, poses: np.ndarray, states: np.ndarray,

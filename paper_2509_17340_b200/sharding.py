@@ -70,3 +70,90 @@ def merge_softmin(partials, lam: float):
         w2 += a * a * w2_g
         ed = ed + a * ed_g
     return rho, ed / eta, eta * eta / w2
+
+
+# ---------------------------------------------------------------------------
+# Device path (amppi_shard_*): one planner per GPU, collectives on torch
+# CUDA tensors.  The partial math above is what k_partials / k_merge compute.
+# ---------------------------------------------------------------------------
+class TorchComm:
+    """torch.distributed collectives (NCCL on GPUs) for plan_step_sharded."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce_min(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+
+    def allgather(self, out, t):
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+
+
+def plan_step_sharded(planner, x, goal, snap, previous, last_applied, cycle: int, seed: int, comm,
+                      want_rollout: bool = True):
+    """plan_step with this rank's share of the samples (config C4).
+
+    Every rank calls it with the same inputs; each screens and refines samples
+    shard_ranges(K, world)[rank] of every instance, and all ranks return the
+    same PlanResult.  planner must launch on torch's current CUDA stream (the
+    collectives are ordered on it)."""
+    import torch
+
+    cfg = planner.cfg
+    M, K = cfg.grid.count(), cfg.mppi.rollouts
+    k0, n = shard_ranges(K, comm.world)[comm.rank]
+    if n == 0:
+        raise ValueError("more shards than samples")
+    stream = torch.cuda.current_stream()
+    planner.set_stream(stream.cuda_stream)
+    dev = stream.device
+    stride = planner.shard_partials_stride()
+    local_min = torch.empty(M, dtype=torch.float32, device=dev)
+    partials = torch.empty(M * stride, dtype=torch.float64, device=dev)
+    gathered = torch.empty(comm.world * M * stride, dtype=torch.float64, device=dev)
+    planner.shard_begin(x, goal, snap, previous, last_applied, cycle, seed, k0, k0 + n)
+    for it in range(cfg.mppi.iterations):
+        planner.shard_screen(it, local_min.data_ptr())
+        comm.allreduce_min(local_min)
+        planner.shard_partials(it, local_min.data_ptr(), partials.data_ptr())
+        comm.allgather(gathered, partials)
+        planner.shard_update(it, gathered.data_ptr(), comm.world)
+    return planner.shard_finish(want_rollout)
+
+
+def plan_step_sharded_local(planners, snaps, x, goal, previous, last_applied, cycle: int, seed: int,
+                            want_rollout: bool = True):
+    """The same protocol run in one process over len(planners) contexts (one
+    shard each, any devices): the collectives are plain tensor ops between
+    phases.  Used to check the sharded path against the unsharded plan."""
+    import torch
+
+    G = len(planners)
+    cfg = planners[0].cfg
+    M, K = cfg.grid.count(), cfg.mppi.rollouts
+    ranges = shard_ranges(K, G)
+    stride = planners[0].shard_partials_stride()
+    dev = torch.device("cuda", planners[0].device)
+    mins = [torch.empty(M, dtype=torch.float32, device=dev) for _ in range(G)]
+    parts = [torch.empty(M * stride, dtype=torch.float64, device=dev) for _ in range(G)]
+    for p, sn, (k0, n) in zip(planners, snaps, ranges):
+        p.shard_begin(x, goal, sn, previous, last_applied, cycle, seed, k0, k0 + n)
+    for it in range(cfg.mppi.iterations):
+        for p, lm in zip(planners, mins):
+            p.shard_screen(it, lm.data_ptr())
+            p.synchronize()
+        gmin = torch.stack(mins).amin(dim=0).contiguous()
+        torch.cuda.synchronize(dev)
+        for p, pt in zip(planners, parts):
+            p.shard_partials(it, gmin.data_ptr(), pt.data_ptr())
+            p.synchronize()
+        allp = torch.cat(parts).contiguous()
+        torch.cuda.synchronize(dev)
+        for p in planners:
+            p.shard_update(it, allp.data_ptr(), G)
+            p.synchronize()
+    return [p.shard_finish(want_rollout) for p in planners]
