@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "amppi_b200.h")
 
 def declared_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(amppi_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|void|const char\*)\s+(amppi_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_boundary():
@@ -23,6 +23,12 @@ def test_header_declares_the_boundary():
     for required in ("amppi_create", "amppi_destroy", "amppi_snapshot", "amppi_snapshot_f64", "amppi_plan",
                      "amppi_cycle_batch", "amppi_cycle_batch_device", "amppi_last_error"):
         assert required in names
+
+
+def test_ctypes_mirror_binds_every_declared_function():
+    from paper_2509_17340_b200 import _abi
+
+    assert sorted(_abi.EXPORTS) == declared_functions()
 
 
 def test_library_exports_every_declared_symbol(product_lib):
