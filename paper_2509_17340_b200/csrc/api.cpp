@@ -24,6 +24,7 @@ using namespace amppi_dev;
 namespace {
 
 constexpr double kPi = std::numbers::pi;
+constexpr int kMaxChunks = 4;  // concurrent chunks of a batch (work-list counters)
 
 struct Arena {
   std::vector<void*> blocks;
@@ -135,6 +136,8 @@ struct amppi_ctx {
   cudaStream_t stream{nullptr};
   bool own_stream{false};
   cudaStream_t copy_stream{nullptr};  // host->device point copies overlapped with planning
+  cudaStream_t stream2{nullptr};      // second compute stream: alternate chunks of a batch run concurrently
+  std::vector<cudaEvent_t> join;
   std::vector<cudaEvent_t> chunk_ready;
   std::string err;
   int S_cap{1};
@@ -296,6 +299,12 @@ int create_impl(amppi_ctx* ctx) {
     ctx->own_stream = true;
   }
   CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->join.push_back(ev);
+  }
   CK(init_kernel_attributes());
   Arena& A = ctx->arena;
   // inputs (device + pinned mirror with identical layout)
@@ -426,7 +435,7 @@ int create_impl(amppi_ctx* ctx) {
   ctx->cand_w = static_cast<double*>(p);
   CK(A.alloc(&p, SM * K * sizeof(uint2)));
   ctx->pairs = static_cast<uint2*>(p);
-  CK(A.alloc(&p, sizeof(unsigned long long)));
+  CK(A.alloc(&p, kMaxChunks * sizeof(unsigned long long)));  // one work-list counter per concurrent chunk
   ctx->pair_count = static_cast<unsigned long long*>(p);
   ctx->timer.enabled = ctx->opt.profile != 0;
   return AMPPI_OK;
@@ -482,6 +491,49 @@ Plan shift_plan(const Plan& p, int64_t s0, const DevConfig& c) {
   if (q.winner_states) q.winner_states += s0 * (c.N + 1) * 10;
   if (q.winner_controls) q.winner_controls += s0 * c.N * 4;
   return q;
+}
+
+// Perception arrays of scenes [s0, ...) (the candidate log is indexed by
+// absolute point and needs no shift).
+Perception shift_perception(const Perception& p, int64_t s0) {
+  Perception q = p;
+  q.cell_r += s0 * kCells;
+  q.cell_idx += s0 * kCells;
+  if (q.ranges) q.ranges += s0 * kCells;
+  if (q.has_point) q.has_point += s0 * kCells;
+  if (q.nearest) q.nearest += s0 * kCells * 3;
+  q.filtered += s0 * kCells * 3;
+  q.safe_range += s0 * kCoarse;
+  q.safe_dir += s0 * kCoarse * 3;
+  q.safe_point += s0 * kCoarse * 3;
+  q.n_filtered += s0;
+  q.grid += s0;
+  q.grid_rec += s0 * kGridCells * 2;
+  q.grid_nbr += s0 * kPadCells;
+  q.grid_leaf += s0 * kCells * 2;
+  q.grid_pts64 += s0 * kCells * 3;
+  q.grid_pts32 += s0 * kCells;
+  return q;
+}
+
+// Snapshot + plan of the batch's scenes [s0, s0 + in.S) with every array
+// (perception, plan, support scratch, refine scratch, work-list counter) at
+// the chunk's own offset, so chunks can run concurrently on different
+// streams.  Needs the fused snapshot (>= 148 scenes per chunk).
+int run_chunk(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, int64_t s0, int chunk, cudaStream_t st) {
+  const DevConfig& dc = ctx->dc;
+  const Perception P = shift_perception(ctx->P, s0);
+  Plan pl = shift_plan(ctx->pl, s0, dc);
+  const int64_t sm0 = s0 * dc.M, smc = static_cast<int64_t>(in.S) * dc.M;
+  pl.pos64 += 4 * sm0 * dc.N * 4;
+  pl.tsum += 4 * sm0;
+  pl.pos_cap = std::min<int64_t>(4 * smc, ctx->pl.pos_cap);
+  cudaError_t e = launch_snapshot(in, P, dc, max_pts_scene, st, &ctx->timer);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_snapshot");
+  const int64_t ks = sm0 * dc.K;
+  e = launch_plan_impl(in, P, pl, dc, ctx->opt.precision, false, ctx->cand_k + ks, ctx->cand_s + ks, ctx->cand_w + ks,
+                       ctx->pairs + ks, ctx->pair_count + chunk, st, &ctx->timer);
+  return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "launch_plan");
 }
 
 int run_cycle(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, bool do_snapshot, bool do_plan,
@@ -608,6 +660,8 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  for (cudaEvent_t e : ctx->join) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->chunk_ready) cudaEventDestroy(e);
   delete ctx;
   return AMPPI_OK;
@@ -904,6 +958,8 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   int chunks = static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, (total + (12 << 20)) / (24 << 20))));
   chunks = std::max(1, std::min(chunks, S / 296));
   if (const char* f = std::getenv("AMPPI_PIPELINE_CHUNKS")) chunks = std::max(1, std::min(S, std::atoi(f)));  // tests
+  chunks = std::min(chunks, kMaxChunks);
+  if (chunks > 1 && S / chunks < 148) chunks = 1;  // concurrent chunks need the fused snapshot
   while (static_cast<int>(ctx->chunk_ready.size()) < chunks) {
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -925,6 +981,14 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     tev.push_back(e);
   };
   tmark(ctx->copy_stream);
+  // chunks alternate between the two compute streams (each chunk's arrays
+  // live at its own offset), so one chunk's latency-bound tail overlaps the
+  // next chunk's work; both streams join ctx->stream before the gather
+  const bool concurrent = chunks > 1;
+  if (concurrent) {
+    CK(cudaEventRecord(ctx->join[0], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->stream2, ctx->join[0], 0));
+  }
   for (int c = 0; c < chunks; ++c) {
     const int s0 = static_cast<int>(static_cast<int64_t>(S) * c / chunks);
     const int s1 = static_cast<int>(static_cast<int64_t>(S) * (c + 1) / chunks);
@@ -934,7 +998,8 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
                          cudaMemcpyHostToDevice, ctx->copy_stream));
     CK(cudaEventRecord(ctx->chunk_ready[c], ctx->copy_stream));
     tmark(ctx->copy_stream);
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ready[c], 0));
+    const cudaStream_t cst = (concurrent && (c & 1)) ? ctx->stream2 : ctx->stream;
+    CK(cudaStreamWaitEvent(cst, ctx->chunk_ready[c], 0));
     int64_t max_chunk_scene = 0;
     for (int s = s0; s < s1; ++s)
       max_chunk_scene = std::max(max_chunk_scene, in->point_offsets[s + 1] - in->point_offsets[s]);
@@ -948,8 +1013,16 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     bin.last_applied += 4 * s0;
     bin.cycles += s0;
     bin.seeds += s0;
-    if (int rc = run_cycle(ctx, bin, max_chunk_scene, true, true, false, s0); rc != AMPPI_OK) return rc;
-    tmark(ctx->stream);
+    if (concurrent) {
+      if (int rc = run_chunk(ctx, bin, max_chunk_scene, s0, c, cst); rc != AMPPI_OK) return rc;
+    } else if (int rc = run_cycle(ctx, bin, max_chunk_scene, true, true, false, s0); rc != AMPPI_OK) {
+      return rc;
+    }
+    tmark(cst);
+  }
+  if (concurrent) {
+    CK(cudaEventRecord(ctx->join[1], ctx->stream2));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
   }
   if (trace) {
     cudaDeviceSynchronize();
@@ -989,7 +1062,34 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
   // context's capacity (blocks beyond a scene's end exit immediately)
   const int64_t max_scene = std::max<int64_t>(1, ctx->P_cap / S);
   if (ctx->P.cand_cap < ctx->P_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point capacity");
-  if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
+  int chunks = 1;
+  if (const char* f = std::getenv("AMPPI_DEVICE_CHUNKS")) chunks = std::max(1, std::min(kMaxChunks, std::atoi(f)));
+  if (chunks > 1 && S / chunks < 148) chunks = 1;
+  if (chunks == 1) {
+    if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
+    return batch_outputs_gather(ctx, S, out, true);
+  }
+  CK(cudaEventRecord(ctx->join[0], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->stream2, ctx->join[0], 0));
+  for (int c = 0; c < chunks; ++c) {
+    const int s0 = static_cast<int>(static_cast<int64_t>(S) * c / chunks);
+    const int s1 = static_cast<int>(static_cast<int64_t>(S) * (c + 1) / chunks);
+    BatchIn cb = bin;
+    cb.S = s1 - s0;
+    cb.offsets += s0;
+    cb.poses += 10 * s0;
+    cb.states += 10 * s0;
+    cb.goals += 10 * s0;
+    if (cb.prev) cb.prev += static_cast<int64_t>(s0) * ctx->dc.N * 4;
+    if (cb.prev_len) cb.prev_len += s0;
+    cb.last_applied += 4 * s0;
+    cb.cycles += s0;
+    cb.seeds += s0;
+    if (int rc = run_chunk(ctx, cb, max_scene, s0, c, (c & 1) ? ctx->stream2 : ctx->stream); rc != AMPPI_OK)
+      return rc;
+  }
+  CK(cudaEventRecord(ctx->join[1], ctx->stream2));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
   return batch_outputs_gather(ctx, S, out, true);
 }
 

@@ -553,15 +553,25 @@ __global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn 
         uint32_t base = 0;
         if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
         base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
-        if (cand)
+        if (cand && g - b < 0x10000)
           log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
       }
     }
   }
   __syncthreads();
   // pass B: lowest point index among the logged points at the minimum
-  // ("strict <, first point wins", perception.cpp:80-86)
-  const uint32_t n_cand = sm.n_cand;
+  // ("strict <, first point wins", perception.cpp:80-86).  The log packs the
+  // index in 16 bits; a scene past that (possible on the device entry point,
+  // whose per-scene counts the host cannot see) re-keys all its points.
+  if (e - b > 0x10000) {
+    for (int64_t g = b + tid; g < e; g += blockDim.x) {
+      int f;
+      uint64_t bits;
+      if (key_point(pose, load_point(in, g), r_max, f, bits) && cell_bits[f] == bits)
+        atomicMin(sm.idx + f, static_cast<uint32_t>(g - b));
+    }
+  }
+  const uint32_t n_cand = e - b > 0x10000 ? 0u : sm.n_cand;
   for (uint32_t c = tid; c < n_cand; c += blockDim.x) {
     const uint32_t en = log[c];
     const int f = static_cast<int>(en >> 16);

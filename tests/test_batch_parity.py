@@ -76,15 +76,50 @@ def test_batch_warm_start_matches_oracle(oracle, batch):
     assert _check_against_oracle(oracle, cfg, data, out, previous=first["winner_nominal"], cycle_shift=1) > S // 2
 
 
-def test_pipelined_host_batch_equals_single_chunk(batch, monkeypatch):
+@pytest.fixture(scope="module")
+def big_batch():
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.workloads import plan_config, scenes
+
+    cfg = plan_config()
+    data = scenes(2 * 148 + 5, points=20000, frames=20, first=1000)
+    planner = Planner(cfg, precision=32, max_scenes=len(data["states"]), max_points=int(data["offsets"][-1]))
+    yield cfg, data, planner
+    planner.close()
+
+
+def test_chunked_batches_equal_single_chunk(big_batch, monkeypatch):
     """amppi_cycle_batch overlaps chunk c+1's point upload with chunk c's
-    planning; results must not depend on the chunking."""
-    cfg, data, planner = batch
+    planning, and chunks alternate between two compute streams (host and
+    device entry points); results must not depend on the chunking."""
+    import torch
+
+    cfg, data, planner = big_batch
     one = _host_call(planner, data)
-    monkeypatch.setenv("AMPPI_PIPELINE_CHUNKS", "3")
-    three = _host_call(planner, data)
+    monkeypatch.setenv("AMPPI_PIPELINE_CHUNKS", "2")
+    two = _host_call(planner, data)
     for k in one:
-        assert np.array_equal(one[k], three[k]), k
+        assert np.array_equal(one[k], two[k]), k
+    S = len(data["states"])
+    dev = torch.device("cuda", 0)
+    keep = {k: torch.from_numpy(np.ascontiguousarray(data[k])).to(dev)
+            for k in ("xyz", "offsets", "poses", "states", "goals", "last")}
+    keep["cycles"] = torch.from_numpy(data["cycles"].view(np.int64)).to(dev)
+    keep["seeds"] = torch.from_numpy(data["seeds"].view(np.int64)).to(dev)
+    N, M = cfg.mppi.horizon, cfg.grid.count()
+    for chunks in ("2", "3"):
+        monkeypatch.setenv("AMPPI_DEVICE_CHUNKS", chunks)
+        dout = {"status": torch.zeros(S, dtype=torch.int32, device=dev),
+                "winner": torch.zeros(S, dtype=torch.int32, device=dev),
+                "control": torch.zeros(S, 4, dtype=torch.float64, device=dev),
+                "winner_nominal": torch.zeros(S, N, 4, dtype=torch.float64, device=dev),
+                "stage2": torch.zeros(S, M, dtype=torch.float64, device=dev),
+                "breakdown": torch.zeros(S, 5, dtype=torch.float64, device=dev)}
+        planner.cycle_batch_device({k: v.data_ptr() for k, v in keep.items()},
+                                   {k: v.data_ptr() for k, v in dout.items()}, S, cfg.r_max)
+        planner.synchronize()
+        for k in dout:
+            assert np.array_equal(dout[k].cpu().numpy(), one[k]), (chunks, k)
 
 
 def test_device_entry_point_equals_host(batch):
