@@ -953,13 +953,13 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   // Pipeline: the points of chunk c+1 cross PCIe on the copy stream while
   // chunk c is planned.  Chunks are whole scenes (>= 2 fused-snapshot waves);
   // results land at each scene's batch position.
-  // Chunks cost ~1.5 ms of extra kernel tails each, so keep them large: ~24M
-  // points (3 for C5's 73M), at most 4.
-  int chunks = static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, (total + (12 << 20)) / (24 << 20))));
+  // Up to 4 chunks of >= ~8M points and >= 296 scenes (the smallest one must
+  // keep the fused snapshot: >= 148 scenes).
+  int chunks = static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, total / (8 << 20))));
   chunks = std::max(1, std::min(chunks, S / 296));
   if (const char* f = std::getenv("AMPPI_PIPELINE_CHUNKS")) chunks = std::max(1, std::min(S, std::atoi(f)));  // tests
   chunks = std::min(chunks, kMaxChunks);
-  if (chunks > 1 && S / chunks < 148) chunks = 1;  // concurrent chunks need the fused snapshot
+  while (chunks > 1 && S * 1.0 / ((std::pow(1.6, chunks) - 1.0) / 0.6) < 148) --chunks;  // smallest chunk >= 148
   while (static_cast<int>(ctx->chunk_ready.size()) < chunks) {
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -989,9 +989,20 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     CK(cudaEventRecord(ctx->join[0], ctx->stream));
     CK(cudaStreamWaitEvent(ctx->stream2, ctx->join[0], 0));
   }
+  // Chunk sizes grow geometrically (ratio 1.6 ~ planning time / upload time
+  // per scene on a B200 over PCIe 5): the first chunk's upload is the only
+  // one not hidden behind planning, so it is the smallest.
+  std::vector<int> bound(chunks + 1, 0);
+  {
+    double w = 1.0, sum = 0.0;
+    std::vector<double> cum(chunks + 1, 0.0);
+    for (int c = 0; c < chunks; ++c, w *= 1.6) cum[c + 1] = (sum += w);
+    for (int c = 1; c <= chunks; ++c) bound[c] = static_cast<int>(std::llround(S * cum[c] / sum));
+    bound[chunks] = S;
+  }
   for (int c = 0; c < chunks; ++c) {
-    const int s0 = static_cast<int>(static_cast<int64_t>(S) * c / chunks);
-    const int s1 = static_cast<int>(static_cast<int64_t>(S) * (c + 1) / chunks);
+    const int s0 = bound[c];
+    const int s1 = bound[c + 1];
     const int64_t p0 = in->point_offsets[s0], p1 = in->point_offsets[s1];
     if (p1 > p0)
       CK(cudaMemcpyAsync(ctx->d_xyz + 3 * p0, in->xyz + 3 * p0, static_cast<size_t>(p1 - p0) * 3 * sizeof(float),
