@@ -35,6 +35,23 @@ namespace amppi_dev {
 
 namespace {
 
+#ifdef AMPPI_STATS
+// Per-phase cycle counts of the per-scene snapshot CTA (stats builds only):
+// thread 0 adds the clock delta since the previous mark to slot 16 + i.
+#define SNAP_PHASE(i)                                                                            \
+  do {                                                                                           \
+    if (threadIdx.x == 0) {                                                                      \
+      const long long now = clock64();                                                           \
+      atomicAdd(&g_query_stats[16 + (i)], static_cast<unsigned long long>(now - phase_t));       \
+      phase_t = now;                                                                             \
+    }                                                                                            \
+  } while (0)
+#define SNAP_PHASE_INIT long long phase_t = clock64()
+#else
+#define SNAP_PHASE(i) ((void)0)
+#define SNAP_PHASE_INIT ((void)0)
+#endif
+
 constexpr double kPiD = 0x1.921fb54442d18p+1;      // std::numbers::pi
 constexpr double kHalfPi = 0x1.921fb54442d18p+0;   // 0.5 * pi
 constexpr double kAzStep = 0x1.acee9f37bebd5p-5;   // 2*pi/120 == pi/60
@@ -172,7 +189,7 @@ constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 
 struct FinalizeSmem {
   double rng[kCells];  // also the u64 range-bits table during fused keying, and
-  uint32_t idx[kCells];  // (rng..idx, 86 KB) the sort keys / values of the grid build
+  uint32_t idx[kCells + 1];  // (rng..idx, 86 KB) the sort keys / values of the grid build; then leaf starts
   uint32_t rows[kGridAxis * kGridAxis];  // non-empty grid cells: bit z of row (x, y)
   uint32_t warp_sums[kFinalizeThreads / 32];
   double bbox_lo[kFinalizeThreads / 32][3];
@@ -218,6 +235,7 @@ __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32
 // preceding __syncthreads().
 __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Perception& P, const DevConfig& cfg,
                               int s) {
+  SNAP_PHASE_INIT;
   const int tid = threadIdx.x;
   const int64_t cell_base = static_cast<int64_t>(s) * kCells;
   const int64_t pt_base = in.offsets[s];
@@ -302,6 +320,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
   }
   __syncthreads();
+  SNAP_PHASE(3);  // pooling + filtered compaction + bbox
   if (tid == 0) {
     GridMeta m{};
     m.n_points = static_cast<int>(n_pts);
@@ -336,6 +355,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   __syncthreads();
   const GridMeta meta = sm.meta;
   if (n_pts == 0) return;  // dims = 0: every query returns +inf
+  SNAP_PHASE(4);  // grid meta
 
   // collision grid: sort the filtered points by (cell, Morton code of the
   // 1/8-cell sub-position) with a block bitonic sort in shared memory (the
@@ -391,6 +411,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       }
       __syncthreads();
     }
+  SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
   // leaves of kLeafSize consecutive (Morton-ordered) points
   double* __restrict__ gp64 = P.grid_pts64 + cell_base * 3;
@@ -416,6 +437,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
   }
   __syncthreads();
+  SNAP_PHASE(6);  // scatter + leaf flags
   // leaf ids = prefix count of leaf starts (contiguous 16-point chunks per thread)
   constexpr uint32_t kPerThread = kCellsPow2 / kFinalizeThreads;
   static_assert(kPerThread * kFinalizeThreads == kCellsPow2, "chunking");
@@ -423,50 +445,91 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   uint32_t n_leaf_starts = 0;
   for (uint32_t i = i0; i < i0 + kPerThread; ++i) n_leaf_starts += lflag[i];
   const uint32_t leaf0 = block_exclusive_scan(n_leaf_starts, sm.warp_sums, &sm.total);
-  uint32_t leaf = leaf0;
-  for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
-    if (!lflag[i]) continue;
-    double llo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, lhi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
-    uint32_t t = i;
-    do {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        llo[a] = fmin(llo[a], gp64[3 * t + a]);
-        lhi[a] = fmax(lhi[a], gp64[3 * t + a]);
-      }
-      ++t;
-    } while (t < n_pts && !lflag[t]);
-    gleaf[2 * leaf] = make_uint4(__float_as_uint(__double2float_rd(llo[0])), __float_as_uint(__double2float_rd(llo[1])),
-                                 __float_as_uint(__double2float_rd(llo[2])), 0u);
-    gleaf[2 * leaf + 1] = make_uint4(__float_as_uint(__double2float_ru(lhi[0])),
-                                     __float_as_uint(__double2float_ru(lhi[1])),
-                                     __float_as_uint(__double2float_ru(lhi[2])), 0u);
-    ++leaf;
+  const uint32_t n_leaves = sm.total;
+  // leaf start table (sm.idx is dead by now): point index, bit 31 = starts a cell
+  uint32_t* lstart = sm.idx;
+  {
+    uint32_t leaf = leaf0;
+    for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
+      if (!lflag[i]) continue;
+      const bool cell_start = i == 0 || (keys[i - 1] >> 9) != (keys[i] >> 9);
+      lstart[leaf++] = i | (cell_start ? 0x80000000u : 0u);
+    }
+    if (tid == 0) lstart[n_leaves] = n_pts | 0x80000000u;  // sentinel
   }
   __syncthreads();
-  // cell records: point range, first leaf, box = union of the leaf boxes
-  leaf = leaf0;
-  for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
-    if (!lflag[i]) continue;
-    const uint32_t c = keys[i] >> 9;
-    if (i == 0 || (keys[i - 1] >> 9) != c) {
-      uint32_t e = i + 1;
-      while (e < n_pts && (keys[e] >> 9) == c) ++e;
-      float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
-      for (uint32_t l = leaf; l < leaf + (e - i + kLeafSize - 1) / kLeafSize; ++l) {
-        const uint4 la = gleaf[2 * l], lb = gleaf[2 * l + 1];
-        lo[0] = fminf(lo[0], __uint_as_float(la.x)); lo[1] = fminf(lo[1], __uint_as_float(la.y));
-        lo[2] = fminf(lo[2], __uint_as_float(la.z));
-        hi[0] = fmaxf(hi[0], __uint_as_float(lb.x)); hi[1] = fmaxf(hi[1], __uint_as_float(lb.y));
-        hi[2] = fmaxf(hi[2], __uint_as_float(lb.z));
+  // leaf boxes: 16 lanes per leaf (2 leaves per warp, warp-uniform loop),
+  // coalesced point loads and a 16-lane min/max reduction
+  const int sub = lane & 15;
+  const uint32_t wstride = 2 * (blockDim.x >> 5);
+  for (uint32_t l0 = 2 * warp; l0 < n_leaves; l0 += wstride) {
+    const uint32_t l = l0 + (lane >> 4);
+    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    if (l < n_leaves) {
+      const uint32_t t = (lstart[l] & 0x7FFFFFFFu) + sub;
+      if (t < (lstart[l + 1] & 0x7FFFFFFFu))
+#pragma unroll
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = gp64[3 * t + a];
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+        hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
       }
-      grec[2 * c] = make_uint4(i | ((e - i) << 16), leaf, __float_as_uint(lo[0]), __float_as_uint(lo[1]));
+    if (sub == 0 && l < n_leaves) {
+      gleaf[2 * l] = make_uint4(__float_as_uint(__double2float_rd(lo[0])), __float_as_uint(__double2float_rd(lo[1])),
+                                __float_as_uint(__double2float_rd(lo[2])), 0u);
+      gleaf[2 * l + 1] = make_uint4(__float_as_uint(__double2float_ru(hi[0])), __float_as_uint(__double2float_ru(hi[1])),
+                                    __float_as_uint(__double2float_ru(hi[2])), 0u);
+    }
+  }
+  __syncthreads();
+  SNAP_PHASE(7);  // leaf boxes
+  // cell records: 16 lanes per cell-starting leaf; the cell's leaves are the
+  // leaves up to the next cell start (the sentinel ends the scan); box = union
+  // of their boxes
+  for (uint32_t l0 = 2 * warp; l0 < n_leaves; l0 += wstride) {
+    const uint32_t l = l0 + (lane >> 4);
+    const bool act = l < n_leaves && (lstart[l] & 0x80000000u);
+    uint32_t nl = 0;
+    bool done = !act;
+    for (uint32_t off = 1;; off += 16) {
+      const uint32_t q = l + off + sub;
+      const bool cs = !done && q <= n_leaves && (lstart[q] & 0x80000000u);
+      const unsigned m = (__ballot_sync(0xffffffffu, cs) >> (lane & 16)) & 0xFFFFu;
+      if (!done && m) {
+        nl = off + __ffs(m) - 1;
+        done = true;
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+    float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (uint32_t k = sub; k < nl; k += 16) {
+      const uint4 la = gleaf[2 * (l + k)], lb = gleaf[2 * (l + k) + 1];
+      lo[0] = fminf(lo[0], __uint_as_float(la.x)); lo[1] = fminf(lo[1], __uint_as_float(la.y));
+      lo[2] = fminf(lo[2], __uint_as_float(la.z));
+      hi[0] = fmaxf(hi[0], __uint_as_float(lb.x)); hi[1] = fmaxf(hi[1], __uint_as_float(lb.y));
+      hi[2] = fmaxf(hi[2], __uint_as_float(lb.z));
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+        hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+      }
+    if (sub == 0 && act) {
+      const uint32_t i = lstart[l] & 0x7FFFFFFFu, e = lstart[l + nl] & 0x7FFFFFFFu;
+      const uint32_t c = keys[i] >> 9;
+      grec[2 * c] = make_uint4(i | ((e - i) << 16), l, __float_as_uint(lo[0]), __float_as_uint(lo[1]));
       grec[2 * c + 1] = make_uint4(__float_as_uint(lo[2]), __float_as_uint(hi[0]), __float_as_uint(hi[1]),
                                    __float_as_uint(hi[2]));
     }
-    ++leaf;
   }
   __syncthreads();
+  SNAP_PHASE(8);  // cell records
   // neighbour masks over the padded lattice: bit i*9+j*3+k of padded cell
   // (x, y, z) <-> grid cell (x-2+i, y-2+j, z-2+k) is non-empty
   uint32_t* __restrict__ gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
@@ -489,6 +552,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
     gnbr[c] = m;
   }
+#ifdef AMPPI_STATS
+  __syncthreads();
+  SNAP_PHASE(9);  // neighbour masks
+#endif
 }
 
 // Global schedule, last step: tables from K1/K1b (reset for the next cycle).
@@ -517,12 +584,14 @@ __global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn 
   unsigned long long* cell_bits = reinterpret_cast<unsigned long long*>(sm.rng);
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
+  SNAP_PHASE_INIT;
   if (tid == 0) sm.pose = load_pose(in.poses + 10 * s);
   for (int f = tid; f < kCells; f += blockDim.x) {
     cell_bits[f] = kEmptyCell;
     sm.idx[f] = 0xFFFFFFFFu;
   }
   __syncthreads();
+  SNAP_PHASE(0);  // table init
   const PoseFrame pose = sm.pose;
   const int64_t b = in.offsets[s], e = in.offsets[s + 1];
   const double r_max = in.r_max;
@@ -559,6 +628,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn 
     }
   }
   __syncthreads();
+  SNAP_PHASE(1);  // pass A keying
   // pass B: lowest point index among the logged points at the minimum
   // ("strict <, first point wins", perception.cpp:80-86).  The log packs the
   // index in 16 bits; a scene past that (possible on the device entry point,
@@ -586,12 +656,24 @@ __global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn 
     sm.rng[f] = bits != kEmptyCell ? __longlong_as_double(static_cast<long long>(bits)) : r_max;
   }
   __syncthreads();
+  SNAP_PHASE(2);  // pass B ties
   finalize_body(sm, in, P, cfg, s);
 }
 
 }  // namespace
 
 size_t finalize_smem_bytes() { return sizeof(FinalizeSmem); }
+
+#ifdef AMPPI_STATS
+extern "C" int amppi_snapshot_phase_cycles(unsigned long long* out10, int reset) {
+  cudaMemcpyFromSymbol(out10, g_query_stats, sizeof(unsigned long long) * 10, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[10] = {};
+    cudaMemcpyToSymbol(g_query_stats, z, sizeof(z), sizeof(unsigned long long) * 16);
+  }
+  return 0;
+}
+#endif
 
 cudaError_t init_kernel_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_finalize_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
