@@ -602,13 +602,30 @@ __global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn 
   if (tid == 0) sm.n_cand = 0u;
   __syncthreads();
   const int lane = tid & 31;
-  constexpr int kUnroll = 4;  // loads of kUnroll points in flight per thread
-  for (int64_t g0 = b; g0 < e; g0 += kUnroll * blockDim.x) {
-    V3<double> w[kUnroll];
+  constexpr int kUnroll = 4;  // points per thread per iteration
+  // software pipeline: the next iteration's points are loaded before this
+  // iteration's keys are computed, so the HBM latency overlaps the keying
+  V3<float> nxt[kUnroll];
+  auto fetch = [&](int64_t g0n) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int64_t g = g0 + u * blockDim.x + tid;
-      w[u] = g < e ? load_point(in, g) : V3<double>{0.0, 0.0, 0.0};
+      const int64_t g = g0n + u * blockDim.x + tid;
+      nxt[u] = g < e ? V3<float>{in.xyz[3 * g], in.xyz[3 * g + 1], in.xyz[3 * g + 2]} : V3<float>{0.f, 0.f, 0.f};
+    }
+  };
+  if (!in.xyz64) fetch(b);
+  for (int64_t g0 = b; g0 < e; g0 += kUnroll * blockDim.x) {
+    V3<double> w[kUnroll];
+    if (in.xyz64) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t g = g0 + u * blockDim.x + tid;
+        w[u] = g < e ? load_point(in, g) : V3<double>{0.0, 0.0, 0.0};
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) w[u] = {nxt[u].x, nxt[u].y, nxt[u].z};
+      fetch(g0 + kUnroll * blockDim.x);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
