@@ -648,6 +648,94 @@ __global__ void __launch_bounds__(128) k_merge(Plan pl, DevConfig cfg, const dou
 // per instance with the collision queries deferred, then one warp per
 // instance evaluating the N collision terms in parallel and summing them in
 // step order (costs.hpp:121-127).
+// Warp-cooperative deferred-collision FP64 rollout (latency-critical paths:
+// support refine and stage II).  Only the RK4 recursion is sequential (lane
+// 0); the perturbation draws, clamps and control costs are computed for all
+// steps in parallel before it, and the per-state cost terms in parallel after
+// it, then lane 0 adds every term in rollout_costs' order -- the same FP64
+// values and sums as rollout_costs<double, Pert, true>.  sm: per-warp scratch
+// of kWarpRolloutDoubles(N) doubles.
+constexpr int kRolloutMaxN = 64;
+__host__ __device__ constexpr int warp_rollout_doubles(int N) { return 4 * N + 10 * (N + 1) + 7 * N; }
+
+template <typename Pert>
+__device__ TrajSums rollout_warp64(St<double> x0, const RolloutEnv<double>& env, const Pert& pert, double* pos_out,
+                                   double* sm) {
+  const int lane = threadIdx.x & 31, N = env.N;
+  double* su = sm;                  // [N*4] applied controls
+  double* sx = su + 4 * N;          // [(N+1)*10] states p q v
+  double* st = sx + 10 * (N + 1);   // [7][N]: trk vn g1 g2 g3 mag rate
+  const Dyn<double>& dy = env.dyn;
+  for (int j = lane; j < N; j += 32) {
+    double d[4];
+    pert(j, d);
+    su[4 * j] = clampv(env.unom_at(j, 0) + d[0], dy.tmin, dy.tmax);
+    su[4 * j + 1] = clampv(env.unom_at(j, 1) + d[1], -dy.wxy, dy.wxy);
+    su[4 * j + 2] = clampv(env.unom_at(j, 2) + d[2], -dy.wxy, dy.wxy);
+    su[4 * j + 3] = clampv(env.unom_at(j, 3) + d[3], -dy.wz, dy.wz);
+  }
+  __syncwarp();
+  for (int j = lane; j < N; j += 32) {
+    const double u0 = su[4 * j], u1 = su[4 * j + 1], u2 = su[4 * j + 2], u3 = su[4 * j + 3];
+    st[5 * N + j] = (((u0 * u0 + u1 * u1) + u2 * u2) + u3 * u3);
+    if (j >= 1) {
+      const double e0 = u0 - su[4 * j - 4], e1 = u1 - su[4 * j - 3], e2 = u2 - su[4 * j - 2], e3 = u3 - su[4 * j - 1];
+      st[6 * N + j] = (((e0 * e0 + e1 * e1) + e2 * e2) + e3 * e3);
+    }
+  }
+  int n_ok = N;  // states 0..n_ok-1 are costed; n_ok < N: the rollout went non-finite
+  if (lane == 0) {
+    St<double> x = x0;
+    for (int j = 0; j < N; ++j) {
+      double* o = sx + 10 * j;
+      o[0] = x.p.x; o[1] = x.p.y; o[2] = x.p.z;
+      o[3] = x.q.w; o[4] = x.q.x; o[5] = x.q.y; o[6] = x.q.z;
+      o[7] = x.v.x; o[8] = x.v.y; o[9] = x.v.z;
+      const St<double> nx = rk4_normalized(x, su[4 * j], V3<double>{su[4 * j + 1], su[4 * j + 2], su[4 * j + 3]}, dy);
+      if (!state_finite(nx)) {
+        n_ok = j + 1;  // state j was costed, then the rollout stopped
+        break;
+      }
+      x = nx;
+    }
+  }
+  n_ok = __shfl_sync(0xffffffffu, n_ok, 0);
+  const bool valid = __shfl_sync(0xffffffffu, n_ok == N ? 1 : 0, 0) != 0;
+  __syncwarp();
+  for (int j = lane; j < n_ok; j += 32) {
+    const double* o = sx + 10 * j;
+    const V3<double> p{o[0], o[1], o[2]}, v{o[7], o[8], o[9]};
+    const Q4<double> q{o[3], o[4], o[5], o[6]};
+    if (env.has_guide) st[j] = norm3(p - env.guide_at(j));
+    st[N + j] = sqnorm(v);
+    st[2 * N + j] = env.q_p * norm3(p - env.pg);
+    st[3 * N + j] = env.q_v * norm3(v - env.vg);
+    st[4 * N + j] = env.q_q * env.attitude(q);
+    pos_out[4 * j] = p.x;
+    pos_out[4 * j + 1] = p.y;
+    pos_out[4 * j + 2] = p.z;
+  }
+  __syncwarp();
+  TrajSums t{0, 0, 0, 0, 0, valid ? 1 : 0};
+  if (lane == 0) {
+    double trk = 0.0, vn = 0.0, goal = 0.0, mag = 0.0, rate = 0.0;
+    for (int j = 0; j < n_ok; ++j) {  // rollout_costs' order, step by step
+      if (env.has_guide) trk = trk + st[j];
+      vn = vn + st[N + j];
+      goal = goal + st[2 * N + j];
+      goal = goal + st[3 * N + j];
+      goal = goal + st[4 * N + j];
+      if (j + 1 < N) {
+        mag = mag + st[5 * N + j];
+        if (j >= 1) rate = rate + st[6 * N + j];
+      }
+    }
+    t = TrajSums{trk, vn, mag, rate, goal, valid ? 1 : 0};
+  }
+  return t;
+}
+
+// Throughput form: one thread per instance.
 __global__ void __launch_bounds__(64) k_stage2_traj(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
   const int64_t smi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
@@ -660,6 +748,21 @@ __global__ void __launch_bounds__(64) k_stage2_traj(BatchIn in, Perception P, Pl
     t = TrajSums{cs.trk, cs.vn, cs.mag, cs.rate, cs.goal, cs.valid ? 1 : 0};
   }
   pl.tsum[smi] = t;
+}
+
+// Latency form: one warp per instance (rollout_warp64).
+__global__ void __launch_bounds__(64) k_stage2_traj_w(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+  __shared__ double s_scr[2][warp_rollout_doubles(kRolloutMaxN)];
+  const int64_t smi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
+  TrajSums t{0, 0, 0, 0, 0, 0};
+  if (pl.alive[smi]) {
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    t = rollout_warp64(load_state(in.states + 10 * s), env, PertZero<double>{}, pl.pos64 + smi * cfg.N * 4,
+                       s_scr[threadIdx.x >> 5]);
+  }
+  if ((threadIdx.x & 31) == 0) pl.tsum[smi] = t;
 }
 
 // Sum of the N collision terms of one deferred trajectory, in step order
@@ -706,6 +809,7 @@ __global__ void __launch_bounds__(128) k_stage2_col(BatchIn in, Perception P, Pl
 
 // Latency-path refine: deferred-collision FP64 trajectory per support slot,
 // then a warp per slot for the collision terms.
+// Throughput form: one thread per support pair.
 __global__ void __launch_bounds__(64) k_refine_traj(BatchIn in, Perception P, Plan pl, DevConfig cfg,
                                                     UpdateScratch us, int iter) {
   const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
@@ -729,6 +833,35 @@ __global__ void __launch_bounds__(64) k_refine_traj(BatchIn in, Perception P, Pl
       cs = rollout_costs<double, PertRngD, true>(x0, env, prng, nullptr, nullptr, pos);
     }
     pl.tsum[w] = TrajSums{cs.trk, cs.vn, cs.mag, cs.rate, cs.goal, cs.valid ? 1 : 0};
+  }
+}
+
+// Latency form: one warp per support pair (rollout_warp64).
+__global__ void __launch_bounds__(64) k_refine_traj_w(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                      UpdateScratch us, int iter) {
+  __shared__ double s_scr[2][warp_rollout_doubles(kRolloutMaxN)];
+  const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
+  for (unsigned long long w = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n;
+       w += (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5) {
+    const uint2 pr = us.pairs[w];
+    const int64_t smi = pr.x;
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+    const int k = static_cast<int>(us.cand_k[smi * cfg.K + pr.y]);
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    const St<double> x0 = load_state(in.states + 10 * s);
+    double* pos = pl.pos64 + static_cast<int64_t>(w) * cfg.N * 4;
+    double* scr = s_scr[threadIdx.x >> 5];
+    TrajSums t;
+    if (in.injected) {
+      t = rollout_warp64(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)}, pos, scr);
+    } else {
+      const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+      const PertRngD prng{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                          cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+      t = rollout_warp64(x0, env, prng, pos, scr);
+    }
+    if ((threadIdx.x & 31) == 0) pl.tsum[w] = t;
+    __syncwarp();
   }
 }
 
@@ -849,8 +982,13 @@ static void launch_support_refine(const BatchIn& in, const Perception& P, const 
   const int64_t jobs = std::min<int64_t>(total, pl.pos_cap);
   {
     TimedRegion t(timer, "k_refine_traj", st);
-    const int64_t b = (jobs + 63) / 64;
-    k_refine_traj<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+    if (jobs < static_cast<int64_t>(sms) * 64) {  // too few rollouts to fill the GPU: cut the latency instead
+      const int64_t b = (jobs * 32 + 63) / 64;
+      k_refine_traj_w<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+    } else {
+      const int64_t b = (jobs + 63) / 64;
+      k_refine_traj<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+    }
   }
   {
     TimedRegion t(timer, "k_refine_col", st);
@@ -870,7 +1008,10 @@ cudaError_t launch_plan_finish(const BatchIn& in, const Perception& P, const Pla
   const int SM = in.S * cfg.M;
   {
     TimedRegion t(timer, "k_stage2_traj", st);
-    k_stage2_traj<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+    if (SM < device_sms() * 64)
+      k_stage2_traj_w<<<(SM * 32 + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+    else
+      k_stage2_traj<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
   }
   {
     TimedRegion t(timer, "k_stage2_col", st);
