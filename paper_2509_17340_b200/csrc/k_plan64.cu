@@ -658,6 +658,56 @@ __global__ void __launch_bounds__(128) k_merge(Plan pl, DevConfig cfg, const dou
 constexpr int kRolloutMaxN = 64;
 __host__ __device__ constexpr int warp_rollout_doubles(int N) { return 4 * N + 10 * (N + 1) + 7 * N; }
 
+// rk4_normalized<double> evaluated by a whole warp: every lane runs the
+// quaternion chain (it does not depend on the thrust direction), lanes 0..3
+// then normalise and rotate one RK stage each in parallel, and the
+// velocity / position combination uses the gathered stage accelerations.
+// Same IEEE operations as rk4_normalized, so the same bits; the latency per
+// step is the quaternion chain plus one stage instead of four.
+__device__ __forceinline__ St<double> rk4_normalized_warp(const St<double>& x, double thrust, V3<double> om,
+                                                          const Dyn<double>& d) {
+  const int lane = threadIdx.x & 31;
+  const Q4<double> w0{0.0, om.x, om.y, om.z};
+  auto dq_of = [&](Q4<double> q) {
+    const Q4<double> qd = qmul(q, w0);
+    return Q4<double>{0.5 * qd.w, 0.5 * qd.x, 0.5 * qd.y, 0.5 * qd.z};
+  };
+  auto adv = [](Q4<double> q, Q4<double> dq, double h) {
+    return Q4<double>{q.w + h * dq.w, q.x + h * dq.x, q.y + h * dq.y, q.z + h * dq.z};
+  };
+  const Q4<double> dq1 = dq_of(x.q);
+  const Q4<double> q2 = adv(x.q, dq1, d.half_dt);
+  const Q4<double> dq2 = dq_of(q2);
+  const Q4<double> q3 = adv(x.q, dq2, d.half_dt);
+  const Q4<double> dq3 = dq_of(q3);
+  const Q4<double> q4 = adv(x.q, dq3, d.dt);
+  const Q4<double> dq4 = dq_of(q4);
+  // stage accelerations, one stage per lane
+  const Q4<double> qs = lane == 0 ? x.q : (lane == 1 ? q2 : (lane == 2 ? q3 : q4));
+  const V3<double> dir = qrot(qnormalized(qs), V3<double>{0.0, 0.0, 1.0});
+  const double a = thrust / d.mass;
+  const V3<double> dvl = V3<double>{a * dir.x, a * dir.y, a * dir.z} + V3<double>{d.gx, d.gy, d.gz};
+  V3<double> dv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    dv[i] = {__shfl_sync(0xffffffffu, dvl.x, i), __shfl_sync(0xffffffffu, dvl.y, i),
+             __shfl_sync(0xffffffffu, dvl.z, i)};
+  const V3<double> v2 = x.v + d.half_dt * dv[0];
+  const V3<double> v3 = x.v + d.half_dt * dv[1];
+  const V3<double> v4 = x.v + d.dt * dv[2];
+  const double h6 = d.dt6;
+  St<double> n;
+  n.p = {x.p.x + h6 * rk_comb(x.v.x, v2.x, v3.x, v4.x), x.p.y + h6 * rk_comb(x.v.y, v2.y, v3.y, v4.y),
+         x.p.z + h6 * rk_comb(x.v.z, v2.z, v3.z, v4.z)};
+  n.v = {x.v.x + h6 * rk_comb(dv[0].x, dv[1].x, dv[2].x, dv[3].x),
+         x.v.y + h6 * rk_comb(dv[0].y, dv[1].y, dv[2].y, dv[3].y),
+         x.v.z + h6 * rk_comb(dv[0].z, dv[1].z, dv[2].z, dv[3].z)};
+  n.q = {x.q.w + h6 * rk_comb(dq1.w, dq2.w, dq3.w, dq4.w), x.q.x + h6 * rk_comb(dq1.x, dq2.x, dq3.x, dq4.x),
+         x.q.y + h6 * rk_comb(dq1.y, dq2.y, dq3.y, dq4.y), x.q.z + h6 * rk_comb(dq1.z, dq2.z, dq3.z, dq4.z)};
+  n.q = qnormalized(n.q);
+  return n;
+}
+
 template <typename Pert>
 __device__ TrajSums rollout_warp64(St<double> x0, const RolloutEnv<double>& env, const Pert& pert, double* pos_out,
                                    double* sm) {
@@ -683,24 +733,27 @@ __device__ TrajSums rollout_warp64(St<double> x0, const RolloutEnv<double>& env,
       st[6 * N + j] = (((e0 * e0 + e1 * e1) + e2 * e2) + e3 * e3);
     }
   }
+  __syncwarp();
   int n_ok = N;  // states 0..n_ok-1 are costed; n_ok < N: the rollout went non-finite
-  if (lane == 0) {
-    St<double> x = x0;
+  {
+    St<double> x = x0;  // identical in every lane
     for (int j = 0; j < N; ++j) {
-      double* o = sx + 10 * j;
-      o[0] = x.p.x; o[1] = x.p.y; o[2] = x.p.z;
-      o[3] = x.q.w; o[4] = x.q.x; o[5] = x.q.y; o[6] = x.q.z;
-      o[7] = x.v.x; o[8] = x.v.y; o[9] = x.v.z;
-      const St<double> nx = rk4_normalized(x, su[4 * j], V3<double>{su[4 * j + 1], su[4 * j + 2], su[4 * j + 3]}, dy);
-      if (!state_finite(nx)) {
+      if (lane == 0) {
+        double* o = sx + 10 * j;
+        o[0] = x.p.x; o[1] = x.p.y; o[2] = x.p.z;
+        o[3] = x.q.w; o[4] = x.q.x; o[5] = x.q.y; o[6] = x.q.z;
+        o[7] = x.v.x; o[8] = x.v.y; o[9] = x.v.z;
+      }
+      const St<double> nx =
+          rk4_normalized_warp(x, su[4 * j], V3<double>{su[4 * j + 1], su[4 * j + 2], su[4 * j + 3]}, dy);
+      if (!state_finite(nx)) {  // warp-uniform
         n_ok = j + 1;  // state j was costed, then the rollout stopped
         break;
       }
       x = nx;
     }
   }
-  n_ok = __shfl_sync(0xffffffffu, n_ok, 0);
-  const bool valid = __shfl_sync(0xffffffffu, n_ok == N ? 1 : 0, 0) != 0;
+  const bool valid = n_ok == N;
   __syncwarp();
   for (int j = lane; j < n_ok; j += 32) {
     const double* o = sx + 10 * j;
