@@ -413,8 +413,6 @@ int create_impl(amppi_ctx* ctx) {
     pl.pos_cap = static_cast<int64_t>(jobs);
     if (const char* f = std::getenv("AMPPI_REFINE_SPLIT_CAP"))  // tests: force the fused-refine overflow path
       pl.pos_cap = std::max<int64_t>(0, std::min<int64_t>(pl.pos_cap, std::atoll(f)));
-    CK(A.alloc(&p, static_cast<size_t>(kLatencyRollouts) * N * 4 * sizeof(float)));
-    pl.pos32 = static_cast<float*>(p);
     CK(A.alloc(&p, jobs * N * 4 * sizeof(double)));
     pl.pos64 = static_cast<double*>(p);
     CK(A.alloc(&p, jobs * sizeof(TrajSums)));

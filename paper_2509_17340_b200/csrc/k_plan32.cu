@@ -329,95 +329,176 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   if (live) out[k] = stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd);
 }
 
-// Latency path, pass 1: one thread per rollout, everything but collision;
-// positions to pl.pos32, partial cost to cost32.
-__global__ void __launch_bounds__(32) k_stage1_traj32(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter) {
-  __shared__ float s_unom[4 * kMaxN];
-  __shared__ float4 s_guide[kMaxN];
-  const int tiles = (cfg.K + blockDim.x - 1) / blockDim.x;
-  int b = blockIdx.x;
-  const int tile = b % tiles;
-  b /= tiles;
-  const int m = b % cfg.M;
-  const int s = b / cfg.M;
-  const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
-  const int N = cfg.N;
-  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) s_guide[i] = pl.guide32[smi * N + i];
-  __syncthreads();
-  const int k = tile * blockDim.x + threadIdx.x;
-  if (k >= cfg.K) return;
-  const int64_t r = smi * cfg.K + k;
-  float* out = pl.cost32 + r;
-  if (!pl.alive[smi]) {
-    *out = __int_as_float(0x7f800000);
-    return;
-  }
-  RolloutEnv<float> env;
-  env.unom = s_unom;
-  env.guide = s_guide;
-  env.N = N;
-  env.dyn = make_dyn<float>(cfg);
-  const double* gl = in.goals + 10 * s;
-  env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
-  env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
-  env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
-  env.q_p = static_cast<float>(cfg.q_p);
-  env.q_v = static_cast<float>(cfg.q_v);
-  env.q_q = static_cast<float>(cfg.q_q);
-  env.has_guide = true;
-  env.abort_above = __int_as_float(0x7f800000);
-  env.wq_track = static_cast<float>(cfg.q_track);
-  env.wq_vnorm = static_cast<float>(cfg.q_vnorm);
-  env.wq_c = static_cast<float>(cfg.q_c);
-  env.wq_cd = static_cast<float>(cfg.q_c_delta);
-  const double* xs = in.states + 10 * s;
-  St<float> x0;
-  x0.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
-  x0.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
-  x0.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
-  float* pos = pl.pos32 + r * N * 4;
-  CostSums<float> cs;
-  if (in.injected) {
-    const int64_t row = (((static_cast<int64_t>(s) * cfg.iterations + iter) * cfg.M + m) * cfg.K + k);
-    cs = rollout_costs<float, PertInjected<float>, true>(x0, env, PertInjected<float>{in.injected + row * N * 4},
-                                                         nullptr, nullptr, pos);
-  } else {
-    const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
-    const PertRngF pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
-                      static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
-                      static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
-    cs = rollout_costs<float, PertRngF, true>(x0, env, pr, nullptr, nullptr, pos);
-  }
-  *out = cs.valid ? stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd) : __int_as_float(0x7f800000);
+// Latency path (few rollouts), one warp per rollout: the draws, clamps and
+// control costs of all steps in parallel (lane = step), the RK4 recursion by
+// the whole warp (quaternion chain in every lane, one stage acceleration per
+// lane), then per-state cost terms and collision terms in parallel (lane =
+// step; no abort here), summed in step order by lane 0.
+__device__ __forceinline__ St<float> rk4_normalized_warp32(const St<float>& x, float thrust, V3<float> om,
+                                                           const Dyn<float>& d) {
+  const int lane = threadIdx.x & 31;
+  const Q4<float> w0{0.f, om.x, om.y, om.z};
+  auto dq_of = [&](Q4<float> q) {
+    const Q4<float> qd = qmul(q, w0);
+    return Q4<float>{0.5f * qd.w, 0.5f * qd.x, 0.5f * qd.y, 0.5f * qd.z};
+  };
+  auto adv = [](Q4<float> q, Q4<float> dq, float h) {
+    return Q4<float>{q.w + h * dq.w, q.x + h * dq.x, q.y + h * dq.y, q.z + h * dq.z};
+  };
+  const Q4<float> dq1 = dq_of(x.q);
+  const Q4<float> q2 = adv(x.q, dq1, d.half_dt);
+  const Q4<float> dq2 = dq_of(q2);
+  const Q4<float> q3 = adv(x.q, dq2, d.half_dt);
+  const Q4<float> dq3 = dq_of(q3);
+  const Q4<float> q4 = adv(x.q, dq3, d.dt);
+  const Q4<float> dq4 = dq_of(q4);
+  const Q4<float> qs = lane == 0 ? x.q : (lane == 1 ? q2 : (lane == 2 ? q3 : q4));
+  const V3<float> dir = qrot_ez_fast(qnormalized(qs));
+  const float a = thrust * d.inv_mass;
+  const V3<float> dvl{a * dir.x + d.gx, a * dir.y + d.gy, a * dir.z + d.gz};
+  V3<float> dv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    dv[i] = {__shfl_sync(0xffffffffu, dvl.x, i), __shfl_sync(0xffffffffu, dvl.y, i),
+             __shfl_sync(0xffffffffu, dvl.z, i)};
+  const V3<float> v2 = x.v + d.half_dt * dv[0];
+  const V3<float> v3 = x.v + d.half_dt * dv[1];
+  const V3<float> v4 = x.v + d.dt * dv[2];
+  const float h6 = d.dt6;
+  St<float> n;
+  n.p = {x.p.x + h6 * rk_comb(x.v.x, v2.x, v3.x, v4.x), x.p.y + h6 * rk_comb(x.v.y, v2.y, v3.y, v4.y),
+         x.p.z + h6 * rk_comb(x.v.z, v2.z, v3.z, v4.z)};
+  n.v = {x.v.x + h6 * rk_comb(dv[0].x, dv[1].x, dv[2].x, dv[3].x),
+         x.v.y + h6 * rk_comb(dv[0].y, dv[1].y, dv[2].y, dv[3].y),
+         x.v.z + h6 * rk_comb(dv[0].z, dv[1].z, dv[2].z, dv[3].z)};
+  n.q = {x.q.w + h6 * rk_comb(dq1.w, dq2.w, dq3.w, dq4.w), x.q.x + h6 * rk_comb(dq1.x, dq2.x, dq3.x, dq4.x),
+         x.q.y + h6 * rk_comb(dq1.y, dq2.y, dq3.y, dq4.y), x.q.z + h6 * rk_comb(dq1.z, dq2.z, dq3.z, dq4.z)};
+  n.q = qnormalized(n.q);
+  return n;
 }
 
-// Latency path, pass 2: one warp per rollout, lane j -> collision term of step j.
-__global__ void __launch_bounds__(128) k_stage1_col32(Perception P, Plan pl, DevConfig cfg, int64_t n_rollouts) {
-  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= n_rollouts) return;
-  const float base = pl.cost32[r];
-  if (!isfinite(base)) return;  // invalid rollout or dead instance
-  const int s = static_cast<int>(r / (static_cast<int64_t>(cfg.M) * cfg.K));
-  const GridMeta g = P.grid[s];
-  const uint4* cells = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+constexpr int kWarpsPerCta32 = 4;
 
-  const uint32_t* occ = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
-  const float4* pts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
+__global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn in, Perception P, Plan pl,
+                                                                       DevConfig cfg, int iter) {
+  __shared__ float s_u[kWarpsPerCta32][4 * kMaxN];
+  __shared__ float s_x[kWarpsPerCta32][10 * (kMaxN + 1)];
+  __shared__ float s_t[kWarpsPerCta32][8 * kMaxN];  // trk vn g1 g2 g3 mag rate col
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta32 + wid;  // rollout (smi*K + k)
+  const int kr = cfg.k_hi - cfg.k_lo;
+  if (r >= static_cast<int64_t>(in.S) * cfg.M * kr) return;
+  const int64_t smi = r / kr;
+  const int k = cfg.k_lo + static_cast<int>(r % kr);
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  float* out = pl.cost32 + smi * cfg.K + k;
+  if (!pl.alive[smi]) {
+    if (lane == 0) *out = __int_as_float(0x7f800000);
+    return;
+  }
+  const int N = cfg.N;
+  const Dyn<float> dy = make_dyn<float>(cfg);
+  float* su = s_u[wid];
+  float* sx = s_x[wid];
+  float* st = s_t[wid];
+  const double* unom = pl.nominal + smi * N * 4;
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  const PertRngF pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                    static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
+                    static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
+  const double* inj =
+      in.injected ? in.injected + ((((static_cast<int64_t>(s) * cfg.iterations + iter) * cfg.M + m) * cfg.K + k) * N * 4)
+                  : nullptr;
+  for (int j = lane; j < N; j += 32) {
+    float d[4];
+    if (inj) {
+      PertInjected<float>{inj}(j, d);
+    } else {
+      pr(j, d);
+    }
+    su[4 * j] = clampv(static_cast<float>(unom[4 * j]) + d[0], dy.tmin, dy.tmax);
+    su[4 * j + 1] = clampv(static_cast<float>(unom[4 * j + 1]) + d[1], -dy.wxy, dy.wxy);
+    su[4 * j + 2] = clampv(static_cast<float>(unom[4 * j + 2]) + d[2], -dy.wxy, dy.wxy);
+    su[4 * j + 3] = clampv(static_cast<float>(unom[4 * j + 3]) + d[3], -dy.wz, dy.wz);
+  }
+  __syncwarp();
+  for (int j = lane; j < N; j += 32) {
+    const float u0 = su[4 * j], u1 = su[4 * j + 1], u2 = su[4 * j + 2], u3 = su[4 * j + 3];
+    st[5 * N + j] = (((u0 * u0 + u1 * u1) + u2 * u2) + u3 * u3);
+    if (j >= 1) {
+      const float e0 = u0 - su[4 * j - 4], e1 = u1 - su[4 * j - 3], e2 = u2 - su[4 * j - 2], e3 = u3 - su[4 * j - 1];
+      st[6 * N + j] = (((e0 * e0 + e1 * e1) + e2 * e2) + e3 * e3);
+    }
+  }
+  const double* xs = in.states + 10 * s;
+  St<float> x;
+  x.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
+  x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
+  int n_ok = N;
+  __syncwarp();
+  for (int j = 0; j < N; ++j) {
+    if (lane == 0) {
+      float* o = sx + 10 * j;
+      o[0] = x.p.x; o[1] = x.p.y; o[2] = x.p.z;
+      o[3] = x.q.w; o[4] = x.q.x; o[5] = x.q.y; o[6] = x.q.z;
+      o[7] = x.v.x; o[8] = x.v.y; o[9] = x.v.z;
+    }
+    const St<float> nx = rk4_normalized_warp32(x, su[4 * j], V3<float>{su[4 * j + 1], su[4 * j + 2], su[4 * j + 3]}, dy);
+    if (!state_finite(nx)) {
+      n_ok = j + 1;
+      break;
+    }
+    x = nx;
+  }
+  __syncwarp();
+  // per-state terms + collision, lane = step
+  const double* gl = in.goals + 10 * s;
+  const V3<float> pg{static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  const V3<float> vg{static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
+  const Q4<float> qg{static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]),
+                     static_cast<float>(gl[9])};
+  const GridMeta g = P.grid[s];
+  const uint4* grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+  const uint32_t* gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  const uint4* gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
+  const float4* gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   const float cs = static_cast<float>(cfg.col_scale), ca = static_cast<float>(cfg.col_slope);
   const float dmin = static_cast<float>(cfg.col_d_min), dmax = static_cast<float>(cfg.col_d_max);
-  const float* pos = pl.pos32 + r * cfg.N * 4;
-  float col = 0.f;
-  for (int j = lane; j < cfg.N; j += 32) {
-    const V3<float> p{pos[4 * j], pos[4 * j + 1], pos[4 * j + 2]};
+  const float4* guide = pl.guide32 + smi * N;
+  for (int j = lane; j < n_ok; j += 32) {
+    const float* o = sx + 10 * j;
+    const V3<float> p{o[0], o[1], o[2]}, v{o[7], o[8], o[9]};
+    const Q4<float> q{o[3], o[4], o[5], o[6]};
+    const float4 gd = guide[j];
+    st[j] = norm3(p - V3<float>{gd.x, gd.y, gd.z});
+    st[N + j] = sqnorm(v);
+    st[2 * N + j] = static_cast<float>(cfg.q_p) * norm3(p - pg);
+    st[3 * N + j] = static_cast<float>(cfg.q_v) * norm3(v - vg);
+    st[4 * N + j] = static_cast<float>(cfg.q_q) * attitude_err_fast(q, qg);
     uint32_t hint = kNoHint;
-    const float d2 = nearest_sq_fast(g, cells, occ, P.grid_leaf + static_cast<int64_t>(s) * kCells * 2, pts, p,
-                                     dmax * dmax * 1.0001f, dmin * dmin, &hint);
-    col += collision_term(sqrtf(d2), cs, ca, dmin, dmax);
+    const float d2 = nearest_sq_fast(g, grec, gnbr, gleaf, gpts, p, dmax * dmax * 1.0001f, dmin * dmin, &hint);
+    st[7 * N + j] = collision_term(sqrtf(d2), cs, ca, dmin, dmax);
   }
-  for (int o = 16; o > 0; o >>= 1) col += __shfl_xor_sync(0xffffffffu, col, o);
-  if (lane == 0) pl.cost32[r] = base + col;
+  __syncwarp();
+  if (lane == 0) {
+    float trk = 0.f, vn = 0.f, goal = 0.f, mag = 0.f, rate = 0.f, col = 0.f;
+    for (int j = 0; j < n_ok; ++j) {
+      trk = trk + st[j];
+      vn = vn + st[N + j];
+      goal = goal + st[2 * N + j];
+      goal = goal + st[3 * N + j];
+      goal = goal + st[4 * N + j];
+      col = col + st[7 * N + j];
+      if (j + 1 < N) {
+        mag = mag + st[5 * N + j];
+        if (j >= 1) rate = rate + st[6 * N + j];
+      }
+    }
+    const float wt = static_cast<float>(cfg.q_track), wv = static_cast<float>(cfg.q_vnorm);
+    const float wc = static_cast<float>(cfg.q_c), wd = static_cast<float>(cfg.q_c_delta);
+    *out = n_ok == N ? ((wt * trk + wv * vn) + (wc * mag + wd * rate)) + (goal + col) : __int_as_float(0x7f800000);
+  }
 }
 
 }  // namespace
@@ -436,13 +517,10 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     // latency mode (few rollouts): one pass, warps spread over the SMs
     const int threads = total < 148 * 128 ? 32 : 128;
     const int tiles = (kr + threads - 1) / threads;
-    if (total < kLatencyRollouts && kr == cfg.K) {
-      {
-        TimedRegion t(timer, "k_stage1_traj32", st);
-        k_stage1_traj32<<<static_cast<unsigned>(SM * ((cfg.K + 31) / 32)), 32, 0, st>>>(in, P, pl, cfg, iter);
-      }
-      TimedRegion t(timer, "k_stage1_col32", st);
-      k_stage1_col32<<<static_cast<unsigned>((total * 32 + 127) / 128), 128, 0, st>>>(P, pl, cfg, total);
+    if (total < kLatencyRollouts) {
+      TimedRegion t(timer, "k_stage1_warp32", st);
+      k_stage1_warp32<<<static_cast<unsigned>((total + kWarpsPerCta32 - 1) / kWarpsPerCta32), 32 * kWarpsPerCta32, 0,
+                        st>>>(in, P, pl, cfg, iter);
       return cudaGetLastError();
     }
     TimedRegion t(timer, "k_stage1_f32", st);

@@ -112,8 +112,8 @@ struct TrajSums {
   int valid;
 };
 
-// Rollouts up to this count per call run the latency path: sequential
-// trajectory pass + parallel collision pass.
+// Rollouts up to this count per call run the latency path: one warp per
+// rollout (k_stage1_warp32).
 constexpr int kLatencyRollouts = 148 * 128;
 
 struct Plan {
@@ -139,7 +139,6 @@ struct Plan {
   double* breakdown;           // [S*M*5]
   uint32_t* n_support;         // [S*M] softmin support size (diagnostics)
   // deferred-collision scratch (latency path and stage II)
-  float* pos32;                // [kLatencyRollouts*N*4]
   double* pos64;               // [pos_cap*N*4]
   TrajSums* tsum;              // [pos_cap]
   int64_t pos_cap;             // support pairs the split refine handles (pos64/tsum hold max(4*S*M, kLatencyRollouts))
