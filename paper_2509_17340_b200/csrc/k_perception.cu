@@ -183,17 +183,18 @@ __global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
 // ---------------------------------------------------------------------------
 // finalize body
 // ---------------------------------------------------------------------------
-constexpr int kFinalizeThreads = 256;
-constexpr int kChunk = (kCells + kFinalizeThreads - 1) / kFinalizeThreads;  // 15
+constexpr int kFinalizeThreads = 256;      // fused per-scene CTAs (two per SM)
+constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
+constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 
 struct FinalizeSmem {
   double rng[kCells];  // also the u64 range-bits table during fused keying, and
   uint32_t idx[kCells + 1];  // (rng..idx, 86 KB) the sort keys / values of the grid build; then leaf starts
   uint32_t rows[kGridAxis * kGridAxis];  // non-empty grid cells: bit z of row (x, y)
-  uint32_t warp_sums[kFinalizeThreads / 32];
-  double bbox_lo[kFinalizeThreads / 32][3];
-  double bbox_hi[kFinalizeThreads / 32][3];
+  uint32_t warp_sums[kMaxWarps];
+  double bbox_lo[kMaxWarps][3];
+  double bbox_hi[kMaxWarps][3];
   GridMeta meta;
   PoseFrame pose;
   uint32_t total;
@@ -273,8 +274,9 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   }
 
   // filtered_cloud + to_world_frame in flat order (perception.cpp:124-144)
-  const int f0 = tid * kChunk;
-  const int f1 = min(f0 + kChunk, kCells);
+  const int chunk = (kCells + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
+  const int f0 = tid * chunk;
+  const int f1 = min(f0 + chunk, kCells);
   uint32_t mine = 0;
   for (int f = f0; f < f1; ++f) mine += sm.idx[f] != 0xFFFFFFFFu;
   const uint32_t pos0 = block_exclusive_scan(mine, sm.warp_sums, &sm.total);
@@ -439,8 +441,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   __syncthreads();
   SNAP_PHASE(6);  // scatter + leaf flags
   // leaf ids = prefix count of leaf starts (contiguous 16-point chunks per thread)
-  constexpr uint32_t kPerThread = kCellsPow2 / kFinalizeThreads;
-  static_assert(kPerThread * kFinalizeThreads == kCellsPow2, "chunking");
+  const uint32_t kPerThread = kCellsPow2 / blockDim.x;  // blockDim.x divides 8192
   const uint32_t i0 = tid * kPerThread;
   uint32_t n_leaf_starts = 0;
   for (uint32_t i = i0; i < i0 + kPerThread; ++i) n_leaf_starts += lflag[i];
@@ -559,7 +560,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
 }
 
 // Global schedule, last step: tables from K1/K1b (reset for the next cycle).
-__global__ void __launch_bounds__(kFinalizeThreads, 2) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
+__global__ void __launch_bounds__(kFinalizeThreadsFew, 1) k_finalize_scene(BatchIn in, Perception P, DevConfig cfg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
   const int s = blockIdx.x;
@@ -725,7 +726,7 @@ cudaError_t launch_snapshot(const BatchIn& in, const Perception& P, const DevCon
   }
   {
     TimedRegion t(timer, "k_finalize_scene", st);
-    k_finalize_scene<<<in.S, kFinalizeThreads, sizeof(FinalizeSmem), st>>>(in, P, cfg);
+    k_finalize_scene<<<in.S, kFinalizeThreadsFew, sizeof(FinalizeSmem), st>>>(in, P, cfg);
   }
   return cudaGetLastError();
 }
