@@ -75,11 +75,20 @@ __device__ __forceinline__ bool near_integer(double v) {
 // ---------------------------------------------------------------------------
 // K4: anchors, guides, warm start
 // ---------------------------------------------------------------------------
+// kL lanes per (scene, instance): lane 0 places the anchor and solves the
+// quintic; the guide table and the warm start are filled lane-parallel.
+// kL = 32 (one warp) for few instances (latency), 1 for many (throughput).
+template <int kL>
 __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double s_c[64 / kL][18];
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / kL;
+  const int lane = static_cast<int>(threadIdx.x % kL), wid = static_cast<int>(threadIdx.x / kL);
   const int M = cfg.M, N = cfg.N;
   if (gid >= in.S * M) return;
   const int s = gid / M, m = gid % M;
+  const int64_t sm = static_cast<int64_t>(s) * M + m;
+  const double T = static_cast<double>(N) * cfg.mppi_dt;
+  if (lane == 0) {
   const St<double> x = load_state(in.states + 10 * s);
   const double* gl = in.goals + 10 * s;
   const V3<double> goal_p{gl[0], gl[1], gl[2]};
@@ -141,7 +150,6 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
     safe_range = in.r_max;
     terminal_speed = 0.0;
   }
-  const int64_t sm = static_cast<int64_t>(s) * M + m;
   double* ai = pl.anchor_init + 3 * sm;
   double* ar = pl.anchor_ref + 3 * sm;
   double* ad = pl.anchor_dir + 3 * sm;
@@ -160,7 +168,6 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
   const V3<double> a0 = derivative(x, lt, lw, dy).dv;
   const V3<double> end_v = terminal_speed * safe_dir;
   // solve_quintic (guidance.cpp:74-94)
-  const double T = horizon_s;
   const double T2 = T * T, T3 = T2 * T, T4 = T3 * T, T5 = T4 * T;
   const V3<double> half_a = 0.5 * a0;
   const V3<double> dp = refined - ((x.p + T * x.v) + T2 * half_a);
@@ -189,9 +196,16 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
     gc[k] = c[k].x;
     gc[6 + k] = c[k].y;
     gc[12 + k] = c[k].z;
+    s_c[wid][3 * k] = c[k].x;
+    s_c[wid][3 * k + 1] = c[k].y;
+    s_c[wid][3 * k + 2] = c[k].z;
   }
+  }  // lane 0
+  if (kL > 1) __syncwarp();
+  V3<double> c[6];
+  for (int k = 0; k < 6; ++k) c[k] = {s_c[wid][3 * k], s_c[wid][3 * k + 1], s_c[wid][3 * k + 2]};
   // guide table g(t * dt) for t < N (tracking cost, costs.hpp:59-66)
-  for (int t = 0; t < N; ++t) {
+  for (int t = lane; t < N; t += kL) {
     double tt = static_cast<double>(t) * cfg.dyn_dt;
     tt = clampv(tt, 0.0, T);
     V3<double> o = c[5];
@@ -207,23 +221,25 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
   double* nom = pl.nominal + sm * N * 4;
   if (plen == N) {
     const double* pv = in.prev + static_cast<int64_t>(s) * N * 4;
-    for (int j = 0; j < N; ++j) {
+    for (int j = lane; j < N; j += kL) {
       const int src = j + 1 < N ? j + 1 : N - 1;
       for (int cc = 0; cc < 4; ++cc) nom[4 * j + cc] = pv[4 * src + cc];
     }
   } else {
     const double hover = cfg.mass * sqrt((cfg.gravity[0] * cfg.gravity[0] + cfg.gravity[1] * cfg.gravity[1]) +
                                          cfg.gravity[2] * cfg.gravity[2]);
-    for (int j = 0; j < N; ++j) {
+    for (int j = lane; j < N; j += kL) {
       nom[4 * j] = hover;
       nom[4 * j + 1] = 0.0;
       nom[4 * j + 2] = 0.0;
       nom[4 * j + 3] = 0.0;
     }
   }
-  pl.alive[sm] = 1;
-  pl.stage1[sm] = 0.0;
-  pl.ess[sm] = 0.0;
+  if (lane == 0) {
+    pl.alive[sm] = 1;
+    pl.stage1[sm] = 0.0;
+    pl.ess[sm] = 0.0;
+  }
 }
 
 // Fill an FP64 rollout environment for (scene, instance); unom may point to
@@ -1012,7 +1028,10 @@ cudaError_t launch_plan_begin(const BatchIn& in, const Perception& P, const Plan
                               cudaStream_t st, KernelTimer* timer) {
   const int SM = in.S * cfg.M;
   TimedRegion t(timer, "k_anchors", st);
-  k_anchors<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+  if (SM < device_sms() * 16)
+    k_anchors<32><<<(SM * 32 + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+  else
+    k_anchors<1><<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
   return cudaGetLastError();
 }
 
