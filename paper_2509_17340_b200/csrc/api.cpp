@@ -137,6 +137,7 @@ struct amppi_ctx {
   bool own_stream{false};
   cudaStream_t copy_stream{nullptr};  // host->device point copies overlapped with planning
   cudaStream_t stream2{nullptr};      // second compute stream: alternate chunks of a batch run concurrently
+  cudaEvent_t inputs_read{nullptr};   // single-scene snapshot inputs copied (staging reusable)
   std::vector<cudaEvent_t> join;
   std::vector<cudaEvent_t> chunk_ready;
   std::string err;
@@ -300,6 +301,7 @@ int create_impl(amppi_ctx* ctx) {
   }
   CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->inputs_read, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -659,6 +661,7 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->inputs_read) cudaEventDestroy(ctx->inputs_read);
   for (cudaEvent_t e : ctx->join) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->chunk_ready) cudaEventDestroy(e);
   delete ctx;
@@ -690,8 +693,17 @@ static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n,
   if (int rc = alloc_points(ctx, n); rc != AMPPI_OK) return rc;
   const size_t bytes = static_cast<size_t>(n) * 3 * (f64 ? sizeof(double) : sizeof(float));
   if (n > 0) {
-    std::memcpy(ctx->h_xyz, pts, bytes);
-    CK(cudaMemcpyAsync(f64 ? static_cast<void*>(ctx->d_xyz64) : static_cast<void*>(ctx->d_xyz), ctx->h_xyz, bytes,
+    // page-locked caller memory is read by the DMA engine directly; anything
+    // else goes through the context's pinned staging buffer
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, pts) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    if (!pinned) cudaGetLastError();  // clear a possible "invalid value" from unregistered memory
+    const void* src = pts;
+    if (!pinned) {
+      std::memcpy(ctx->h_xyz, pts, bytes);
+      src = ctx->h_xyz;
+    }
+    CK(cudaMemcpyAsync(f64 ? static_cast<void*>(ctx->d_xyz64) : static_cast<void*>(ctx->d_xyz), src, bytes,
                        cudaMemcpyHostToDevice, ctx->stream));
   }
   put_pose(ctx->hin.poses, pose);
@@ -700,15 +712,20 @@ static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n,
   // upload pose + offsets (the start of the input block)
   CK(cudaMemcpyAsync(ctx->din.poses, ctx->hin.poses, 10 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->din.offsets, ctx->hin.offsets, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->inputs_read, ctx->stream));
   BatchIn in = batch_from_block(ctx, 1, r_max, f64);
   if (int rc = run_cycle(ctx, in, n, true, false, false); rc != AMPPI_OK) return rc;
   ctx->have_snapshot = true;
   ctx->snap_r_max = r_max;
   ctx->snap_points = n;
   std::memcpy(ctx->snap_pose, pose, sizeof(ctx->snap_pose));
-  // cudaMemcpyAsync from pinned staging: the staging buffer is reused by the
-  // next call, so finish the copy before returning.
-  return sync_and_collect(ctx);
+  // Return once the inputs have been copied (the caller's buffer and the
+  // staging block may be reused); the snapshot kernels keep running and the
+  // plan that follows queues behind them on the stream -- no host round trip
+  // between build_snapshot and plan_step.  Kernel errors surface at the next
+  // synchronising call.
+  CK(cudaEventSynchronize(ctx->inputs_read));
+  return AMPPI_OK;
 }
 
 int amppi_snapshot(amppi_ctx* ctx, const float* xyz, int64_t n, const amppi_state* pose, double r_max) {
@@ -722,6 +739,7 @@ int amppi_snapshot_f64(amppi_ctx* ctx, const double* xyz, int64_t n, const amppi
 int amppi_snapshot_download(amppi_ctx* ctx, amppi_snapshot_view* v) {
   if (!ctx || !v) return AMPPI_INVALID_ARGUMENT;
   if (!ctx->have_snapshot) return ctx->fail(AMPPI_NO_SNAPSHOT, "no snapshot");
+  if (int rc = sync_and_collect(ctx); rc != AMPPI_OK) return rc;  // the snapshot kernels may still run
   const Perception& P = ctx->P;
   if ((v->ranges || v->has_point || v->nearest) && !P.ranges)
     return ctx->fail(AMPPI_INVALID_ARGUMENT, "verification views need max_scenes <= 64");
