@@ -218,9 +218,12 @@ __device__ __forceinline__ void normal_pair_f(uint64_t key, uint32_t p, float& n
     lg = logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
   }
   const float r = sqrtf(-2.0f * lg);
-  const float u2x2 = static_cast<float>(b >> 11) * 0x1.0p-52f;  // 2*u2
+  // angle 2*pi*u2 in [0, 2pi): hardware sin/cos after reduction to [-pi, pi)
+  // (abs error ~1e-6, far inside the screening window)
+  const float u2 = static_cast<float>(b >> 11) * 0x1.0p-53f;
+  const float ang = 6.28318530717958647f * (u2 < 0.5f ? u2 : u2 - 1.0f);
   float s, c;
-  sincospif(u2x2, &s, &c);
+  __sincosf(ang, &s, &c);
   n0 = r * c;
   n1 = r * s;
 }
