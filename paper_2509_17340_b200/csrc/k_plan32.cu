@@ -536,7 +536,7 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
   TimedRegion t(timer, "k_stage1_f32", st);
   static const char* cmp = std::getenv("AMPPI_COMPACT");  // experiment switch: compaction interval (0 = off)
-  const int every = cmp ? std::atoi(cmp) : 3;
+  const int every = cmp ? std::atoi(cmp) : 10;
   if (in.injected || every <= 0) {
     kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
   } else if (every == 1) {
@@ -547,8 +547,12 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     k_stage1_f32c<8, 3><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
   } else if (every <= 5) {
     k_stage1_f32c<8, 5><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-  } else {
+  } else if (every <= 8) {
     k_stage1_f32c<8, 8><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  } else if (every <= 10) {
+    k_stage1_f32c<8, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+  } else {
+    k_stage1_f32c<8, 15><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
   }
   return cudaGetLastError();
 }
