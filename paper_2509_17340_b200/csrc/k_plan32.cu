@@ -26,9 +26,11 @@ constexpr int kMaxN = 64;
 
 // mode 0: every sample, no bound.  mode 1: samples [0, k1) without bound.
 // mode 2: samples [k1, K) aborted once their partial cost exceeds
-// U + 2 window, U = min cost of samples [0, k1) -- an actual sample cost, so
-// the instance minimum rho <= U and no softmin-support member (cost <= rho +
-// 64 lambda) can abort.  Aborted samples report FLT_MAX.
+// U + window(U), U = min cost of samples [0, k1) -- an actual sample cost,
+// so the instance minimum rho <= U.  The FP32 partial sums only grow towards
+// the final FP32 cost (non-negative terms, monotone rounding), so an aborted
+// sample ends above rho + window(rho) (window(U) >= window(rho)): outside the
+// support k_support selects.  Aborted samples report FLT_MAX.
 template <int kMinBlocks>
 __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perception P, Plan pl, DevConfig cfg,
                                                                 int iter, int mode, int k1) {
@@ -54,7 +56,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (threadIdx.x == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
-      s_bound = (mode == 2 && u < 3.0e38f) ? u + 2.0f * window : __int_as_float(0x7f800000);
+      // + 1e-6 |u| covers the float rounding of the threshold itself
+      s_bound = (mode == 2 && u < 3.0e38f) ? u + window + (1e-6f * fabsf(u) + 1e-5f) : __int_as_float(0x7f800000);
     }
   }
   __syncthreads();
@@ -220,7 +223,8 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (tid == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
-      s_bound = u < 3.0e38f ? u + 2.0f * window : __int_as_float(0x7f800000);
+      // + 1e-6 |u| covers the float rounding of the threshold itself
+      s_bound = u < 3.0e38f ? u + window + (1e-6f * fabsf(u) + 1e-5f) : __int_as_float(0x7f800000);
     }
   }
   __syncthreads();
