@@ -554,7 +554,18 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   } else if (every <= 8) {
     k_stage1_f32c<8, 8><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
   } else if (every <= 10) {
-    k_stage1_f32c<8, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+    static const char* mb = std::getenv("AMPPI_MINBLOCKS");  // experiment switch: register budget
+    const int minb = mb ? std::atoi(mb) : 9;
+    if (minb == 10)
+      k_stage1_f32c<10, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+    else if (minb == 9)
+      k_stage1_f32c<9, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+    else if (minb == 6)
+      k_stage1_f32c<6, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+    else if (minb == 7)
+      k_stage1_f32c<7, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+    else
+      k_stage1_f32c<8, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
   } else {
     k_stage1_f32c<8, 15><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
   }
