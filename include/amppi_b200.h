@@ -217,6 +217,35 @@ int amppi_shard_update(amppi_ctx* ctx, int32_t iter, const double* all_partials,
 int amppi_shard_finish(amppi_ctx* ctx, amppi_plan_result* out);
 int32_t amppi_shard_partials_stride(const amppi_ctx* ctx);
 
+/* GPU-resident closed loop (execute_cycle, ensemble.cpp:245-305; SURVEY.md
+ * §8f row 1): the reference's scenario family `scene_kind` (0 empty,
+ * 1 forest, 2 verticals, 3 inclines, 4 two_gap; generate_scenario seed
+ * `scene_seed`), its LiDAR and PointCloudBuffer ring (`buffer_capacity`
+ * frames) and the vehicle at 1/replan_hz all stay on the device; every cycle
+ * is scan -> build_snapshot -> plan_step -> vehicle step with no host
+ * traffic.  Episode parameters are the reference's defaults (goal radius 1 m,
+ * timeout 60 s, drone radius 0.2 m, 50 consecutive planner failures).  The
+ * loop drives the context's planner (configuration and stream). */
+typedef struct amppi_loop amppi_loop;
+typedef struct {
+  uint64_t cycle;
+  int32_t planned;             /* 0: "planning failed" (hover applied) */
+  int32_t winner;              /* -1 when not planned */
+  double x[10];                /* state the plan saw: p, q (w x y z), v */
+  double control[4];           /* applied control */
+  double stage2;               /* winner's stage-II cost */
+  int32_t status;              /* after the cycle: 0 running, 1 success, 2 collision, 3 timeout, 4 planner failure */
+  int32_t n_points;            /* points in the buffer the plan saw */
+} amppi_loop_record;
+
+int amppi_loop_create(amppi_ctx* ctx, int32_t scene_kind, uint64_t scene_seed, uint64_t seed,
+                      int32_t buffer_capacity, int64_t max_cycles, amppi_loop** out);
+/* Runs up to `cycles` cycles (fewer once the episode ends); *ran = cycles executed. */
+int amppi_loop_run(amppi_loop* loop, int64_t cycles, int64_t* ran);
+int amppi_loop_records(amppi_loop* loop, amppi_loop_record* out, int64_t cap, int64_t* count);
+int amppi_loop_state(amppi_loop* loop, double* x10, int32_t* status, double* t);
+int amppi_loop_destroy(amppi_loop* loop);
+
 /* Profiling: per-kernel device time accumulated since the last reset
  * (requires opt.profile = 1).  names/ms/launches are caller arrays of cap. */
 int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches,

@@ -7,6 +7,7 @@ the reference planner's interface.  See DESIGN.md.
 from .planner import (  # noqa: F401
     Anchor,
     AnchorGrid,
+    ClosedLoop,
     AmppiError,
     CollisionParams,
     ControlInput,

@@ -109,6 +109,12 @@ class BatchOutput(ctypes.Structure):
     ]
 
 
+class LoopRecord(ctypes.Structure):
+    _fields_ = [("cycle", ctypes.c_uint64), ("planned", ctypes.c_int32), ("winner", ctypes.c_int32),
+                ("x", ctypes.c_double * 10), ("control", ctypes.c_double * 4), ("stage2", ctypes.c_double),
+                ("status", ctypes.c_int32), ("n_points", ctypes.c_int32)]
+
+
 EXPORTS = {
     "amppi_config_default": (None, [ctypes.POINTER(Config)]),
     "amppi_options_default": (None, [ctypes.POINTER(Options)]),
@@ -141,6 +147,12 @@ EXPORTS = {
     "amppi_shard_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32]),
     "amppi_shard_finish": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PlanResult)]),
     "amppi_shard_partials_stride": (ctypes.c_int32, [ctypes.c_void_p]),
+    "amppi_loop_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "amppi_loop_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_int64_p]),
+    "amppi_loop_records": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(LoopRecord), ctypes.c_int64, c_int64_p]),
+    "amppi_loop_state": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_int32_p, c_double_p]),
+    "amppi_loop_destroy": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 _lib = None

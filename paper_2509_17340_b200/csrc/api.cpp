@@ -18,6 +18,7 @@
 #include "../../include/amppi_b200.h"
 #include "kernels.h"
 #include "layout.h"
+#include "loop.h"
 
 using namespace amppi_dev;
 
@@ -1187,3 +1188,181 @@ static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, 
     CK(cudaMemcpyAsync(out->stage2, g.stage2, static_cast<size_t>(S) * M * sizeof(double), cudaMemcpyDeviceToHost, st));
   return sync_and_collect(ctx);
 }
+
+// ---------------------------------------------------------------------------
+// GPU-resident closed loop
+// ---------------------------------------------------------------------------
+struct amppi_loop {
+  amppi_ctx* ctx{nullptr};
+  amppi_dev::LoopDev L{};
+  amppi_dev::LoopParams prm{};
+  void* mem{nullptr};
+  int64_t max_cycles{0};
+};
+
+static_assert(sizeof(amppi_loop_record) == sizeof(amppi_dev::LoopRecord), "record layout");
+
+extern "C" {
+
+int amppi_loop_create(amppi_ctx* ctx, int32_t scene_kind, uint64_t scene_seed, uint64_t seed,
+                      int32_t buffer_capacity, int64_t max_cycles, amppi_loop** out) {
+  using namespace amppi_dev;
+  if (!ctx || !out) return AMPPI_INVALID_ARGUMENT;
+  if (buffer_capacity < 1 || max_cycles < 1) return ctx->fail(AMPPI_INVALID_ARGUMENT, "bad loop size");
+  std::vector<LoopPrim> prims;
+  try {
+    prims = loop_scenario(scene_kind, scene_seed);
+  } catch (const std::exception& e) {
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, e.what());
+  }
+  if (prims.size() > 1024) return ctx->fail(AMPPI_INVALID_ARGUMENT, "more than 1024 obstacles");
+  const int64_t cloud_cap = static_cast<int64_t>(buffer_capacity) * kLidarRays;
+  if (int rc = alloc_points(ctx, cloud_cap); rc != AMPPI_OK) return rc;
+  const int N = ctx->dc.N;
+  auto* lp = new (std::nothrow) amppi_loop();
+  if (!lp) return ctx->fail(AMPPI_CUDA_ERROR, "out of host memory");
+  lp->ctx = ctx;
+  lp->max_cycles = max_cycles;
+  // one device block: prims | state | frames | frame_n | cloud | offsets | goal | nominal | hover | cycles | seeds | records
+  auto align = [](size_t v) { return (v + 255) & ~size_t(255); };
+  const size_t sizes[] = {std::max<size_t>(prims.size(), 1) * sizeof(LoopPrim), sizeof(LoopState),
+                          static_cast<size_t>(cloud_cap) * 3 * sizeof(double), buffer_capacity * sizeof(int32_t),
+                          static_cast<size_t>(cloud_cap) * 3 * sizeof(double), 2 * sizeof(int64_t),
+                          10 * sizeof(double), static_cast<size_t>(N) * 4 * sizeof(double), 4 * sizeof(double),
+                          sizeof(uint64_t), sizeof(uint64_t), static_cast<size_t>(max_cycles) * sizeof(LoopRecord)};
+  size_t total = 0;
+  for (size_t s : sizes) total += align(s);
+  if (cudaMalloc(&lp->mem, total) != cudaSuccess) {
+    delete lp;
+    return ctx->fail(AMPPI_CUDA_ERROR, "loop allocation");
+  }
+  unsigned char* cur = static_cast<unsigned char*>(lp->mem);
+  auto take = [&](size_t s) {
+    void* p = cur;
+    cur += align(s);
+    return p;
+  };
+  LoopDev& L = lp->L;
+  L.prims = static_cast<const LoopPrim*>(take(sizes[0]));
+  L.st = static_cast<LoopState*>(take(sizes[1]));
+  L.frames = static_cast<double*>(take(sizes[2]));
+  L.frame_n = static_cast<int32_t*>(take(sizes[3]));
+  L.cloud = static_cast<double*>(take(sizes[4]));
+  L.offsets = static_cast<int64_t*>(take(sizes[5]));
+  L.goal = static_cast<double*>(take(sizes[6]));
+  L.nominal = static_cast<double*>(take(sizes[7]));
+  L.hover = static_cast<double*>(take(sizes[8]));
+  L.cycles = static_cast<uint64_t*>(take(sizes[9]));
+  L.seeds = static_cast<uint64_t*>(take(sizes[10]));
+  L.records = static_cast<LoopRecord*>(take(sizes[11]));
+  L.max_records = max_cycles;
+  // initial episode (make_episode_state, ensemble.cpp:238-243): start (0, 0, 2) at rest,
+  // last applied = hover, goal = GoalSpec::facing(start, goal (45, 0, 2))
+  const amppi_config& c = ctx->cfg;
+  const double g = std::sqrt((c.gravity[0] * c.gravity[0] + c.gravity[1] * c.gravity[1]) + c.gravity[2] * c.gravity[2]);
+  const double hover[4] = {c.mass * g, 0.0, 0.0, 0.0};
+  LoopState st{};
+  st.x[0] = 0.0; st.x[1] = 0.0; st.x[2] = 2.0;
+  st.x[3] = 1.0;
+  for (int k = 0; k < 4; ++k) st.last[k] = hover[k];
+  st.ring_head = buffer_capacity - 1;
+  const double sx = 0.0, sy = 0.0, gxp = 45.0, gyp = 0.0;
+  const double yaw = std::atan2(gyp - sy, gxp - sx), hy = 0.5 * yaw;
+  const double goal[10] = {45.0, 0.0, 2.0, 0.0, 0.0, 0.0, std::cos(hy), 0.0, 0.0, std::sin(hy)};
+  CK(cudaMemcpy(const_cast<LoopPrim*>(L.prims), prims.data(), prims.size() * sizeof(LoopPrim), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(L.st, &st, sizeof(st), cudaMemcpyHostToDevice));
+  CK(cudaMemset(L.frame_n, 0, sizes[3]));
+  CK(cudaMemcpy(L.goal, goal, sizeof(goal), cudaMemcpyHostToDevice));
+  CK(cudaMemset(L.nominal, 0, sizes[7]));
+  CK(cudaMemcpy(L.hover, hover, sizeof(hover), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(L.seeds, &seed, sizeof(seed), cudaMemcpyHostToDevice));
+  LoopParams& prm = lp->prm;
+  prm.n_prims = static_cast<int>(prims.size());
+  prm.capacity = buffer_capacity;
+  prm.seed = seed;
+  prm.r_max = c.r_max;
+  prm.el_min = -45.0 * std::numbers::pi / 180.0;
+  prm.el_max = 45.0 * std::numbers::pi / 180.0;
+  prm.range_sigma = 0.01;
+  prm.goal_radius = 1.0;
+  prm.timeout = 60.0;
+  prm.drone_radius = 0.2;
+  prm.max_failures = 50;
+  prm.step_dt = 1.0 / c.replan_hz;
+  *out = lp;
+  return AMPPI_OK;
+}
+
+int amppi_loop_run(amppi_loop* lp, int64_t cycles, int64_t* ran) {
+  using namespace amppi_dev;
+  if (!lp) return AMPPI_INVALID_ARGUMENT;
+  amppi_ctx* ctx = lp->ctx;
+  const LoopDev& L = lp->L;
+  uint64_t c0 = 0;
+  CK(cudaMemcpyAsync(&c0, &L.st->cycle, sizeof(c0), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int64_t room = lp->max_cycles - static_cast<int64_t>(c0);
+  if (cycles > room) cycles = std::max<int64_t>(room, 0);
+  BatchIn in{};
+  in.xyz = nullptr;
+  in.xyz64 = L.cloud;
+  in.offsets = L.offsets;
+  in.poses = L.st->x;
+  in.states = L.st->x;
+  in.goals = L.goal;
+  in.prev = L.nominal;
+  in.prev_len = &L.st->prev_len;
+  in.last_applied = L.st->last;
+  in.cycles = L.cycles;
+  in.seeds = L.seeds;
+  in.injected = nullptr;
+  in.S = 1;
+  in.r_max = ctx->cfg.r_max;
+  const int64_t max_pts = static_cast<int64_t>(lp->prm.capacity) * kLidarRays;
+  for (int64_t i = 0; i < cycles; ++i) {
+    cudaError_t e = launch_loop_scan(L, lp->prm, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_loop_scan");
+    if (int rc = run_cycle(ctx, in, max_pts, true, true, false); rc != AMPPI_OK) return rc;
+    e = launch_loop_step(L, lp->prm, ctx->pl, ctx->dc, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_loop_step");
+  }
+  uint64_t c1 = 0;
+  CK(cudaMemcpyAsync(&c1, &L.st->cycle, sizeof(c1), cudaMemcpyDeviceToHost, ctx->stream));
+  if (int rc = sync_and_collect(ctx); rc != AMPPI_OK) return rc;
+  if (ran) *ran = static_cast<int64_t>(c1 - c0);
+  return AMPPI_OK;
+}
+
+int amppi_loop_records(amppi_loop* lp, amppi_loop_record* out, int64_t cap, int64_t* count) {
+  if (!lp) return AMPPI_INVALID_ARGUMENT;
+  amppi_ctx* ctx = lp->ctx;
+  uint64_t c = 0;
+  CK(cudaMemcpy(&c, &lp->L.st->cycle, sizeof(c), cudaMemcpyDeviceToHost));
+  const int64_t n = std::min<int64_t>(static_cast<int64_t>(c), lp->max_cycles);
+  if (count) *count = n;
+  if (out && cap > 0)
+    CK(cudaMemcpy(out, lp->L.records, static_cast<size_t>(std::min(n, cap)) * sizeof(amppi_loop_record),
+                  cudaMemcpyDeviceToHost));
+  return AMPPI_OK;
+}
+
+int amppi_loop_state(amppi_loop* lp, double* x10, int32_t* status, double* t) {
+  if (!lp) return AMPPI_INVALID_ARGUMENT;
+  amppi_ctx* ctx = lp->ctx;
+  amppi_dev::LoopState st{};
+  CK(cudaMemcpy(&st, lp->L.st, sizeof(st), cudaMemcpyDeviceToHost));
+  if (x10) std::memcpy(x10, st.x, sizeof(st.x));
+  if (status) *status = st.status;
+  if (t) *t = st.t;
+  return AMPPI_OK;
+}
+
+int amppi_loop_destroy(amppi_loop* lp) {
+  if (!lp) return AMPPI_OK;
+  cudaStreamSynchronize(lp->ctx->stream);
+  cudaFree(lp->mem);
+  delete lp;
+  return AMPPI_OK;
+}
+
+}  // extern "C"

@@ -581,3 +581,54 @@ class Planner:
 
     def kernel_times_reset(self) -> None:
         self._check(self.lib.amppi_kernel_times_reset(self._h))
+
+
+class ClosedLoop:
+    """GPU-resident closed loop (amppi_loop_*): execute_cycle
+    (ensemble.cpp:245-305) with the LiDAR, the point-cloud ring and the vehicle
+    on the device.  Uses the planner's configuration and stream."""
+
+    STATUS = {0: "running", 1: "success", 2: "collision", 3: "timeout", 4: "planner_failure"}
+
+    def __init__(self, planner: Planner, scene_kind: int, scene_seed: int, seed: int, buffer_capacity: int = 10,
+                 max_cycles: int = 4096):
+        self.planner = planner
+        self.lib = planner.lib
+        h = ctypes.c_void_p()
+        planner._check(self.lib.amppi_loop_create(planner._h, scene_kind, ctypes.c_uint64(scene_seed),
+                                                  ctypes.c_uint64(seed), buffer_capacity, max_cycles,
+                                                  ctypes.byref(h)))
+        self._h = h
+
+    def run(self, cycles: int) -> int:
+        ran = ctypes.c_int64()
+        self.planner._check(self.lib.amppi_loop_run(self._h, cycles, ctypes.byref(ran)))
+        return int(ran.value)
+
+    def records(self) -> list:
+        n = ctypes.c_int64()
+        self.planner._check(self.lib.amppi_loop_records(self._h, None, 0, ctypes.byref(n)))
+        buf = (_abi.LoopRecord * max(int(n.value), 1))()
+        self.planner._check(self.lib.amppi_loop_records(self._h, buf, int(n.value), ctypes.byref(n)))
+        return [dict(cycle=int(r.cycle), planned=bool(r.planned), winner=int(r.winner), x=np.array(r.x[:]),
+                     control=np.array(r.control[:]), stage2=float(r.stage2), status=int(r.status),
+                     n_points=int(r.n_points)) for r in buf[: int(n.value)]]
+
+    def state(self):
+        x = np.zeros(10)
+        st = ctypes.c_int32()
+        t = ctypes.c_double()
+        self.planner._check(self.lib.amppi_loop_state(self._h, _ptr(x, ctypes.c_double), ctypes.byref(st),
+                                                      ctypes.byref(t)))
+        return x, self.STATUS.get(int(st.value), str(st.value)), float(t.value)
+
+    def close(self) -> None:
+        if self._h:
+            self.lib.amppi_loop_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
