@@ -41,9 +41,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c4"],
+    ap.add_argument("--workload", default="c5", choices=["c5", "c4", "c2"],
                     help="c5: batched scenes (default, the driver's line); c4: 64x8192x50 ensemble, samples "
-                         "sharded over the ranks with NCCL")
+                         "sharded over the ranks with NCCL; c2: 200-cycle closed loop on the device")
     ap.add_argument("--scenes", type=int, default=4096)
     ap.add_argument("--points", type=int, default=20000)
     ap.add_argument("--latency-cycles", type=int, default=1000)
@@ -517,10 +517,79 @@ def run_c4(args):
         dist.destroy_process_group()
 
 
+def run_c2(args):
+    """Config C2: the 200-cycle closed-loop forest flight (speed cap 7 m/s,
+    4x2 anchors x 256 x 30) run entirely on the device (amppi_loop_*: LiDAR,
+    point-cloud ring, snapshot, plan, vehicle step); one step = one episode of
+    200 cycles.  value = rollout-steps/s of the planning inside the loop;
+    cpu_baseline = the oracle's execute_cycle loop on the host cores."""
+    import torch
+
+    from paper_2509_17340_b200 import ClosedLoop, Planner
+    from paper_2509_17340_b200.planner import apply_velocity_cap
+    from paper_2509_17340_b200.workloads import plan_config, rollout_steps
+
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    cfg = apply_velocity_cap(plan_config(), 7.0)
+    cycles = 200
+    planner = Planner(cfg, device=local, precision=32, max_points=10 * 7200)
+
+    def episode(i):
+        lp = ClosedLoop(planner, 1, 1, 31 + i, buffer_capacity=10, max_cycles=cycles)
+        t0 = time.perf_counter()
+        ran = lp.run(cycles)
+        dt = time.perf_counter() - t0
+        lp.close()
+        return ran, dt
+
+    for i in range(args.warmup):
+        episode(i)
+    sampler = ClockSampler(local)
+    sampler.start()
+    total_cycles, total_t = 0, 0.0
+    for i in range(args.steps):
+        ran, dt = episode(args.warmup + i)
+        total_cycles += ran
+        total_t += dt
+    clocks = sampler.stop()
+    planner.close()
+    ms_cycle = 1e3 * total_t / max(total_cycles, 1)
+    value = rollout_steps(cfg, 1) * total_cycles / total_t
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_py import Oracle
+
+    orc = Oracle()
+    orc.set_workers(os.cpu_count() or 1)
+    lo = orc.loop(1, 1, orc.config(cfg), 31, capacity=10)
+    t0 = time.perf_counter()
+    n_cpu = lo.run(50)
+    t_cpu = time.perf_counter() - t0
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "rollout-steps/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True,
+        "scaling": "replicas", "vs_baseline": None, "dtype": "f32 screening / f64 plan, LiDAR and vehicle",
+        "data": "synthetic",
+        "config": {"workload": "C2: 200-cycle closed-loop forest flight (seed 1), speed cap 7 m/s, 4x2 anchors x 256 "
+                               "x 30, LiDAR + point-cloud ring + snapshot + plan + vehicle step on the device "
+                               "(amppi_loop_run, one CUDA graph per cycle); one step = one episode",
+                   "cycles_per_episode": cycles, "ms_per_cycle": ms_cycle},
+        "cpu_baseline": {"value": rollout_steps(cfg, 1) * n_cpu / t_cpu, "unit": "rollout-steps/s",
+                         "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{n_cpu} cycles of the oracle's execute_cycle loop ({1e3 * t_cpu / n_cpu:.2f} "
+                                   f"ms/cycle)"},
+        "clocks": clocks,
+    }), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "b200" and args.workload == "c4":
         run_c4(args)
+    elif args.impl == "b200" and args.workload == "c2":
+        run_c2(args)
     elif args.impl == "reference":
         run_reference(args)
     else:

@@ -1198,6 +1198,7 @@ struct amppi_loop {
   amppi_dev::LoopParams prm{};
   void* mem{nullptr};
   int64_t max_cycles{0};
+  cudaGraphExec_t cycle_graph{nullptr};  // one captured cycle, replayed (all state lives on the device)
 };
 
 static_assert(sizeof(amppi_loop_record) == sizeof(amppi_dev::LoopRecord), "record layout");
@@ -1319,12 +1320,34 @@ int amppi_loop_run(amppi_loop* lp, int64_t cycles, int64_t* ran) {
   in.S = 1;
   in.r_max = ctx->cfg.r_max;
   const int64_t max_pts = static_cast<int64_t>(lp->prm.capacity) * kLidarRays;
-  for (int64_t i = 0; i < cycles; ++i) {
+  auto one_cycle = [&]() -> int {
     cudaError_t e = launch_loop_scan(L, lp->prm, ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_loop_scan");
     if (int rc = run_cycle(ctx, in, max_pts, true, true, false); rc != AMPPI_OK) return rc;
     e = launch_loop_step(L, lp->prm, ctx->pl, ctx->dc, ctx->stream);
-    if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_loop_step");
+    return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "launch_loop_step");
+  };
+  // Every cycle launches the same kernels on device-resident state, so one
+  // captured cycle is replayed as a CUDA graph (no per-kernel launch cost);
+  // with per-kernel profiling on, the cycles are launched individually.
+  const bool graph = !ctx->timer.enabled && std::getenv("AMPPI_LOOP_NO_GRAPH") == nullptr;
+  if (graph && !lp->cycle_graph && cycles > 0) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = one_cycle();
+    const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc != AMPPI_OK) return rc;
+    if (ce != cudaSuccess) return ctx->cuda_fail(ce, "graph capture");
+    const cudaError_t ie = cudaGraphInstantiate(&lp->cycle_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return ctx->cuda_fail(ie, "graph instantiate");
+  }
+  for (int64_t i = 0; i < cycles; ++i) {
+    if (graph) {
+      CK(cudaGraphLaunch(lp->cycle_graph, ctx->stream));
+    } else if (int rc = one_cycle(); rc != AMPPI_OK) {
+      return rc;
+    }
   }
   uint64_t c1 = 0;
   CK(cudaMemcpyAsync(&c1, &L.st->cycle, sizeof(c1), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1360,6 +1383,7 @@ int amppi_loop_state(amppi_loop* lp, double* x10, int32_t* status, double* t) {
 int amppi_loop_destroy(amppi_loop* lp) {
   if (!lp) return AMPPI_OK;
   cudaStreamSynchronize(lp->ctx->stream);
+  if (lp->cycle_graph) cudaGraphExecDestroy(lp->cycle_graph);
   cudaFree(lp->mem);
   delete lp;
   return AMPPI_OK;
