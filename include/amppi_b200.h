@@ -236,7 +236,18 @@ typedef struct {
   double stage2;               /* winner's stage-II cost */
   int32_t status;              /* after the cycle: 0 running, 1 success, 2 collision, 3 timeout, 4 planner failure */
   int32_t n_points;            /* points in the buffer the plan saw */
+  /* TrajectoryLog LogRecord (ensemble.hpp:84-94): after the vehicle step */
+  double t;                    /* episode time */
+  double x_after[10];          /* p, q (w x y z), v */
+  double clearance;            /* true clearance of the new position */
+  double breakdown[5];         /* winner's cost breakdown (zeros when not planned) */
 } amppi_loop_record;
+
+/* EpisodeMetrics (metrics.hpp:11-18) from the device log (compute_metrics,
+ * metrics.cpp:12-49); needs >= 4 cycles. */
+typedef struct {
+  double avg_vel, max_vel, smoothness, path_length, avg_clearance, min_clearance;
+} amppi_episode_metrics;
 
 int amppi_loop_create(amppi_ctx* ctx, int32_t scene_kind, uint64_t scene_seed, uint64_t seed,
                       int32_t buffer_capacity, int64_t max_cycles, amppi_loop** out);
@@ -244,6 +255,7 @@ int amppi_loop_create(amppi_ctx* ctx, int32_t scene_kind, uint64_t scene_seed, u
 int amppi_loop_run(amppi_loop* loop, int64_t cycles, int64_t* ran);
 int amppi_loop_records(amppi_loop* loop, amppi_loop_record* out, int64_t cap, int64_t* count);
 int amppi_loop_state(amppi_loop* loop, double* x10, int32_t* status, double* t);
+int amppi_loop_metrics(amppi_loop* loop, amppi_episode_metrics* out);
 int amppi_loop_destroy(amppi_loop* loop);
 
 /* Profiling: per-kernel device time accumulated since the last reset

@@ -112,7 +112,13 @@ class BatchOutput(ctypes.Structure):
 class LoopRecord(ctypes.Structure):
     _fields_ = [("cycle", ctypes.c_uint64), ("planned", ctypes.c_int32), ("winner", ctypes.c_int32),
                 ("x", ctypes.c_double * 10), ("control", ctypes.c_double * 4), ("stage2", ctypes.c_double),
-                ("status", ctypes.c_int32), ("n_points", ctypes.c_int32)]
+                ("status", ctypes.c_int32), ("n_points", ctypes.c_int32), ("t", ctypes.c_double),
+                ("x_after", ctypes.c_double * 10), ("clearance", ctypes.c_double), ("breakdown", ctypes.c_double * 5)]
+
+
+class EpisodeMetrics(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in
+                ("avg_vel", "max_vel", "smoothness", "path_length", "avg_clearance", "min_clearance")]
 
 
 EXPORTS = {
@@ -153,6 +159,7 @@ EXPORTS = {
     "amppi_loop_records": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(LoopRecord), ctypes.c_int64, c_int64_p]),
     "amppi_loop_state": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_int32_p, c_double_p]),
     "amppi_loop_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "amppi_loop_metrics": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(EpisodeMetrics)]),
 }
 
 _lib = None

@@ -1202,6 +1202,7 @@ struct amppi_loop {
 };
 
 static_assert(sizeof(amppi_loop_record) == sizeof(amppi_dev::LoopRecord), "record layout");
+static_assert(sizeof(amppi_episode_metrics) == sizeof(amppi_dev::LoopMetrics), "metrics layout");
 
 extern "C" {
 
@@ -1378,6 +1379,22 @@ int amppi_loop_state(amppi_loop* lp, double* x10, int32_t* status, double* t) {
   if (status) *status = st.status;
   if (t) *t = st.t;
   return AMPPI_OK;
+}
+
+int amppi_loop_metrics(amppi_loop* lp, amppi_episode_metrics* out) {
+  if (!lp || !out) return AMPPI_INVALID_ARGUMENT;
+  amppi_ctx* ctx = lp->ctx;
+  uint64_t c = 0;
+  CK(cudaMemcpy(&c, &lp->L.st->cycle, sizeof(c), cudaMemcpyDeviceToHost));
+  const int64_t n = std::min<int64_t>(static_cast<int64_t>(c), lp->max_cycles);
+  if (n < 4) return ctx->fail(AMPPI_INVALID_ARGUMENT, "log too short for jerk estimation");
+  void* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(amppi_dev::LoopMetrics)));
+  cudaError_t e = amppi_dev::launch_loop_metrics(lp->L, n, static_cast<amppi_dev::LoopMetrics*>(d), ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, sizeof(*out), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d);
+  return e == cudaSuccess ? AMPPI_OK : ctx->cuda_fail(e, "loop metrics");
 }
 
 int amppi_loop_destroy(amppi_loop* lp) {

@@ -372,8 +372,49 @@ __global__ void __launch_bounds__(256) k_loop_step(LoopDev L, LoopParams prm, Pl
       status = 3;  // timeout
     }
     st->status = status;
-    if (static_cast<int64_t>(rc) < L.max_records) L.records[rc].status = status;
+    if (static_cast<int64_t>(rc) < L.max_records) {
+      LoopRecord& r = L.records[rc];
+      r.status = status;
+      r.t = st->t;
+      for (int i = 0; i < 10; ++i) r.x_after[i] = s_x[i];
+      r.clearance = clearance;
+      for (int i = 0; i < 5; ++i) r.breakdown[i] = planned ? pl.breakdown[static_cast<int64_t>(winner) * 5 + i] : 0.0;
+    }
   }
+}
+
+// compute_metrics (metrics.cpp:12-49) on the device log, in the reference's
+// summation order (one thread; a log is a few thousand records).
+__global__ void k_loop_metrics(LoopDev L, int64_t n, LoopMetrics* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const LoopRecord* rec = L.records;
+  auto vel = [&](int64_t i) { return V{rec[i].x_after[7], rec[i].x_after[8], rec[i].x_after[9]}; };
+  auto pos = [&](int64_t i) { return V{rec[i].x_after[0], rec[i].x_after[1], rec[i].x_after[2]}; };
+  auto norm = [](V a) { return sqrt((a.x * a.x + a.y * a.y) + a.z * a.z); };
+  const double dt = rec[1].t - rec[0].t;
+  LoopMetrics m{0.0, 0.0, 0.0, 0.0, 0.0, __longlong_as_double(0x7ff0000000000000ll)};
+  double speed_sum = 0.0, clearance_sum = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double speed = norm(vel(i));
+    speed_sum += speed;
+    m.max_vel = fmax(m.max_vel, speed);
+    if (i + 1 < n) m.path_length += norm(vsub(pos(i + 1), pos(i)));
+    const double c = rec[i].clearance;
+    clearance_sum += c;
+    m.min_clearance = fmin(m.min_clearance, c);
+  }
+  m.avg_vel = speed_sum / static_cast<double>(n);
+  m.avg_clearance = clearance_sum / static_cast<double>(n);
+  auto second_diff = [&](int64_t a, int64_t b, int64_t c) {  // (v_c - 2 v_b + v_a) / dt^2
+    const V va = vel(a), vb = vel(b), vc = vel(c);
+    const double d2 = dt * dt;
+    return V{((vc.x - 2.0 * vb.x) + va.x) / d2, ((vc.y - 2.0 * vb.y) + va.y) / d2, ((vc.z - 2.0 * vb.z) + va.z) / d2};
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    const V j = i == 0 ? second_diff(0, 1, 2) : (i == n - 1 ? second_diff(n - 3, n - 2, n - 1) : second_diff(i - 1, i, i + 1));
+    m.smoothness += ((j.x * j.x + j.y * j.y) + j.z * j.z) * dt;
+  }
+  *out = m;
 }
 
 }  // namespace
@@ -387,6 +428,11 @@ cudaError_t launch_loop_scan(const LoopDev& L, const LoopParams& prm, cudaStream
 cudaError_t launch_loop_step(const LoopDev& L, const LoopParams& prm, const Plan& pl, const DevConfig& cfg,
                              cudaStream_t st) {
   k_loop_step<<<1, 256, 0, st>>>(L, prm, pl, cfg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loop_metrics(const LoopDev& L, int64_t n, LoopMetrics* out, cudaStream_t st) {
+  k_loop_metrics<<<1, 32, 0, st>>>(L, n, out);
   return cudaGetLastError();
 }
 

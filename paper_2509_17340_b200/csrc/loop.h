@@ -55,6 +55,16 @@ struct LoopRecord {
   double stage2;        // winner's stage-II cost
   int32_t status;       // episode status after this cycle
   int32_t n_points;     // points in the buffer the plan saw
+  // TrajectoryLog LogRecord (ensemble.hpp:84-94, ensemble.cpp:280-290): after the step
+  double t;             // episode time
+  double x_after[10];   // p, q, v after the vehicle step
+  double clearance;     // true_clearance of the new position
+  double breakdown[5];  // winner's cost breakdown (zeros when not planned)
+};
+
+// EpisodeMetrics (metrics.hpp:11-18), same layout as amppi_episode_metrics.
+struct LoopMetrics {
+  double avg_vel, max_vel, smoothness, path_length, avg_clearance, min_clearance;
 };
 
 struct LoopParams {
@@ -90,5 +100,7 @@ std::vector<LoopPrim> loop_scenario(int kind, uint64_t seed);  // generate_scena
 cudaError_t launch_loop_scan(const LoopDev& L, const LoopParams& prm, cudaStream_t st);
 cudaError_t launch_loop_step(const LoopDev& L, const LoopParams& prm, const Plan& pl, const DevConfig& cfg,
                              cudaStream_t st);
+// compute_metrics (metrics.cpp:12-49) over records [0, n); n >= 4.
+cudaError_t launch_loop_metrics(const LoopDev& L, int64_t n, LoopMetrics* out, cudaStream_t st);
 
 }  // namespace amppi_dev

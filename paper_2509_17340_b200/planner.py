@@ -612,7 +612,29 @@ class ClosedLoop:
         self.planner._check(self.lib.amppi_loop_records(self._h, buf, int(n.value), ctypes.byref(n)))
         return [dict(cycle=int(r.cycle), planned=bool(r.planned), winner=int(r.winner), x=np.array(r.x[:]),
                      control=np.array(r.control[:]), stage2=float(r.stage2), status=int(r.status),
-                     n_points=int(r.n_points)) for r in buf[: int(n.value)]]
+                     n_points=int(r.n_points), t=float(r.t), x_after=np.array(r.x_after[:]),
+                     clearance=float(r.clearance), breakdown=np.array(r.breakdown[:]))
+                for r in buf[: int(n.value)]]
+
+    def metrics(self) -> dict:
+        """EpisodeMetrics (metrics.hpp:11-18) computed on the device log."""
+        m = _abi.EpisodeMetrics()
+        self.planner._check(self.lib.amppi_loop_metrics(self._h, ctypes.byref(m)))
+        return {k: float(getattr(m, k)) for k, _ in _abi.EpisodeMetrics._fields_}
+
+    def trajectory_csv(self) -> str:
+        """The episode as the reference's TrajectoryLog CSV (# amppi-trajectory v1,
+        %.17g; ensemble.cpp:192-230)."""
+        lines = ["# amppi-trajectory v1",
+                 "t,px,py,pz,vx,vy,vz,qw,qx,qy,qz,thrust,wx,wy,wz,winner,stage2,"
+                 "clearance,j_track,j_vnorm,j_ctrl,j_goal,j_col"]
+        for r in self.records():
+            x = r["x_after"]
+            vals = [r["t"], x[0], x[1], x[2], x[7], x[8], x[9], x[3], x[4], x[5], x[6], *r["control"]]
+            row = ",".join("%.17g" % v for v in vals) + ",%d," % r["winner"]
+            row += ",".join("%.17g" % v for v in [r["stage2"], r["clearance"], *r["breakdown"]])
+            lines.append(row)
+        return "\n".join(lines) + "\n"
 
     def state(self):
         x = np.zeros(10)

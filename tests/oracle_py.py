@@ -230,6 +230,11 @@ class OracleLoop:
     def status(self) -> int:
         return self.o.L.oracle_loop_status(self.h)
 
+    def state(self) -> np.ndarray:
+        x = np.zeros(10)
+        self.o.L.oracle_loop_state(self.h, _p(x))
+        return x
+
     def goal(self):
         gp, gv, gq = np.zeros(3), np.zeros(3), np.zeros(4)
         self.o.L.oracle_loop_goal(self.h, _p(gp), _p(gv), _p(gq))

@@ -96,3 +96,59 @@ def test_device_bookkeeping(loops):
     for g in grecs:
         if not g["planned"]:
             assert np.allclose(g["control"], [cfg.dynamics.hover().thrust, 0, 0, 0])
+
+
+def _reference_metrics(log):
+    """compute_metrics (metrics.cpp:12-49) restated over (t, p, v, clearance)."""
+    n = len(log)
+    dt = log[1][0] - log[0][0]
+    speed_sum = clear_sum = path = smooth = max_vel = 0.0
+    min_clear = float("inf")
+    for i, (t, p, v, c) in enumerate(log):
+        speed = float(np.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]))
+        speed_sum += speed
+        max_vel = max(max_vel, speed)
+        if i + 1 < n:
+            d = log[i + 1][1] - p
+            path += float(np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]))
+        clear_sum += c
+        min_clear = min(min_clear, c)
+
+    def sd(a, b, c):
+        return ((log[c][2] - 2.0 * log[b][2]) + log[a][2]) / (dt * dt)
+
+    for i in range(n):
+        j = sd(0, 1, 2) if i == 0 else (sd(n - 3, n - 2, n - 1) if i == n - 1 else sd(i - 1, i, i + 1))
+        smooth += float((j[0] * j[0] + j[1] * j[1]) + j[2] * j[2]) * dt
+    return dict(avg_vel=speed_sum / n, max_vel=max_vel, smoothness=smooth, path_length=path,
+                avg_clearance=clear_sum / n, min_clearance=min_clear)
+
+
+def test_trajectory_log_and_metrics(oracle, loops):
+    """The device TrajectoryLog (post-step state, clearance, time) and the
+    EpisodeMetrics computed from it on the device match the reference's,
+    rebuilt from the oracle loop (next cycle's state, oracle true_clearance)."""
+    cfg, orecs, grecs, ran, loop = loops
+    scene = oracle.scene(1, 1)
+    dt = 1.0 / cfg.replan_hz
+    ref, t = [], 0.0
+    for i in range(len(orecs) - 1):
+        t = t + dt
+        x = orecs[i + 1]["x"]
+        ref.append((t, x[0:3].copy(), x[7:10].copy(), scene.true_clearance(x[0:3])))
+    for g, (t, p, v, c) in zip(grecs, ref):
+        assert abs(g["t"] - t) <= 1e-12
+        assert np.max(np.abs(g["x_after"][0:3] - p)) <= 1e-9
+        assert np.max(np.abs(g["x_after"][7:10] - v)) <= 1e-9
+        assert abs(g["clearance"] - c) <= 1e-9
+    dev = _reference_metrics([(g["t"], g["x_after"][0:3], g["x_after"][7:10], g["clearance"]) for g in grecs])
+    got = loop.metrics()
+    for k, v in dev.items():  # the device reduction equals its restatement on the device log
+        assert abs(got[k] - v) <= 1e-12 * max(1.0, abs(v)), k
+    want = _reference_metrics(ref)  # and the reference's on the oracle log (one cycle shorter)
+    mine = _reference_metrics([(g["t"], g["x_after"][0:3], g["x_after"][7:10], g["clearance"])
+                               for g in grecs[: len(ref)]])
+    for k, v in want.items():
+        assert abs(mine[k] - v) <= 1e-8 * max(1.0, abs(v)), k
+    csv = loop.trajectory_csv().splitlines()
+    assert csv[0] == "# amppi-trajectory v1" and len(csv) == len(grecs) + 2
