@@ -258,6 +258,20 @@ int amppi_loop_state(amppi_loop* loop, double* x10, int32_t* status, double* t);
 int amppi_loop_metrics(amppi_loop* loop, amppi_episode_metrics* out);
 int amppi_loop_destroy(amppi_loop* loop);
 
+/* Formats around the path (host only, no context).
+ * Cloud frames: the reference's text "# amppi-cloud v1" (io.cpp:24-66,
+ * %.17g: exact round trip) or "# amppi-cloud-bin v1" (u64 frame id, u64
+ * count, n x 3 float64).  amppi_cloud_read detects the format, writes up to
+ * `cap` points and always reports the frame's point count in *n_points.
+ * amppi_partition_csv / amppi_anchors_csv write the reference's debug dumps
+ * (io.cpp:68-99) from a snapshot's ranges [7200] (flat i*60+j) and a plan's
+ * refined anchors [M*3] + guide coefficients [M*18]. */
+int amppi_cloud_read(const char* path, double* xyz, int64_t cap, int64_t* n_points, uint64_t* frame_id);
+int amppi_cloud_write(const char* path, const double* xyz, int64_t n_points, uint64_t frame_id, int32_t binary);
+int amppi_partition_csv(const char* path, const double* ranges);
+int amppi_anchors_csv(const char* path, int32_t step, int32_t n_anchors, const double* refined,
+                      const double* guide_coeffs, double horizon, int32_t samples);
+
 /* Profiling: per-kernel device time accumulated since the last reset
  * (requires opt.profile = 1).  names/ms/launches are caller arrays of cap. */
 int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches,

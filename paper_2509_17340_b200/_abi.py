@@ -160,6 +160,12 @@ EXPORTS = {
     "amppi_loop_state": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_int32_p, c_double_p]),
     "amppi_loop_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "amppi_loop_metrics": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(EpisodeMetrics)]),
+    "amppi_cloud_read": (ctypes.c_int, [ctypes.c_char_p, c_double_p, ctypes.c_int64, c_int64_p, c_uint64_p]),
+    "amppi_cloud_write": (ctypes.c_int, [ctypes.c_char_p, c_double_p, ctypes.c_int64, ctypes.c_uint64,
+                                         ctypes.c_int32]),
+    "amppi_partition_csv": (ctypes.c_int, [ctypes.c_char_p, c_double_p]),
+    "amppi_anchors_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, c_double_p, c_double_p,
+                                         ctypes.c_double, ctypes.c_int32]),
 }
 
 _lib = None
