@@ -170,7 +170,10 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
       abortable = true;
     }
   }
-  const float d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, lim2, stop2, &env.hint);
+  // step 0 is x0 for every sample: its query was answered once per CTA
+  const float d2 = j == 0 ? env.d2_x0
+                          : nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, lim2, stop2,
+                                            &env.hint);
   if (abortable && d2 < stop2) return 1;
   s.col = s.col + collision_term(sqrtf(d2), env.cs, env.ca, env.cdmin, env.cdmax);
   if (((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col) >
@@ -190,17 +193,20 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
 constexpr int kScreenThreads = 128;
 constexpr int kStateWords = 21;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint
 
-template <int kMinBlocks, int kCompact>
-__global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
-    k_stage1_f32c(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter, int k1) {
+// Samples [k_lo + kb0, k_lo + kend) of every instance, aborted against the
+// minimum of samples [k_lo, k_lo + nb) (main pass: kb0 = nb = 32; bound
+// pass: kb0 = nb = 1, kend = 32).
+template <int kMinBlocks, int kCompact, int kT = kScreenThreads>
+__global__ void __launch_bounds__(kT, kMinBlocks)
+    k_stage1_f32c(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter, int kb0, int kend, int nb) {
   __shared__ float s_unom[4 * kMaxN];
   __shared__ float4 s_guide[kMaxN];
   __shared__ float s_bound;
-  __shared__ float s_state[kStateWords][kScreenThreads];
-  __shared__ int s_k[kScreenThreads];
-  __shared__ int s_wcount[2][kScreenThreads / 32];
-  const int k_n = cfg.k_hi - cfg.k_lo - k1;
-  const int tiles = (k_n + kScreenThreads - 1) / kScreenThreads;
+  __shared__ float s_state[kStateWords][kT];
+  __shared__ int s_k[kT];
+  __shared__ int s_wcount[2][kT / 32];
+  const int k_n = kend - kb0;
+  const int tiles = (k_n + kT - 1) / kT;
   int b = blockIdx.x;
   const int tile = b % tiles;
   b /= tiles;
@@ -211,15 +217,15 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* __restrict__ out = pl.cost32 + smi * cfg.K;
   if (!pl.alive[smi]) {
-    const int k = cfg.k_lo + k1 + tile * kScreenThreads + tid;
-    if (k < cfg.k_hi) out[k] = __int_as_float(0x7f800000);
+    const int k = cfg.k_lo + kb0 + tile * kT + tid;
+    if (k < cfg.k_lo + kend) out[k] = __int_as_float(0x7f800000);
     return;
   }
-  for (int i = tid; i < 4 * N; i += kScreenThreads) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
-  for (int i = tid; i < N; i += kScreenThreads) s_guide[i] = pl.guide32[smi * N + i];
+  for (int i = tid; i < 4 * N; i += kT) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
+  for (int i = tid; i < N; i += kT) s_guide[i] = pl.guide32[smi * N + i];
   if (tid < 32) {
     float u = __int_as_float(0x7f800000);
-    for (int k = cfg.k_lo + tid; k < cfg.k_lo + k1; k += 32) u = fminf(u, out[k]);
+    for (int k = cfg.k_lo + tid; k < cfg.k_lo + nb; k += 32) u = fminf(u, out[k]);
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (tid == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
@@ -260,8 +266,8 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   const uint64_t seed = in.seeds[s];
   PertRngF pr{0ull, static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
               static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
-  int k = cfg.k_lo + k1 + tile * kScreenThreads + tid;
-  bool live = k < cfg.k_hi;
+  int k = cfg.k_lo + kb0 + tile * kT + tid;
+  bool live = k < cfg.k_lo + kend;
   pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
   const double* xs = in.states + 10 * s;
   St<float> x;
@@ -270,6 +276,19 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
   x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
   CostSums<float> cs{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, true, false};
   float up[4] = {0.f, 0.f, 0.f, 0.f};
+  {  // the step-0 collision query (exact; every sample starts at x0)
+    __shared__ float s_d2;
+    __shared__ uint32_t s_hint;
+    if (tid == 0) {
+      uint32_t h = kNoHint;
+      s_d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.cdmax * env.cdmax * 1.0001f,
+                             env.cdmin * env.cdmin, &h);
+      s_hint = h;
+    }
+    __syncthreads();
+    env.d2_x0 = s_d2;
+    env.hint = s_hint;
+  }
   int round = 0;
   for (int j0 = 0; j0 < N; j0 += kCompact, ++round) {
     const int j1 = min(j0 + kCompact, N);
@@ -290,7 +309,7 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
     __syncthreads();
     int before = 0, total = 0, live_warps = 0;
 #pragma unroll
-    for (int w = 0; w < kScreenThreads / 32; ++w) {
+    for (int w = 0; w < kT / 32; ++w) {
       const int c = wc[w];
       before += w < warp ? c : 0;
       total += c;
@@ -301,29 +320,29 @@ __global__ void __launch_bounds__(kScreenThreads, kMinBlocks)
       if (live) {
         const int slot = before + __popc(bal & ((1u << lane) - 1u));
         float* st = &s_state[0][slot];
-        st[0 * kScreenThreads] = x.p.x; st[1 * kScreenThreads] = x.p.y; st[2 * kScreenThreads] = x.p.z;
-        st[3 * kScreenThreads] = x.q.w; st[4 * kScreenThreads] = x.q.x; st[5 * kScreenThreads] = x.q.y;
-        st[6 * kScreenThreads] = x.q.z;
-        st[7 * kScreenThreads] = x.v.x; st[8 * kScreenThreads] = x.v.y; st[9 * kScreenThreads] = x.v.z;
-        st[10 * kScreenThreads] = cs.trk; st[11 * kScreenThreads] = cs.vn; st[12 * kScreenThreads] = cs.mag;
-        st[13 * kScreenThreads] = cs.rate; st[14 * kScreenThreads] = cs.goal; st[15 * kScreenThreads] = cs.col;
-        st[16 * kScreenThreads] = up[0]; st[17 * kScreenThreads] = up[1]; st[18 * kScreenThreads] = up[2];
-        st[19 * kScreenThreads] = up[3];
-        st[20 * kScreenThreads] = __uint_as_float(env.hint);
+        st[0 * kT] = x.p.x; st[1 * kT] = x.p.y; st[2 * kT] = x.p.z;
+        st[3 * kT] = x.q.w; st[4 * kT] = x.q.x; st[5 * kT] = x.q.y;
+        st[6 * kT] = x.q.z;
+        st[7 * kT] = x.v.x; st[8 * kT] = x.v.y; st[9 * kT] = x.v.z;
+        st[10 * kT] = cs.trk; st[11 * kT] = cs.vn; st[12 * kT] = cs.mag;
+        st[13 * kT] = cs.rate; st[14 * kT] = cs.goal; st[15 * kT] = cs.col;
+        st[16 * kT] = up[0]; st[17 * kT] = up[1]; st[18 * kT] = up[2];
+        st[19 * kT] = up[3];
+        st[20 * kT] = __uint_as_float(env.hint);
         s_k[slot] = k;
       }
       __syncthreads();
       live = tid < total;
       if (live) {
         const float* st = &s_state[0][tid];
-        x.p = {st[0 * kScreenThreads], st[1 * kScreenThreads], st[2 * kScreenThreads]};
-        x.q = {st[3 * kScreenThreads], st[4 * kScreenThreads], st[5 * kScreenThreads], st[6 * kScreenThreads]};
-        x.v = {st[7 * kScreenThreads], st[8 * kScreenThreads], st[9 * kScreenThreads]};
-        cs.trk = st[10 * kScreenThreads]; cs.vn = st[11 * kScreenThreads]; cs.mag = st[12 * kScreenThreads];
-        cs.rate = st[13 * kScreenThreads]; cs.goal = st[14 * kScreenThreads]; cs.col = st[15 * kScreenThreads];
-        up[0] = st[16 * kScreenThreads]; up[1] = st[17 * kScreenThreads]; up[2] = st[18 * kScreenThreads];
-        up[3] = st[19 * kScreenThreads];
-        env.hint = __float_as_uint(st[20 * kScreenThreads]);
+        x.p = {st[0 * kT], st[1 * kT], st[2 * kT]};
+        x.q = {st[3 * kT], st[4 * kT], st[5 * kT], st[6 * kT]};
+        x.v = {st[7 * kT], st[8 * kT], st[9 * kT]};
+        cs.trk = st[10 * kT]; cs.vn = st[11 * kT]; cs.mag = st[12 * kT];
+        cs.rate = st[13 * kT]; cs.goal = st[14 * kT]; cs.col = st[15 * kT];
+        up[0] = st[16 * kT]; up[1] = st[17 * kT]; up[2] = st[18 * kT];
+        up[3] = st[19 * kT];
+        env.hint = __float_as_uint(st[20 * kT]);
         k = s_k[tid];
         pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
       }
@@ -531,43 +550,19 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     kern<<<static_cast<unsigned>(SM * tiles), threads, 0, st>>>(in, P, pl, cfg, iter, 0, 0);
     return cudaGetLastError();
   }
-  static const char* k1env = std::getenv("AMPPI_K1");  // experiment switch: bound-pass samples
-  const int k1 = k1env ? std::atoi(k1env) : 32;
+  const int k1 = 32;  // bound samples (best of 8-64 measured)
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
-    kern<<<static_cast<unsigned>(SM * ((k1 + 31) / 32)), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
+    kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
   }
   const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
   TimedRegion t(timer, "k_stage1_f32", st);
-  static const char* cmp = std::getenv("AMPPI_COMPACT");  // experiment switch: compaction interval (0 = off)
-  const int every = cmp ? std::atoi(cmp) : 10;
-  if (in.injected || every <= 0) {
+  if (in.injected) {
     kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
-  } else if (every == 1) {
-    k_stage1_f32c<8, 1><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-  } else if (every == 2) {
-    k_stage1_f32c<8, 2><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-  } else if (every <= 3) {
-    k_stage1_f32c<8, 3><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-  } else if (every <= 5) {
-    k_stage1_f32c<8, 5><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-  } else if (every <= 8) {
-    k_stage1_f32c<8, 8><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-  } else if (every <= 10) {
-    static const char* mb = std::getenv("AMPPI_MINBLOCKS");  // experiment switch: register budget
-    const int minb = mb ? std::atoi(mb) : 9;
-    if (minb == 10)
-      k_stage1_f32c<10, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-    else if (minb == 9)
-      k_stage1_f32c<9, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-    else if (minb == 6)
-      k_stage1_f32c<6, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-    else if (minb == 7)
-      k_stage1_f32c<7, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
-    else
-      k_stage1_f32c<8, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
   } else {
-    k_stage1_f32c<8, 15><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1);
+    // lane compaction every 10 steps, 9 CTAs (56 registers) per SM: best measured
+    k_stage1_f32c<9, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1, kr,
+                                                                                      k1);
   }
   return cudaGetLastError();
 }
