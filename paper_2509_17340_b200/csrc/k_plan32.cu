@@ -531,12 +531,10 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   const int kr = cfg.k_hi - cfg.k_lo;  // samples per instance screened here
   const int64_t total = static_cast<int64_t>(in.S) * cfg.M * kr;
   const int64_t SM = static_cast<int64_t>(in.S) * cfg.M;
-  static const char* sched = std::getenv("AMPPI_SCREEN");  // experiment switch: "single" disables the bound
-  const bool single = sched && std::strcmp(sched, "single") == 0;
   // throughput mode: 64 registers (8 CTAs = 32 warps per SM, a few bytes of
   // L1-resident spill); latency mode: no cap (fastest single rollout)
   auto kern = k_stage1_f32<8>;
-  if (single || total < 148 * 128 * 4 || kr <= 64) {
+  if (total < 148 * 128 * 4 || kr <= 64) {
     // latency mode (few rollouts): one pass, warps spread over the SMs
     const int threads = total < 148 * 128 ? 32 : 128;
     const int tiles = (kr + threads - 1) / threads;
