@@ -466,6 +466,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   for (uint32_t l0 = 2 * warp; l0 < n_leaves; l0 += wstride) {
     const uint32_t l = l0 + (lane >> 4);
     double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    static_assert(kLeafSize <= 16, "one lane per leaf point");
     if (l < n_leaves) {
       const uint32_t t = (lstart[l] & 0x7FFFFFFFu) + sub;
       if (t < (lstart[l + 1] & 0x7FFFFFFFu))

@@ -26,7 +26,10 @@ constexpr double kHorizonReach = 25.0;
 // 27-bit mask of its non-empty neighbours (bit i*9+j*3+k <-> offset
 // (i-1, j-1, k-1)); mask 0 = no point within one cell.
 constexpr int kGridAxis = 24;
-constexpr uint32_t kLeafSize = 16;
+#ifndef AMPPI_LEAF_SIZE
+#define AMPPI_LEAF_SIZE 16
+#endif
+constexpr uint32_t kLeafSize = AMPPI_LEAF_SIZE;
 constexpr uint32_t kNoHint = 0xFFFFFFFFu;
 constexpr int kGridCells = kGridAxis * kGridAxis * kGridAxis;
 constexpr int kPadAxis = kGridAxis + 2;
