@@ -191,6 +191,15 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
 // memory, so warps whose lanes all aborted stop issuing.  Same per-sample
 // arithmetic as k_stage1_f32 mode 2.
 constexpr int kScreenThreads = 128;
+#ifndef AMPPI_MAIN_THREADS  // experiment switches (make variant DEFS=...)
+#define AMPPI_MAIN_THREADS 224
+#define AMPPI_MAIN_MINBLOCKS 5
+#endif
+#ifndef AMPPI_MAIN_COMPACT
+#define AMPPI_MAIN_COMPACT 10
+#endif
+constexpr int kMainThreads = AMPPI_MAIN_THREADS, kMainMinBlocks = AMPPI_MAIN_MINBLOCKS;
+constexpr int kMainCompact = AMPPI_MAIN_COMPACT;
 constexpr int kStateWords = 21;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint
 
 // Samples [k_lo + kb0, k_lo + kend) of every instance, aborted against the
@@ -553,14 +562,24 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     TimedRegion t(timer, "k_stage1_f32_bound", st);
     kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
   }
-  const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
   TimedRegion t(timer, "k_stage1_f32", st);
   if (in.injected) {
+    const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
     kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
   } else {
-    // lane compaction every 10 steps, 9 CTAs (56 registers) per SM: best measured
-    k_stage1_f32c<9, 10><<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1, kr,
-                                                                                      k1);
+    // Lane compaction every 10 steps at 56 registers.  The larger the CTA,
+    // the better live samples pack: 224 threads (5 CTAs per SM; the whole
+    // K = 256 main pass of an instance in one CTA) beat 128 (9 per SM) by 4%,
+    // 64 threads lose 15% (C5, measured); 128 when that covers the samples.
+    if (kr - k1 > 128) {
+      const int tiles = (kr - k1 + kMainThreads - 1) / kMainThreads;
+      k_stage1_f32c<kMainMinBlocks, kMainCompact, kMainThreads>
+          <<<static_cast<unsigned>(SM * tiles), kMainThreads, 0, st>>>(in, P, pl, cfg, iter, k1, kr, k1);
+    } else {
+      const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
+      k_stage1_f32c<9, kMainCompact, kScreenThreads>
+          <<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1, kr, k1);
+    }
   }
   return cudaGetLastError();
 }
