@@ -1014,7 +1014,7 @@ cudaError_t launch_gather(const Plan& pl, const DevConfig& cfg, int S, const Gat
   return cudaGetLastError();
 }
 
-static int device_sms() {
+int device_sms() {
   static int sms = [] {
     int v = 148, dev = 0;
     cudaGetDevice(&dev);

@@ -119,6 +119,7 @@ struct GatherOut {
 cudaError_t launch_gather(const Plan& pl, const DevConfig& cfg, int S, const GatherOut& g, cudaStream_t st);
 
 // FP32 stage-I screening rollouts (k_plan32.cu).
+int device_sms();  // SM count of the current device (cached)
 cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
                               cudaStream_t st, KernelTimer* timer);
 
