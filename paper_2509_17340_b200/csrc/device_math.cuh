@@ -433,16 +433,49 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
   return best;
 }
 
+// Squared norm with a pinned evaluation shape, fma(z, z, fma(y, y, x * x)):
+// the FP32 box bounds and the packed point distances below both use it, and
+// it is monotone in each |component|, so a box distance never exceeds the
+// distance of a point inside the box.
+__device__ __forceinline__ float sq3f(float x, float y, float z) {
+  return __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
+}
+
+// Squared distances from p to the 4 points of one FP32 point block
+// ({x0..x3}, {y0..y3}, {z0..z3}), as two packed FP32x2 pairs: per pair one
+// FADD2 per axis, FMUL2, two FFMA2 (sm_100 packed FP32) -- the sq3f shape.
+__device__ __forceinline__ void block_d2(const float4* __restrict__ blk, V3<float> p, float2& d01, float2& d23) {
+  const float4 X = __ldg(blk), Y = __ldg(blk + 1), Z = __ldg(blk + 2);
+  const float2 npx = make_float2(-p.x, -p.x), npy = make_float2(-p.y, -p.y), npz = make_float2(-p.z, -p.z);
+  float2 dx = __fadd2_rn(make_float2(X.x, X.y), npx), dy = __fadd2_rn(make_float2(Y.x, Y.y), npy),
+         dz = __fadd2_rn(make_float2(Z.x, Z.y), npz);
+  d01 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+  dx = __fadd2_rn(make_float2(X.z, X.w), npx);
+  dy = __fadd2_rn(make_float2(Y.z, Y.w), npy);
+  dz = __fadd2_rn(make_float2(Z.z, Z.w), npz);
+  d23 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+}
+
+__device__ __forceinline__ float block_min_d2(const float4* __restrict__ pts, uint32_t blk, V3<float> p) {
+  float2 a, b;
+  block_d2(pts + 3 * blk, p, a, b);
+  return fminf(fminf(a.x, a.y), fminf(b.x, b.y));
+}
+
 // FP32 screening query: as nearest_sq_exact, plus a second branch-and-bound
-// level over each scanned cell's 16-point leaves (float leaf boxes).  Returns
+// level over each scanned cell's 16-point leaves (float leaf boxes).  Points
+// are stored in blocks of 4 (kPointBlock, struct-of-arrays x4 / y4 / z4,
+// +inf padding past the last point) and scanned a block at a time with
+// packed FP32x2 arithmetic; a leaf's blocks may include a few points of the
+// neighbouring leaves -- real points, so the minimum is unchanged.  Returns
 // the exact squared distance when it lies in [stop2, lim2); any value below
 // stop2 once a point closer than sqrt(stop2) is found (with stop2 = lim2 this
 // is an existence test for a point within reach); >= lim2 (or +inf) when no
-// point is closer than sqrt(lim2).  *hint (a point index, kNoHint for none)
-// seeds the search with that point's distance -- an upper bound on the
-// minimum, so every box at least that far is pruned from the start -- and
-// receives the nearest point found (the previous step's nearest point is a
-// good seed for the next step of the same rollout).
+// point is closer than sqrt(lim2).  *hint (a block index, kNoHint for none)
+// seeds the search with that block's nearest distance -- an upper bound on
+// the minimum, so every box at least that far is pruned from the start --
+// and receives the block of the nearest point found (the previous step's
+// nearest block is a good seed for the next step of the same rollout).
 __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4* __restrict__ rec,
                                                  const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
                                                  const float4* __restrict__ pts, V3<float> p, float lim2, float stop2,
@@ -451,8 +484,7 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
   if (g.dims[0] == 0) return best;
   uint32_t bi = *hint;
   if (bi != kNoHint) {
-    const float4 qq = __ldg(pts + bi);
-    best = sqnorm(V3<float>{p.x - qq.x, p.y - qq.y, p.z - qq.z});
+    best = block_min_d2(pts, bi, p);
     if (best < stop2) return best;
   }
   const int cx = __float2int_rd((p.x - g.origin_f[0]) * g.inv_h_f);
@@ -479,27 +511,26 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
       const int c = cbase + nbr_offset(b, d12, d2);
       const uint4 ra = __ldg(rec + 2 * c), rb = __ldg(rec + 2 * c + 1);
       AMPPI_STAT(2, 1);
-      const V3<float> gap{fmaxf(fmaxf(__uint_as_float(ra.z) - p.x, p.x - __uint_as_float(rb.y)), 0.f),
-                          fmaxf(fmaxf(__uint_as_float(ra.w) - p.y, p.y - __uint_as_float(rb.z)), 0.f),
-                          fmaxf(fmaxf(__uint_as_float(rb.x) - p.z, p.z - __uint_as_float(rb.w)), 0.f)};
-      if (sqnorm(gap) >= fminf(best, lim2)) continue;
+      if (sq3f(fmaxf(fmaxf(__uint_as_float(ra.z) - p.x, p.x - __uint_as_float(rb.y)), 0.f),
+               fmaxf(fmaxf(__uint_as_float(ra.w) - p.y, p.y - __uint_as_float(rb.z)), 0.f),
+               fmaxf(fmaxf(__uint_as_float(rb.x) - p.z, p.z - __uint_as_float(rb.w)), 0.f)) >= fminf(best, lim2))
+        continue;
       AMPPI_STAT(3, 1);
       const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
       const uint4* lf = leaves + 2 * ra.y;
       for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
         const uint4 la = __ldg(lf), lb = __ldg(lf + 1);
-        const V3<float> lg{fmaxf(fmaxf(__uint_as_float(la.x) - p.x, p.x - __uint_as_float(lb.x)), 0.f),
-                           fmaxf(fmaxf(__uint_as_float(la.y) - p.y, p.y - __uint_as_float(lb.y)), 0.f),
-                           fmaxf(fmaxf(__uint_as_float(la.z) - p.z, p.z - __uint_as_float(lb.z)), 0.f)};
-        if (sqnorm(lg) >= fminf(best, lim2)) continue;
+        if (sq3f(fmaxf(fmaxf(__uint_as_float(la.x) - p.x, p.x - __uint_as_float(lb.x)), 0.f),
+                 fmaxf(fmaxf(__uint_as_float(la.y) - p.y, p.y - __uint_as_float(lb.y)), 0.f),
+                 fmaxf(fmaxf(__uint_as_float(la.z) - p.z, p.z - __uint_as_float(lb.z)), 0.f)) >= fminf(best, lim2))
+          continue;
         const uint32_t te = min(t + kLeafSize, k1);
         AMPPI_STAT(4, te - t);
 #ifdef AMPPI_STATS
         q_scanned += te - t;
 #endif
-        for (uint32_t u = t; u < te; ++u) {
-          const float4 qq = __ldg(pts + u);
-          const float dd = sqnorm(V3<float>{p.x - qq.x, p.y - qq.y, p.z - qq.z});
+        for (uint32_t u = t / kPointBlock; u <= (te - 1) / kPointBlock; ++u) {
+          const float dd = block_min_d2(pts, u, p);
           if (dd < best) {
             best = dd;
             bi = u;

@@ -422,6 +422,12 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   uint4* __restrict__ gleaf = P.grid_leaf + cell_base * 2;
   uint8_t* lflag = reinterpret_cast<uint8_t*>(vals + kCellsPow2);  // [8192] (inside rng, past keys/vals)
   for (uint32_t i = tid; i < kCellsPow2; i += blockDim.x) lflag[i] = 0;
+  // +inf padding of the last FP32 point block
+  if (n_pts + tid < (n_pts + kPointBlock - 1) / kPointBlock * kPointBlock) {
+    const uint32_t i = n_pts + tid;
+    float* blk = reinterpret_cast<float*>(gp32 + 3 * (i / kPointBlock)) + i % kPointBlock;
+    blk[0] = blk[kPointBlock] = blk[2 * kPointBlock] = __int_as_float(0x7f800000);
+  }
   __syncthreads();
   for (uint32_t i = tid; i < n_pts; i += blockDim.x) {
     const uint32_t k = vals[i];
@@ -429,7 +435,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     gp64[3 * i] = x;
     gp64[3 * i + 1] = y;
     gp64[3 * i + 2] = z;
-    gp32[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.f);
+    float* blk = reinterpret_cast<float*>(gp32 + 3 * (i / kPointBlock)) + i % kPointBlock;
+    blk[0] = static_cast<float>(x);
+    blk[kPointBlock] = static_cast<float>(y);
+    blk[2 * kPointBlock] = static_cast<float>(z);
     const uint32_t c = keys[i] >> 9;
     if (i == 0 || (keys[i - 1] >> 9) != c) {  // first point of cell c
       uint32_t e = i + 1;

@@ -30,6 +30,7 @@ constexpr int kGridAxis = 24;
 #define AMPPI_LEAF_SIZE 16
 #endif
 constexpr uint32_t kLeafSize = AMPPI_LEAF_SIZE;
+constexpr uint32_t kPointBlock = 4;  // FP32 query points per struct-of-arrays block
 constexpr uint32_t kNoHint = 0xFFFFFFFFu;
 constexpr int kGridCells = kGridAxis * kGridAxis * kGridAxis;
 constexpr int kPadAxis = kGridAxis + 2;
@@ -106,7 +107,7 @@ struct Perception {
   uint32_t* grid_nbr;          // [S*kPadCells] neighbour masks over the padded lattice
   uint4* grid_leaf;            // [S*7200*2] leaf boxes
   double* grid_pts64;          // [S*7200*3] sorted by grid cell
-  float4* grid_pts32;          // [S*7200]
+  float4* grid_pts32;          // [S*7200]: per scene 1800 blocks of kPointBlock points {x4, y4, z4} (+inf padding)
 };
 
 // Non-collision cost sums of a deferred-collision FP64 rollout (latency path).
