@@ -205,19 +205,17 @@ __device__ __forceinline__ void normal_pair(uint64_t key, uint32_t p, double& n0
   n1 = r * s;
 }
 
-// FP32 screening draw: same integers, float arithmetic with full-range tails
-// (1 - U kept exact via the integer complement; small U via log1p).
+// FP32 screening draw: same integers, float arithmetic.  1 - U comes from
+// the integer complement (so U near 1 keeps its tail) rounded once to float,
+// and one hardware log2 serves every U -- no data-dependent branch, so the
+// lanes of a warp stay converged (absolute error of log(1-U) < 1e-6, far
+// inside the screening window).
 __device__ __forceinline__ void normal_pair_f(uint64_t key, uint32_t p, float& n0, float& n1) {
   const uint64_t a = mix64(key + (2ull * p + 1ull) * kGamma);
   const uint64_t b = mix64(key + (2ull * p + 2ull) * kGamma);
   const uint64_t ma = a >> 11;
-  float lg;
-  if (ma < (1ull << 52)) {  // U < 0.5: log(1-U) = log1p(-U)
-    lg = log1pf(-static_cast<float>(ma) * 0x1.0p-53f);
-  } else {
-    lg = logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
-  }
-  const float r = sqrtf(-2.0f * lg);
+  const float lg = __logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
+  const float r = sqrtf(fmaxf(-2.0f * lg, 0.0f));  // (the approximate log may round above 0 next to 1)
   // angle 2*pi*u2 in [0, 2pi): hardware sin/cos after reduction to [-pi, pi)
   // (abs error ~1e-6, far inside the screening window)
   const float u2 = static_cast<float>(b >> 11) * 0x1.0p-53f;
