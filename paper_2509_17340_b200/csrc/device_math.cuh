@@ -406,12 +406,12 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
       mm &= mm - 1;
       const int c = cbase + nbr_offset(b, d12, d2);
       const uint4 ra = rec[2 * c], rb = rec[2 * c + 1];
-      if (box_d2(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
+      if (box_d2(ra.z, rb.x, rb.z, ra.w, rb.y, rb.w) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
       const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
       const uint4* lf = leaves + 2 * ra.y;
       for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
         const uint4 la = lf[0], lb = lf[1];
-        if (box_d2(la.x, la.y, la.z, lb.x, lb.y, lb.z) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
+        if (box_d2(la.x, la.z, lb.x, la.y, la.w, lb.y) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
         const uint32_t te = min(t + kLeafSize, k1);
         for (uint32_t k = t; k < te; ++k) {
           const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
@@ -437,6 +437,18 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
 // distance of a point inside the box.
 __device__ __forceinline__ float sq3f(float x, float y, float z) {
   return __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
+}
+
+// Squared distance from p to a float box given as per-axis (lo, hi) pairs
+// (the cell record / leaf box layout): per axis one packed FADD2 gives
+// (lo - p, hi - p); gap = max(lo - p, p - hi, 0) in the same rounding as
+// the point differences, squared in the sq3f shape.
+__device__ __forceinline__ float box_gap_sq(uint32_t lx, uint32_t hx, uint32_t ly, uint32_t hy, uint32_t lz,
+                                           uint32_t hz, V3<float> p) {
+  const float2 dx = __fadd2_rn(make_float2(__uint_as_float(lx), __uint_as_float(hx)), make_float2(-p.x, -p.x));
+  const float2 dy = __fadd2_rn(make_float2(__uint_as_float(ly), __uint_as_float(hy)), make_float2(-p.y, -p.y));
+  const float2 dz = __fadd2_rn(make_float2(__uint_as_float(lz), __uint_as_float(hz)), make_float2(-p.z, -p.z));
+  return sq3f(fmaxf(fmaxf(dx.x, -dx.y), 0.f), fmaxf(fmaxf(dy.x, -dy.y), 0.f), fmaxf(fmaxf(dz.x, -dz.y), 0.f));
 }
 
 // Squared distances from p to the 4 points of one FP32 point block
@@ -509,19 +521,13 @@ __device__ __forceinline__ float nearest_sq_fast(const GridMeta& g, const uint4*
       const int c = cbase + nbr_offset(b, d12, d2);
       const uint4 ra = __ldg(rec + 2 * c), rb = __ldg(rec + 2 * c + 1);
       AMPPI_STAT(2, 1);
-      if (sq3f(fmaxf(fmaxf(__uint_as_float(ra.z) - p.x, p.x - __uint_as_float(rb.y)), 0.f),
-               fmaxf(fmaxf(__uint_as_float(ra.w) - p.y, p.y - __uint_as_float(rb.z)), 0.f),
-               fmaxf(fmaxf(__uint_as_float(rb.x) - p.z, p.z - __uint_as_float(rb.w)), 0.f)) >= fminf(best, lim2))
-        continue;
+      if (box_gap_sq(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w, p) >= fminf(best, lim2)) continue;
       AMPPI_STAT(3, 1);
       const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
       const uint4* lf = leaves + 2 * ra.y;
       for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
         const uint4 la = __ldg(lf), lb = __ldg(lf + 1);
-        if (sq3f(fmaxf(fmaxf(__uint_as_float(la.x) - p.x, p.x - __uint_as_float(lb.x)), 0.f),
-                 fmaxf(fmaxf(__uint_as_float(la.y) - p.y, p.y - __uint_as_float(lb.y)), 0.f),
-                 fmaxf(fmaxf(__uint_as_float(la.z) - p.z, p.z - __uint_as_float(lb.z)), 0.f)) >= fminf(best, lim2))
-          continue;
+        if (box_gap_sq(la.x, la.y, la.z, la.w, lb.x, lb.y, p) >= fminf(best, lim2)) continue;
         const uint32_t te = min(t + kLeafSize, k1);
         AMPPI_STAT(4, te - t);
 #ifdef AMPPI_STATS

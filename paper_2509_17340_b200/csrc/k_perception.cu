@@ -490,10 +490,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
         hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
       }
     if (sub == 0 && l < n_leaves) {
-      gleaf[2 * l] = make_uint4(__float_as_uint(__double2float_rd(lo[0])), __float_as_uint(__double2float_rd(lo[1])),
-                                __float_as_uint(__double2float_rd(lo[2])), 0u);
-      gleaf[2 * l + 1] = make_uint4(__float_as_uint(__double2float_ru(hi[0])), __float_as_uint(__double2float_ru(hi[1])),
-                                    __float_as_uint(__double2float_ru(hi[2])), 0u);
+      gleaf[2 * l] = make_uint4(__float_as_uint(__double2float_rd(lo[0])), __float_as_uint(__double2float_ru(hi[0])),
+                                __float_as_uint(__double2float_rd(lo[1])), __float_as_uint(__double2float_ru(hi[1])));
+      gleaf[2 * l + 1] =
+          make_uint4(__float_as_uint(__double2float_rd(lo[2])), __float_as_uint(__double2float_ru(hi[2])), 0u, 0u);
     }
   }
   __syncthreads();
@@ -519,10 +519,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (uint32_t k = sub; k < nl; k += 16) {
       const uint4 la = gleaf[2 * (l + k)], lb = gleaf[2 * (l + k) + 1];
-      lo[0] = fminf(lo[0], __uint_as_float(la.x)); lo[1] = fminf(lo[1], __uint_as_float(la.y));
-      lo[2] = fminf(lo[2], __uint_as_float(la.z));
-      hi[0] = fmaxf(hi[0], __uint_as_float(lb.x)); hi[1] = fmaxf(hi[1], __uint_as_float(lb.y));
-      hi[2] = fmaxf(hi[2], __uint_as_float(lb.z));
+      lo[0] = fminf(lo[0], __uint_as_float(la.x)); lo[1] = fminf(lo[1], __uint_as_float(la.z));
+      lo[2] = fminf(lo[2], __uint_as_float(lb.x));
+      hi[0] = fmaxf(hi[0], __uint_as_float(la.y)); hi[1] = fmaxf(hi[1], __uint_as_float(la.w));
+      hi[2] = fmaxf(hi[2], __uint_as_float(lb.y));
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1)
@@ -534,8 +534,8 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     if (sub == 0 && act) {
       const uint32_t i = lstart[l] & 0x7FFFFFFFu, e = lstart[l + nl] & 0x7FFFFFFFu;
       const uint32_t c = keys[i] >> 9;
-      grec[2 * c] = make_uint4(i | ((e - i) << 16), l, __float_as_uint(lo[0]), __float_as_uint(lo[1]));
-      grec[2 * c + 1] = make_uint4(__float_as_uint(lo[2]), __float_as_uint(hi[0]), __float_as_uint(hi[1]),
+      grec[2 * c] = make_uint4(i | ((e - i) << 16), l, __float_as_uint(lo[0]), __float_as_uint(hi[0]));
+      grec[2 * c + 1] = make_uint4(__float_as_uint(lo[1]), __float_as_uint(hi[1]), __float_as_uint(lo[2]),
                                    __float_as_uint(hi[2]));
     }
   }

@@ -19,10 +19,11 @@ constexpr double kHorizonReach = 25.0;
 
 // Collision grid: at most kGridAxis cells per axis, cell size >= d_max.
 // Every cell owns a 32-byte record (two uint4: {start | count << 16, first
-// leaf, lo.x, lo.y}, {lo.z, hi.x, hi.y, hi.z}; the float box holds the cell's
-// points, rounded outward from FP64).  A cell's points (sorted by Morton code
-// of the 1/8-cell sub-position) form leaves of kLeafSize consecutive points;
-// a leaf box is {lo.xyz, -}, {hi.xyz, -} in float (outward-rounded).  The padded lattice (dims+2)^3 holds, per cell, the
+// leaf, lo.x, hi.x}, {lo.y, hi.y, lo.z, hi.z}; the float box holds the cell's
+// points, rounded outward from FP64; per-axis (lo, hi) pairs feed the packed
+// FP32x2 box test).  A cell's points (sorted by Morton code of the 1/8-cell
+// sub-position) form leaves of kLeafSize consecutive points; a leaf box is
+// {lo.x, hi.x, lo.y, hi.y}, {lo.z, hi.z, -, -} in float (outward-rounded).  The padded lattice (dims+2)^3 holds, per cell, the
 // 27-bit mask of its non-empty neighbours (bit i*9+j*3+k <-> offset
 // (i-1, j-1, k-1)); mask 0 = no point within one cell.
 constexpr int kGridAxis = 24;
