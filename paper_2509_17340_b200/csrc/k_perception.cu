@@ -183,7 +183,10 @@ __global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
 // ---------------------------------------------------------------------------
 // finalize body
 // ---------------------------------------------------------------------------
-constexpr int kFinalizeThreads = 256;      // fused per-scene CTAs (two per SM)
+#ifndef AMPPI_SNAP_THREADS
+#define AMPPI_SNAP_THREADS 512
+#endif
+constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (two per SM)
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
@@ -589,7 +592,10 @@ __global__ void __launch_bounds__(kFinalizeThreadsFew, 1) k_finalize_scene(Batch
 }
 
 // Fused schedule: one CTA per scene, per-cell minimum in shared memory.
-__global__ void __launch_bounds__(kFinalizeThreads, 2) k_snapshot_scene(BatchIn in, Perception P, DevConfig cfg) {
+#ifndef AMPPI_SNAP_MINB
+#define AMPPI_SNAP_MINB 2
+#endif
+__global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_scene(BatchIn in, Perception P, DevConfig cfg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FinalizeSmem& sm = *reinterpret_cast<FinalizeSmem*>(smem_raw);
   unsigned long long* cell_bits = reinterpret_cast<unsigned long long*>(sm.rng);

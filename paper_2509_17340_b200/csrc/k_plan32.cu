@@ -193,6 +193,8 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
 constexpr int kScreenThreads = 128;
 #ifndef AMPPI_MAIN_THREADS  // experiment switches (make variant DEFS=...)
 #define AMPPI_MAIN_THREADS 224
+#endif
+#ifndef AMPPI_MAIN_MINBLOCKS
 #define AMPPI_MAIN_MINBLOCKS 5
 #endif
 #ifndef AMPPI_MAIN_COMPACT
