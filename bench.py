@@ -306,10 +306,14 @@ def run_b200(args):
     # e2e through the host-pointer API
     e2e = None
     if not args.no_e2e:
+        # the user-facing call, without the per-kernel timing events of the
+        # device-resident measurement above
+        planner.close()
+        planner = Planner(cfg, device=local, precision=32, max_scenes=S, max_points=max(P, 1 << 16),
+                          stream=stream.cuda_stream)
         pinned_xyz = torch.from_numpy(data["xyz"]).pin_memory()  # keep alive while in use
         host = {k: data[k] for k in ("offsets", "poses", "states", "goals", "last", "cycles", "seeds")}
         host["xyz"] = pinned_xyz.numpy()
-        planner.kernel_times_reset()
         for i in range(max(1, args.warmup)):
             planner.cycle_batch(host["offsets"], host["xyz"], host["poses"], host["states"], host["goals"],
                                 host["last"], host["cycles"] + i, host["seeds"])

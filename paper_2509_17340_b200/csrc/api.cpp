@@ -25,7 +25,7 @@ using namespace amppi_dev;
 namespace {
 
 constexpr double kPi = std::numbers::pi;
-constexpr int kMaxChunks = 4;  // concurrent chunks of a batch (work-list counters)
+constexpr int kMaxChunks = 8;  // chunks of a pipelined batch (one work-list counter each)
 
 struct Arena {
   std::vector<void*> blocks;
@@ -970,13 +970,16 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   // Pipeline: the points of chunk c+1 cross PCIe on the copy stream while
   // chunk c is planned.  Chunks are whole scenes (>= 2 fused-snapshot waves);
   // results land at each scene's batch position.
-  // Up to 4 chunks of >= ~8M points and >= 296 scenes (the smallest one must
+  // Up to 6 chunks of >= ~8M points and >= 296 scenes (the smallest one must
   // keep the fused snapshot: >= 148 scenes).
-  int chunks = static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, total / (8 << 20))));
+  int chunks = static_cast<int>(std::min<int64_t>(6, std::max<int64_t>(1, total / (8 << 20))));
   chunks = std::max(1, std::min(chunks, S / 296));
+  double ratio = 1.3;  // C5 on a B200 over PCIe 5: best of 4-8 chunks x ratio 1.0-1.6 (tools/pipe_sweep.py)
   if (const char* f = std::getenv("AMPPI_PIPELINE_CHUNKS")) chunks = std::max(1, std::min(S, std::atoi(f)));  // tests
+  if (const char* f = std::getenv("AMPPI_PIPELINE_RATIO")) ratio = std::max(1.0, std::atof(f));
   chunks = std::min(chunks, kMaxChunks);
-  while (chunks > 1 && S * 1.0 / ((std::pow(1.6, chunks) - 1.0) / 0.6) < 148) --chunks;  // smallest chunk >= 148
+  auto first_chunk = [&](int n) { return ratio > 1.0 ? S * (ratio - 1.0) / (std::pow(ratio, n) - 1.0) : 1.0 * S / n; };
+  while (chunks > 1 && first_chunk(chunks) < 148) --chunks;  // smallest chunk >= 148
   while (static_cast<int>(ctx->chunk_ready.size()) < chunks) {
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1006,14 +1009,14 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     CK(cudaEventRecord(ctx->join[0], ctx->stream));
     CK(cudaStreamWaitEvent(ctx->stream2, ctx->join[0], 0));
   }
-  // Chunk sizes grow geometrically (ratio 1.6 ~ planning time / upload time
-  // per scene on a B200 over PCIe 5): the first chunk's upload is the only
-  // one not hidden behind planning, so it is the smallest.
+  // Chunk sizes grow geometrically: the first chunk's upload is the only one
+  // not hidden behind planning, so it is the smallest; later chunks grow so
+  // their uploads stay ahead of the planning.
   std::vector<int> bound(chunks + 1, 0);
   {
     double w = 1.0, sum = 0.0;
     std::vector<double> cum(chunks + 1, 0.0);
-    for (int c = 0; c < chunks; ++c, w *= 1.6) cum[c + 1] = (sum += w);
+    for (int c = 0; c < chunks; ++c, w *= ratio) cum[c + 1] = (sum += w);
     for (int c = 1; c <= chunks; ++c) bound[c] = static_cast<int>(std::llround(S * cum[c] / sum));
     bound[chunks] = S;
   }
