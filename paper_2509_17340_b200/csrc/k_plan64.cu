@@ -25,6 +25,10 @@
 #include "kernels.h"
 #include "rollout.cuh"
 
+#ifndef AMPPI_COL_MINB
+#define AMPPI_COL_MINB 8  // FP64 collision-term kernels at 64 registers (8 CTAs per SM): measured best of 1-16
+#endif
+
 namespace amppi_dev {
 
 namespace {
@@ -848,7 +852,7 @@ __device__ __forceinline__ double collision_sum_warp(const RolloutEnv<double>& e
   return __shfl_sync(0xffffffffu, col, 0);
 }
 
-__global__ void __launch_bounds__(128) k_stage2_col(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+__global__ void __launch_bounds__(128, AMPPI_COL_MINB) k_stage2_col(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
   __shared__ double s_terms[4][64];
   const int64_t smi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -934,7 +938,7 @@ __global__ void __launch_bounds__(64) k_refine_traj_w(BatchIn in, Perception P, 
   }
 }
 
-__global__ void __launch_bounds__(128) k_refine_col(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+__global__ void __launch_bounds__(128, AMPPI_COL_MINB) k_refine_col(BatchIn in, Perception P, Plan pl, DevConfig cfg,
                                                     UpdateScratch us) {
   __shared__ double s_terms[4][64];
   const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
