@@ -26,6 +26,7 @@ namespace {
 
 constexpr double kPi = std::numbers::pi;
 constexpr int kMaxChunks = 8;  // chunks of a pipelined batch (one work-list counter each)
+constexpr int kExtraStreams = 2;  // compute streams beyond stream / stream2
 
 struct Arena {
   std::vector<void*> blocks;
@@ -138,6 +139,7 @@ struct amppi_ctx {
   bool own_stream{false};
   cudaStream_t copy_stream{nullptr};  // host->device point copies overlapped with planning
   cudaStream_t stream2{nullptr};      // second compute stream: alternate chunks of a batch run concurrently
+  cudaStream_t xstream[kExtraStreams]{};  // further compute streams for pipelined chunks
   cudaEvent_t inputs_read{nullptr};   // single-scene snapshot inputs copied (staging reusable)
   std::vector<cudaEvent_t> join;
   std::vector<cudaEvent_t> chunk_ready;
@@ -302,8 +304,9 @@ int create_impl(amppi_ctx* ctx) {
   }
   CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+  for (cudaStream_t& x : ctx->xstream) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->inputs_read, cudaEventDisableTiming));
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 2 + kExtraStreams; ++i) {
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     ctx->join.push_back(ev);
@@ -662,6 +665,8 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  for (cudaStream_t x : ctx->xstream)
+    if (x) cudaStreamDestroy(x);
   if (ctx->inputs_read) cudaEventDestroy(ctx->inputs_read);
   for (cudaEvent_t e : ctx->join) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->chunk_ready) cudaEventDestroy(e);
@@ -1001,13 +1006,21 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     tev.push_back(e);
   };
   tmark(ctx->copy_stream);
-  // chunks alternate between the two compute streams (each chunk's arrays
-  // live at its own offset), so one chunk's latency-bound tail overlaps the
-  // next chunk's work; both streams join ctx->stream before the gather
+  // chunks rotate over the compute streams (each chunk's arrays live at its
+  // own offset), so one chunk's latency-bound tail overlaps the next chunks'
+  // work; every stream joins ctx->stream before the gather
   const bool concurrent = chunks > 1;
+  static const int n_streams = [] {
+    const char* f = std::getenv("AMPPI_PIPELINE_STREAMS");
+    return f ? std::max(2, std::min(2 + kExtraStreams, std::atoi(f))) : 3;  // 3: best of 2-4 (tools/pipe_sweep.py)
+  }();
+  auto cstream = [&](int c) {
+    const int i = c % n_streams;
+    return i == 0 ? ctx->stream : (i == 1 ? ctx->stream2 : ctx->xstream[i - 2]);
+  };
   if (concurrent) {
     CK(cudaEventRecord(ctx->join[0], ctx->stream));
-    CK(cudaStreamWaitEvent(ctx->stream2, ctx->join[0], 0));
+    for (int i = 1; i < n_streams; ++i) CK(cudaStreamWaitEvent(cstream(i), ctx->join[0], 0));
   }
   // Chunk sizes grow geometrically: the first chunk's upload is the only one
   // not hidden behind planning, so it is the smallest; later chunks grow so
@@ -1029,7 +1042,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
                          cudaMemcpyHostToDevice, ctx->copy_stream));
     CK(cudaEventRecord(ctx->chunk_ready[c], ctx->copy_stream));
     tmark(ctx->copy_stream);
-    const cudaStream_t cst = (concurrent && (c & 1)) ? ctx->stream2 : ctx->stream;
+    const cudaStream_t cst = concurrent ? cstream(c) : ctx->stream;
     CK(cudaStreamWaitEvent(cst, ctx->chunk_ready[c], 0));
     int64_t max_chunk_scene = 0;
     for (int s = s0; s < s1; ++s)
@@ -1051,10 +1064,11 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     }
     tmark(cst);
   }
-  if (concurrent) {
-    CK(cudaEventRecord(ctx->join[1], ctx->stream2));
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
-  }
+  if (concurrent)
+    for (int i = 1; i < n_streams; ++i) {
+      CK(cudaEventRecord(ctx->join[i], cstream(i)));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->join[i], 0));
+    }
   if (trace) {
     cudaDeviceSynchronize();
     std::fprintf(stderr, "pipeline %d chunks:", chunks);
