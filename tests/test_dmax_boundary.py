@@ -1,0 +1,38 @@
+"""The collision term jumps at d_max (C exp(-a (d_max - d_min)) -> 0), so an
+FP32 screening distance on the wrong side of d_max changes a sample's FP32
+cost by ~5e4 while its FP64 cost does not move.  The support selection must
+stay exact anyway: here the best sample (zero perturbation, every other
+sample far worse) passes a single obstacle point at d_max (1 + eps) for
+eps in +-3e-7, so its FP32 distance rounds to either side; the FP64 result
+must equal the oracle's for every eps (contract of test_plan_parity)."""
+import numpy as np
+import pytest
+
+from test_plan_parity import make_cfg, run_case, state
+
+pytestmark = pytest.mark.gpu
+
+
+def _scenario(oracle):
+    cfg = make_cfg(1, 1, K=64, N=30)
+    rs = np.random.default_rng(4)
+    inj = rs.normal(size=(1, 1, 64, 30, 4)) * np.array([1.0, 1.0, 1.0, 0.5]) * 2.0
+    inj[0, 0, 0] = 0.0  # sample 0 flies the nominal exactly
+    x = state((0.0, 0.0, 2.0), v=(2.0, 0.0, 0.0))
+    far = np.array([[60.0, 40.0, 2.0]])
+    _, o = run_case(oracle, cfg, far, x, x, goal_target=(20, 0, 2), cycle=0, seed=1, injected=inj)
+    assert o["ess"][0] < 1.001  # sample 0 carries the whole softmin weight
+    return cfg, inj, x, far, o["winner_states"]
+
+
+@pytest.mark.parametrize("step", [8, 17])
+def test_best_sample_grazes_d_max(oracle, step):
+    cfg, inj, x, far, traj = _scenario(oracle)
+    dmax = cfg.weights.collision.d_max
+    p = traj[step, 0:3]
+    for eps in (-3e-7, -1e-7, -3e-8, 0.0, 3e-8, 1e-7, 2e-7, 3e-7):
+        q = p + np.array([0.0, 1.0, 0.0]) * dmax * (1.0 + eps)
+        # every other step of sample 0 stays clear of the point
+        d = np.linalg.norm(traj[:, 0:3] - q, axis=1)
+        assert np.all(np.delete(d, step) > dmax * (1 + 1e-6))
+        run_case(oracle, cfg, np.vstack([q, far]), x, x, goal_target=(20, 0, 2), cycle=0, seed=1, injected=inj)
