@@ -119,7 +119,8 @@ typedef struct {
   double* anchor_safe_range;   /* [M] */
   int32_t* anchor_ij;          /* [M*2] coarse (I, J) */
   double* guide_coeffs;        /* [M*3*6] GuidingTrajectory::coeffs, [m][axis][power] */
-  double* sample_costs;        /* [M*K] stage-I cost of every sample, last iteration (verification) */
+  double* sample_costs;        /* [M*K] stage-I screening cost of every sample, last iteration (verification);
+                                  a sample with a clearance within the d_max band reports a lower bound */
 } amppi_plan_result;
 
 /* Snapshot contents for verification (SphericalPartition / CoarsePartition /

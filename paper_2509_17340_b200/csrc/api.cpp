@@ -833,7 +833,7 @@ int collect_plan_result(amppi_ctx* ctx, amppi_plan_result* out, bool want_states
   const int status = r.status[0];
   if (out) {
     if (!c32.empty())
-      for (size_t i = 0; i < c32.size(); ++i) out->sample_costs[i] = c32[i];
+      for (size_t i = 0; i < c32.size(); ++i) out->sample_costs[i] = std::fabs(c32[i]);  // flagged: a lower bound
     out->winner = r.winner[0];
     if (status == 0) {
       out->control.thrust = r.control[0];

@@ -22,7 +22,7 @@ namespace amppi_dev {
 // [4] points scanned, [5]/[6] queries ending with / without a point within
 // reach, [7] points scanned by queries without one; [8 + j] live screening
 // lanes at step j.
-constexpr int kStatSlots = 8 + 64;
+constexpr int kStatSlots = 8 + 64 + 8;  // query counters, live samples by step, d_max band
 __device__ unsigned long long g_query_stats[kStatSlots];
 #define AMPPI_STAT(i, v) atomicAdd(&g_query_stats[i], static_cast<unsigned long long>(v))
 #else
@@ -337,6 +337,33 @@ __device__ __forceinline__ R collision_term(R d, R scale, R slope, R dmin, R dma
   }
   return R(0);
 }
+
+// FP32 screening collision term with the d_max jump guarded.  The term
+// falls from C exp(-a (d_max - d_min)) (~5e4 with the paper's weights) to 0
+// at d_max, so a screening distance on the other side of d_max than the
+// FP64 one would move the sample's FP32 cost far outside the softmin window.
+// Within kAmbBand of d_max the screening adds 0 -- a lower bound of either
+// branch -- and flags the sample (*amb): its screening cost is then a lower
+// bound, k_support admits it by that bound and leaves it out of the FP32
+// minimum.  The band covers the FP32 distance error
+// (coordinates and RK4 in float) with a wide margin; queries reach
+// d_max + band so a point just past d_max is seen.
+__device__ __forceinline__ float amb_band(float dmax) { return 1e-4f * dmax + 1e-4f; }
+__device__ __forceinline__ float screen_reach2(float dmax) {
+  const float r = dmax + amb_band(dmax);
+  return r * r * 1.0001f;
+}
+__device__ __forceinline__ float screen_collision(float d2, float cs, float ca, float dmin, float dmax, bool& amb) {
+  const float d = sqrtf(d2);
+  if (fabsf(d - dmax) < amb_band(dmax)) {
+    AMPPI_STAT(72, 1);
+    amb = true;
+    return 0.f;
+  }
+  return collision_term(d, cs, ca, dmin, dmax);
+}
+// Stored screening cost: a flagged (lower-bound) cost carries the sign bit.
+__device__ __forceinline__ float screen_store(float cost, bool amb) { return amb ? -cost : cost; }
 
 // Collision-grid queries (replacing ClearanceIndex::nearest,
 // perception.cpp:191-235).  The squared distance to the nearest filtered point

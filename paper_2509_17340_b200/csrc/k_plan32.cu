@@ -52,7 +52,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   if (threadIdx.x < 32) {
     float u = __int_as_float(0x7f800000);
     if (mode == 2)
-      for (int k = cfg.k_lo + threadIdx.x; k < cfg.k_lo + k1; k += 32) u = fminf(u, pl.cost32[smi * cfg.K + k]);
+      for (int k = cfg.k_lo + threadIdx.x; k < cfg.k_lo + k1; k += 32) {
+        const float c = pl.cost32[smi * cfg.K + k];
+        if (!signbit(c)) u = fminf(u, c);  // U is an unflagged sample's cost
+      }
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (threadIdx.x == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
     cs = rollout_costs(x0, env, pr);
   }
   *out = cs.aborted ? 3.4028234663852886e38f
-                    : cs.valid ? stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd)
+                    : cs.valid ? screen_store(stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd), cs.amb)
                                : __int_as_float(0x7f800000);
 }
 
@@ -158,13 +161,13 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   // Abort radius: a point closer than d_thr adds more than the remaining
   // budget (C exp(-a (d_thr - d_min)) = budget e^0.001), so finding one ends
   // the sample; otherwise the query returns the exact distance (>= d_thr).
-  const float lim2 = env.cdmax * env.cdmax * 1.0001f;
+  const float lim2 = screen_reach2(env.cdmax);
   float stop2 = env.cdmin * env.cdmin;
   bool abortable = false;
   const float budget = env.abort_above - part;
   if (budget < env.cs) {
     float d_thr = env.cdmin + (__logf(env.cs / budget) - 1e-3f) / env.ca;
-    d_thr = fminf(d_thr, env.cdmax * 0.9999995f);  // d2 < d_thr^2 => sqrtf(d2) < d_max
+    d_thr = fminf(d_thr, (env.cdmax - amb_band(env.cdmax)) * 0.9999995f);  // d < d_thr: a counted term
     if (d_thr > env.cdmin) {
       stop2 = d_thr * d_thr;
       abortable = true;
@@ -175,7 +178,7 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
                           : nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, lim2, stop2,
                                             &env.hint);
   if (abortable && d2 < stop2) return 1;
-  s.col = s.col + collision_term(sqrtf(d2), env.cs, env.ca, env.cdmin, env.cdmax);
+  s.col = s.col + screen_collision(d2, env.cs, env.ca, env.cdmin, env.cdmax, s.amb);
   if (((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col) >
       env.abort_above)
     return 1;
@@ -202,7 +205,7 @@ constexpr int kScreenThreads = 128;
 #endif
 constexpr int kMainThreads = AMPPI_MAIN_THREADS, kMainMinBlocks = AMPPI_MAIN_MINBLOCKS;
 constexpr int kMainCompact = AMPPI_MAIN_COMPACT;
-constexpr int kStateWords = 21;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint
+constexpr int kStateWords = 22;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint amb
 
 // Samples [k_lo + kb0, k_lo + kend) of every instance, aborted against the
 // minimum of samples [k_lo, k_lo + nb) (main pass: kb0 = nb = 32; bound
@@ -238,7 +241,8 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   for (int i = tid; i < N; i += kT) s_guide[i] = pl.guide32[smi * N + i];
   if (tid < 32) {
     float u = __int_as_float(0x7f800000);
-    for (int k = cfg.k_lo + tid; k < cfg.k_lo + nb; k += 32) u = fminf(u, out[k]);
+    for (int k = cfg.k_lo + tid; k < cfg.k_lo + nb; k += 32)
+      if (!signbit(out[k])) u = fminf(u, out[k]);  // U is an unflagged sample's cost
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (tid == 0) {
       const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
@@ -287,14 +291,14 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   x.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
   x.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
   x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
-  CostSums<float> cs{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, true, false};
+  CostSums<float> cs{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, true, false, false};
   float up[4] = {0.f, 0.f, 0.f, 0.f};
   {  // the step-0 collision query (exact; every sample starts at x0)
     __shared__ float s_d2;
     __shared__ uint32_t s_hint;
     if (tid == 0) {
       uint32_t h = kNoHint;
-      s_d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.cdmax * env.cdmax * 1.0001f,
+      s_d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, screen_reach2(env.cdmax),
                              env.cdmin * env.cdmin, &h);
       s_hint = h;
     }
@@ -377,6 +381,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         st[16 * kT] = up[0]; st[17 * kT] = up[1]; st[18 * kT] = up[2];
         st[19 * kT] = up[3];
         st[20 * kT] = __uint_as_float(env.hint);
+        st[21 * kT] = cs.amb ? 1.f : 0.f;
         s_k[slot] = k;
       }
       __syncthreads();
@@ -391,13 +396,18 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         up[0] = st[16 * kT]; up[1] = st[17 * kT]; up[2] = st[18 * kT];
         up[3] = st[19 * kT];
         env.hint = __float_as_uint(st[20 * kT]);
+        cs.amb = st[21 * kT] != 0.f;
         k = s_k[tid];
         pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
       }
       __syncthreads();
     }
   }
-  if (live) out[k] = stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd);
+  if (live) {
+    AMPPI_STAT(73, cs.amb ? 1 : 0);
+    AMPPI_STAT(74, 1);
+    out[k] = screen_store(stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd), cs.amb);
+  }
 }
 
 // Latency path (few rollouts), one warp per rollout: the draws, clamps and
@@ -537,6 +547,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn i
   const float cs = static_cast<float>(cfg.col_scale), ca = static_cast<float>(cfg.col_slope);
   const float dmin = static_cast<float>(cfg.col_d_min), dmax = static_cast<float>(cfg.col_d_max);
   const float4* guide = pl.guide32 + smi * N;
+  bool amb = false;
   for (int j = lane; j < n_ok; j += 32) {
     const float* o = sx + 10 * j;
     const V3<float> p{o[0], o[1], o[2]}, v{o[7], o[8], o[9]};
@@ -548,9 +559,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn i
     st[3 * N + j] = static_cast<float>(cfg.q_v) * norm3(v - vg);
     st[4 * N + j] = static_cast<float>(cfg.q_q) * attitude_err_fast(q, qg);
     uint32_t hint = kNoHint;
-    const float d2 = nearest_sq_fast(g, grec, gnbr, gleaf, gpts, p, dmax * dmax * 1.0001f, dmin * dmin, &hint);
-    st[7 * N + j] = collision_term(sqrtf(d2), cs, ca, dmin, dmax);
+    const float d2 = nearest_sq_fast(g, grec, gnbr, gleaf, gpts, p, screen_reach2(dmax), dmin * dmin, &hint);
+    st[7 * N + j] = screen_collision(d2, cs, ca, dmin, dmax, amb);
   }
+  amb = __any_sync(0xffffffffu, amb);
   __syncwarp();
   if (lane == 0) {
     float trk = 0.f, vn = 0.f, goal = 0.f, mag = 0.f, rate = 0.f, col = 0.f;
@@ -568,7 +580,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn i
     }
     const float wt = static_cast<float>(cfg.q_track), wv = static_cast<float>(cfg.q_vnorm);
     const float wc = static_cast<float>(cfg.q_c), wd = static_cast<float>(cfg.q_c_delta);
-    *out = n_ok == N ? ((wt * trk + wv * vn) + (wc * mag + wd * rate)) + (goal + col) : __int_as_float(0x7f800000);
+    *out = n_ok == N ? screen_store(((wt * trk + wv * vn) + (wc * mag + wd * rate)) + (goal + col), amb)
+                     : __int_as_float(0x7f800000);
   }
 }
 

@@ -345,7 +345,11 @@ struct UpdateScratch {  // global, per (scene, instance): [K] each
 };
 
 __device__ __forceinline__ double load_cost(const Plan& pl, int precision, int64_t i) {
-  return precision == 32 ? static_cast<double>(pl.cost32[i]) : pl.cost64[i];
+  return precision == 32 ? static_cast<double>(fabsf(pl.cost32[i])) : pl.cost64[i];
+}
+// FP32 screening cost flagged as a lower bound (d_max band, screen_collision)
+__device__ __forceinline__ bool cost_flagged(const Plan& pl, int precision, int64_t i) {
+  return precision == 32 && signbit(pl.cost32[i]);
 }
 
 // Softmin support of each instance over samples [k_lo, k_hi): every sample
@@ -369,18 +373,29 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
   if (rho_ext) {
     if (tid == 0) s_rho = static_cast<double>(rho_ext[smi]);
   } else {
+    // rho over the unflagged costs; flagged ones only bound their sample from
+    // below.  With finite costs that are all flagged, every one is admitted
+    // (rho = -FLT_MAX, "admit all").
     double lmin = kInf;
+    bool any_flagged = false;
     for (int k = k_lo + tid; k < cfg.k_hi; k += blockDim.x) {
       const double c = load_cost(pl, precision, base + k);
-      if (isfinite(c)) lmin = fmin(lmin, c);
+      if (!isfinite(c)) continue;
+      if (cost_flagged(pl, precision, base + k)) any_flagged = true;
+      else lmin = fmin(lmin, c);
     }
     for (int o = 16; o > 0; o >>= 1) lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
-    if (lane == 0) s_red[warp] = lmin;
+    any_flagged = __any_sync(0xffffffffu, any_flagged);
+    if (lane == 0) s_red[warp] = any_flagged && !isfinite(lmin) ? -1.0 : lmin;
     __syncthreads();
     if (tid == 0) {
       double r = kInf;
-      for (int w = 0; w < kSupportThreads / 32; ++w) r = fmin(r, s_red[w]);
-      s_rho = r;
+      bool flagged_only = false;
+      for (int w = 0; w < kSupportThreads / 32; ++w) {
+        if (s_red[w] == -1.0) flagged_only = true;
+        else r = fmin(r, s_red[w]);
+      }
+      s_rho = (!isfinite(r) && flagged_only) ? -3.4028234663852886e38 : r;
     }
   }
   __syncthreads();
@@ -392,13 +407,14 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
     }
     return;
   }
+  const bool admit_all = rho_s <= -3.0e38;
   const double window = precision == 32 ? 64.0 * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
   const int per = (kr + blockDim.x - 1) / blockDim.x;
   const int k0 = k_lo + min(tid * per, kr), k1 = min(k0 + per, cfg.k_hi);
   uint32_t mine = 0;
   for (int k = k0; k < k1; ++k) {
     const double c = load_cost(pl, precision, base + k);
-    mine += (isfinite(c) && c - rho_s <= window);
+    mine += (isfinite(c) && (admit_all || c - rho_s <= window));
   }
   uint32_t x = mine;
   for (int o = 1; o < 32; o <<= 1) {
@@ -424,7 +440,7 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
   uint32_t pos = s_cnt[warp] + x - mine;
   for (int k = k0; k < k1; ++k) {
     const double c = load_cost(pl, precision, base + k);
-    if (isfinite(c) && c - rho_s <= window) {
+    if (isfinite(c) && (admit_all || c - rho_s <= window)) {
       us.cand_k[base + pos] = static_cast<uint32_t>(k);
       us.cand_s[base + pos] = c;
       ++pos;
@@ -545,15 +561,22 @@ __global__ void __launch_bounds__(128) k_nominal(BatchIn in, Plan pl, DevConfig 
 // sum e_k * applied_k[jc] (mppi.cpp:70-101 split by shard).
 // ---------------------------------------------------------------------------
 __global__ void k_local_min(Plan pl, DevConfig cfg, float* out) {
+  // minimum over the unflagged screening costs; a shard whose finite costs
+  // are all flagged reports -FLT_MAX, so the global minimum admits every
+  // flagged sample (k_support "admit all")
   const int64_t smi = blockIdx.x;
   float v = __int_as_float(0x7f800000);
+  bool flagged = false;
   if (pl.alive[smi])
     for (int k = cfg.k_lo + threadIdx.x; k < cfg.k_hi; k += blockDim.x) {
       const float c = pl.cost32[smi * cfg.K + k];
-      if (isfinite(c)) v = fminf(v, c);
+      if (!isfinite(c)) continue;
+      if (signbit(c)) flagged = true;
+      else v = fminf(v, c);
     }
   for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if (threadIdx.x == 0) out[smi] = v;
+  flagged = __any_sync(0xffffffffu, flagged);
+  if (threadIdx.x == 0) out[smi] = (flagged && !isfinite(v)) ? -3.4028234663852886e38f : v;
 }
 
 __global__ void __launch_bounds__(128) k_partials(BatchIn in, Plan pl, DevConfig cfg, UpdateScratch us, int iter,

@@ -18,6 +18,7 @@ struct CostSums {
   R trk, vn, mag, rate, goal, col;
   bool valid;
   bool aborted;  // partial stage-I cost passed RolloutEnv::abort_above (FP32 screening only)
+  bool amb;      // a step's FP32 distance fell within amb_band of d_max (FP32 screening only)
 };
 
 // Read-only per-(scene, instance) environment of a rollout.
@@ -81,9 +82,9 @@ struct RolloutEnv<float> {
   }
   __device__ __forceinline__ float unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ float attitude(Q4<float> q) const { return attitude_err_fast(q, qg); }
-  __device__ __forceinline__ float collision(V3<float> p) const {
-    const float d2 = nearest_sq_fast(grid, grec, gnbr, gleaf, gpts, p, cdmax * cdmax * 1.0001f, cdmin * cdmin, &hint);
-    return collision_term(sqrtf(d2), cs, ca, cdmin, cdmax);
+  __device__ __forceinline__ float collision(V3<float> p, bool& amb) const {
+    const float d2 = nearest_sq_fast(grid, grec, gnbr, gleaf, gpts, p, screen_reach2(cdmax), cdmin * cdmin, &hint);
+    return screen_collision(d2, cs, ca, cdmin, cdmax, amb);
   }
 };
 
@@ -141,7 +142,7 @@ template <typename R, typename Pert, bool kDeferCol = false>
 __device__ __forceinline__ CostSums<R> rollout_costs(St<R> x, const RolloutEnv<R>& env, const Pert& pert,
                                                       R* states_out = nullptr, R* controls_out = nullptr,
                                                       R* pos_out = nullptr) {
-  CostSums<R> s{R(0), R(0), R(0), R(0), R(0), R(0), true, false};
+  CostSums<R> s{R(0), R(0), R(0), R(0), R(0), R(0), true, false, false};
   const Dyn<R>& dy = env.dyn;
   R up0 = R(0), up1 = R(0), up2 = R(0), up3 = R(0);
   const int N = env.N;
@@ -166,7 +167,8 @@ __device__ __forceinline__ CostSums<R> rollout_costs(St<R> x, const RolloutEnv<R
       pos_out[4 * j + 1] = x.p.y;
       pos_out[4 * j + 2] = x.p.z;
     } else {
-      s.col = s.col + env.collision(x.p);
+      if constexpr (std::is_same_v<R, float>) s.col = s.col + env.collision(x.p, s.amb);
+      else s.col = s.col + env.collision(x.p);
     }
     // perturbed, clamped control (mppi.cpp:40-45)
     R d[4];

@@ -121,7 +121,10 @@ def run_case(oracle, cfg, pts, pose, x, goal_target=None, goal=None, previous=No
         assert np.all((osc > rho + 64 * cfg.mppi.lambda_)[aborted]), "an aborted sample was in the support"
     fin = np.isfinite(osc) & ~aborted
     assert np.array_equal(np.isfinite(sc) & ~aborted, fin)
-    ok = fin & (margin > 1e-4)
+    # samples whose clearance comes within the d_max band are flagged by the
+    # screening and report a lower bound (device_math.cuh screen_collision)
+    ok = fin & (margin > 1e-3)
+    assert np.all(sc[fin] <= osc[fin] * (1 + 1e-4) + 1e-2)
     tol = 1e-4 if precision == 32 else 1e-11
     assert rel(sc[ok], osc[ok]) <= tol
     return r, o

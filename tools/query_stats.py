@@ -11,7 +11,7 @@ from paper_2509_17340_b200.workloads import plan_config, scenes  # noqa: E402
 
 lib = load()
 lib.amppi_query_stats.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-SLOTS = 8 + 64
+SLOTS = 8 + 64 + 8
 cfg = plan_config()
 out = {}
 for kind in (1, 2, 3):
@@ -28,6 +28,7 @@ for kind in (1, 2, 3):
         "points_per_scanned_cell": st[4] / max(st[3], 1),
         "hit_queries": st[5] / q, "scanned_miss_queries": st[6] / q,
         "points_per_hit_query": (st[4] - st[7]) / max(st[5], 1), "points_per_miss_query": st[7] / max(st[6], 1),
+        "d_max_band_steps_per_query": st[72] / q, "main_pass_flagged_of_completed": st[73] / max(st[74], 1),
         "main_pass_live_fraction_by_step": [round(st[8 + j] / max(st[8], 1), 3) for j in range(cfg.mppi.horizon)]}
     p.close()
 print(json.dumps(out, indent=1))
