@@ -399,6 +399,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     vals[k] = static_cast<uint16_t>(k);
   }
   __syncthreads();
+  // Stages with stride <= 32 keep every warp inside its own 64-key windows
+  // (pair t -> keys 2t - t % stride, + stride; warp w owns keys [64w, 64w+64)
+  // of each 32-pair block), so consecutive such stages need only a warp
+  // barrier; a block barrier is needed when a stage reaches across windows.
   for (uint32_t size = 2; size <= n2; size <<= 1)
     for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
       for (uint32_t t = tid; t < (n2 >> 1); t += blockDim.x) {
@@ -414,7 +418,11 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
           vals[j] = v;
         }
       }
-      __syncthreads();
+      const uint32_t next = stride > 1 ? stride >> 1 : size;  // the next stage's stride
+      if (stride > 32 || next > 32)
+        __syncthreads();
+      else
+        __syncwarp();
     }
   SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
