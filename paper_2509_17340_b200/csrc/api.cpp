@@ -499,6 +499,36 @@ Plan shift_plan(const Plan& p, int64_t s0, const DevConfig& c) {
 
 // Perception arrays of scenes [s0, ...) (the candidate log is indexed by
 // absolute point and needs no shift).
+// Compute streams that pipelined chunks rotate over (AMPPI_PIPELINE_STREAMS,
+// 2..4, default 3: best measured with tools/pipe_sweep.py).
+int pipeline_streams() {
+  static const int n = [] {
+    const char* f = std::getenv("AMPPI_PIPELINE_STREAMS");
+    return f ? std::max(2, std::min(2 + kExtraStreams, std::atoi(f))) : 3;
+  }();
+  return n;
+}
+
+cudaStream_t compute_stream(amppi_ctx* ctx, int c) {
+  const int i = c % pipeline_streams();
+  return i == 0 ? ctx->stream : (i == 1 ? ctx->stream2 : ctx->xstream[i - 2]);
+}
+
+// Fork the compute streams off ctx->stream / join them back into it.
+int fork_streams(amppi_ctx* ctx) {
+  CK(cudaEventRecord(ctx->join[0], ctx->stream));
+  for (int i = 1; i < pipeline_streams(); ++i) CK(cudaStreamWaitEvent(compute_stream(ctx, i), ctx->join[0], 0));
+  return AMPPI_OK;
+}
+
+int join_streams(amppi_ctx* ctx) {
+  for (int i = 1; i < pipeline_streams(); ++i) {
+    CK(cudaEventRecord(ctx->join[i], compute_stream(ctx, i)));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->join[i], 0));
+  }
+  return AMPPI_OK;
+}
+
 Perception shift_perception(const Perception& p, int64_t s0) {
   Perception q = p;
   q.cell_r += s0 * kCells;
@@ -1010,18 +1040,8 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   // own offset), so one chunk's latency-bound tail overlaps the next chunks'
   // work; every stream joins ctx->stream before the gather
   const bool concurrent = chunks > 1;
-  static const int n_streams = [] {
-    const char* f = std::getenv("AMPPI_PIPELINE_STREAMS");
-    return f ? std::max(2, std::min(2 + kExtraStreams, std::atoi(f))) : 3;  // 3: best of 2-4 (tools/pipe_sweep.py)
-  }();
-  auto cstream = [&](int c) {
-    const int i = c % n_streams;
-    return i == 0 ? ctx->stream : (i == 1 ? ctx->stream2 : ctx->xstream[i - 2]);
-  };
-  if (concurrent) {
-    CK(cudaEventRecord(ctx->join[0], ctx->stream));
-    for (int i = 1; i < n_streams; ++i) CK(cudaStreamWaitEvent(cstream(i), ctx->join[0], 0));
-  }
+  if (concurrent)
+    if (int rc = fork_streams(ctx); rc != AMPPI_OK) return rc;
   // Chunk sizes grow geometrically: the first chunk's upload is the only one
   // not hidden behind planning, so it is the smallest; later chunks grow so
   // their uploads stay ahead of the planning.
@@ -1042,7 +1062,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
                          cudaMemcpyHostToDevice, ctx->copy_stream));
     CK(cudaEventRecord(ctx->chunk_ready[c], ctx->copy_stream));
     tmark(ctx->copy_stream);
-    const cudaStream_t cst = concurrent ? cstream(c) : ctx->stream;
+    const cudaStream_t cst = concurrent ? compute_stream(ctx, c) : ctx->stream;
     CK(cudaStreamWaitEvent(cst, ctx->chunk_ready[c], 0));
     int64_t max_chunk_scene = 0;
     for (int s = s0; s < s1; ++s)
@@ -1065,10 +1085,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     tmark(cst);
   }
   if (concurrent)
-    for (int i = 1; i < n_streams; ++i) {
-      CK(cudaEventRecord(ctx->join[i], cstream(i)));
-      CK(cudaStreamWaitEvent(ctx->stream, ctx->join[i], 0));
-    }
+    if (int rc = join_streams(ctx); rc != AMPPI_OK) return rc;
   if (trace) {
     cudaDeviceSynchronize();
     std::fprintf(stderr, "pipeline %d chunks:", chunks);
@@ -1107,15 +1124,19 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
   // context's capacity (blocks beyond a scene's end exit immediately)
   const int64_t max_scene = std::max<int64_t>(1, ctx->P_cap / S);
   if (ctx->P.cand_cap < ctx->P_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point capacity");
-  int chunks = 1;
+  // Device-resident inputs need no upload pipeline, but a few chunks on the
+  // compute streams still overlap one chunk's latency-bound tail kernels with
+  // the others' work (C5: 3 chunks 18.9 ms, 2 chunks 19.0, 1 chunk 19.3,
+  // 4 chunks 20.9).
+  int chunks = std::min(pipeline_streams(), S / (2 * 148));
+  chunks = std::max(1, std::min(chunks, 3));
   if (const char* f = std::getenv("AMPPI_DEVICE_CHUNKS")) chunks = std::max(1, std::min(kMaxChunks, std::atoi(f)));
   if (chunks > 1 && S / chunks < 148) chunks = 1;
   if (chunks == 1) {
     if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
     return batch_outputs_gather(ctx, S, out, true);
   }
-  CK(cudaEventRecord(ctx->join[0], ctx->stream));
-  CK(cudaStreamWaitEvent(ctx->stream2, ctx->join[0], 0));
+  if (int rc = fork_streams(ctx); rc != AMPPI_OK) return rc;
   for (int c = 0; c < chunks; ++c) {
     const int s0 = static_cast<int>(static_cast<int64_t>(S) * c / chunks);
     const int s1 = static_cast<int>(static_cast<int64_t>(S) * (c + 1) / chunks);
@@ -1130,11 +1151,9 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
     cb.last_applied += 4 * s0;
     cb.cycles += s0;
     cb.seeds += s0;
-    if (int rc = run_chunk(ctx, cb, max_scene, s0, c, (c & 1) ? ctx->stream2 : ctx->stream); rc != AMPPI_OK)
-      return rc;
+    if (int rc = run_chunk(ctx, cb, max_scene, s0, c, compute_stream(ctx, c)); rc != AMPPI_OK) return rc;
   }
-  CK(cudaEventRecord(ctx->join[1], ctx->stream2));
-  CK(cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
+  if (int rc = join_streams(ctx); rc != AMPPI_OK) return rc;
   return batch_outputs_gather(ctx, S, out, true);
 }
 
