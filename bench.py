@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "rollout-steps/s (anchors×samples×horizon); p50 plan-cycle latency ms"
 FLOPS_PER_STEP = 440  # algorithmic FP32 flops per rollout-step (FMA = 2)
-TRAFFIC_BYTES_PER_LAUNCH = 232.3e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
+TRAFFIC_BYTES_PER_LAUNCH = 235.0e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
 
 
 def parse():
@@ -286,6 +286,23 @@ def run_b200(args):
     value = total_steps / (ms_max / 1e3)
     n_ok = int((dout["status"] == 0).sum().item())
     launches = sum(v[1] for v in ktimes.values())
+    # Per-kernel times for the roofline and the `kernels` table: a short extra
+    # pass with the whole batch as one chunk.  (The timed steps above split it
+    # into chunks on concurrent streams, where a kernel's events also span the
+    # other streams' kernels.)
+    prev_chunks = os.environ.get("AMPPI_DEVICE_CHUNKS")
+    os.environ["AMPPI_DEVICE_CHUNKS"] = "1"
+    step()
+    torch.cuda.synchronize(dev)
+    planner.kernel_times_reset()
+    for _ in range(min(args.steps, 5)):
+        step()
+    planner.synchronize()
+    ktimes = planner.kernel_times()
+    if prev_chunks is None:
+        del os.environ["AMPPI_DEVICE_CHUNKS"]
+    else:
+        os.environ["AMPPI_DEVICE_CHUNKS"] = prev_chunks
 
     # roofline of the dominant kernel (FP32 stage-I rollouts)
     lib = load()
