@@ -408,6 +408,8 @@ int create_impl(amppi_ctx* ctx) {
   pl.guide64 = static_cast<double*>(p);
   CK(A.alloc(&p, SM * N * sizeof(float4)));
   pl.guide32 = static_cast<float4*>(p);
+  CK(A.alloc(&p, SM * N * sizeof(float4)));
+  pl.unom32 = static_cast<float4*>(p);
   CK(A.alloc(&p, SM * K * sizeof(float)));
   pl.cost32 = static_cast<float*>(p);
   CK(A.alloc(&p, SM * K * sizeof(double)));
@@ -478,6 +480,7 @@ Plan shift_plan(const Plan& p, int64_t s0, const DevConfig& c) {
   q.guide_coef += sm * 18;
   q.guide64 += sm * c.N * 3;
   q.guide32 += sm * c.N;
+  q.unom32 += sm * c.N;
   q.nominal += sm * c.N * 4;
   q.cost32 += sm * c.K;
   q.cost64 += sm * c.K;

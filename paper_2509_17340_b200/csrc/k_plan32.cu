@@ -24,6 +24,16 @@ namespace {
 
 constexpr int kMaxN = 64;
 
+// The current nominal in float (one thread per instance step), the table the
+// screening kernels bulk-copy into shared memory.
+__global__ void k_unom32(Plan pl, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* u = pl.nominal + 4 * i;
+  pl.unom32[i] = make_float4(static_cast<float>(u[0]), static_cast<float>(u[1]), static_cast<float>(u[2]),
+                             static_cast<float>(u[3]));
+}
+
 // mode 0: every sample, no bound.  mode 1: samples [0, k1) without bound.
 // mode 2: samples [k1, K) aborted once their partial cost exceeds
 // U + window(U), U = min cost of samples [0, k1) -- an actual sample cost,
@@ -34,9 +44,10 @@ constexpr int kMaxN = 64;
 template <int kMinBlocks>
 __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perception P, Plan pl, DevConfig cfg,
                                                                 int iter, int mode, int k1) {
-  __shared__ float s_unom[4 * kMaxN];
+  __shared__ float4 s_unom[kMaxN];
   __shared__ float4 s_guide[kMaxN];
   __shared__ float s_bound;
+  __shared__ uint64_t s_bar;
   const int k_lo = mode == 2 ? cfg.k_lo + k1 : cfg.k_lo;
   const int k_n = mode == 0 ? cfg.k_hi - cfg.k_lo : (mode == 1 ? k1 : cfg.k_hi - cfg.k_lo - k1);
   const int tiles = (k_n + blockDim.x - 1) / blockDim.x;
@@ -47,8 +58,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   const int s = b / cfg.M;
   const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
   const int N = cfg.N;
-  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) s_guide[i] = pl.guide32[smi * N + i];
+  if (threadIdx.x == 0) {  // the instance's nominal and guide tables: bulk async copies into smem
+    mbar_init(&s_bar, 1);
+    mbar_expect_tx(&s_bar, 2u * 16u * static_cast<uint32_t>(N));
+    bulk_copy_g2s(s_unom, pl.unom32 + smi * N, 16u * N, &s_bar);
+    bulk_copy_g2s(s_guide, pl.guide32 + smi * N, 16u * N, &s_bar);
+  }
   if (threadIdx.x < 32) {
     float u = __int_as_float(0x7f800000);
     if (mode == 2)
@@ -64,6 +79,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
     }
   }
   __syncthreads();
+  mbar_wait(&s_bar, 0);
   const int k = k_lo + tile * blockDim.x + threadIdx.x;
   if (k >= k_lo + k_n) return;
   float* out = pl.cost32 + smi * cfg.K + k;
@@ -72,7 +88,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
     return;
   }
   RolloutEnv<float> env;
-  env.unom = s_unom;
+  env.unom = reinterpret_cast<const float*>(s_unom);
   env.guide = s_guide;
   env.N = N;
   env.dyn = make_dyn<float>(cfg);
@@ -213,9 +229,10 @@ constexpr int kStateWords = 22;  // p(3) q(4) v(3) trk vn mag rate goal col up(4
 template <int kMinBlocks, int kCompact, int kT = kScreenThreads>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     k_stage1_f32c(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter, int kb0, int kend, int nb) {
-  __shared__ float s_unom[4 * kMaxN];
+  __shared__ float4 s_unom[kMaxN];
   __shared__ float4 s_guide[kMaxN];
   __shared__ float s_bound;
+  __shared__ uint64_t s_bar;
   __shared__ float s_state[kStateWords][kT];
   __shared__ int s_k[kT];
   __shared__ int s_wcount[2][kT / 32];
@@ -237,8 +254,12 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     if (k < cfg.k_lo + kend) out[k] = __int_as_float(0x7f800000);
     return;
   }
-  for (int i = tid; i < 4 * N; i += kT) s_unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);
-  for (int i = tid; i < N; i += kT) s_guide[i] = pl.guide32[smi * N + i];
+  if (tid == 0) {  // the instance's nominal and guide tables: bulk async copies into smem
+    mbar_init(&s_bar, 1);
+    mbar_expect_tx(&s_bar, 2u * 16u * static_cast<uint32_t>(N));
+    bulk_copy_g2s(s_unom, pl.unom32 + smi * N, 16u * N, &s_bar);
+    bulk_copy_g2s(s_guide, pl.guide32 + smi * N, 16u * N, &s_bar);
+  }
   if (tid < 32) {
     float u = __int_as_float(0x7f800000);
     for (int k = cfg.k_lo + tid; k < cfg.k_lo + nb; k += 32)
@@ -251,8 +272,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     }
   }
   __syncthreads();
+  mbar_wait(&s_bar, 0);
   RolloutEnv<float> env;
-  env.unom = s_unom;
+  env.unom = reinterpret_cast<const float*>(s_unom);
   env.guide = s_guide;
   env.N = N;
   env.dyn = make_dyn<float>(cfg);
@@ -595,6 +617,10 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   // throughput mode: 64 registers (8 CTAs = 32 warps per SM, a few bytes of
   // L1-resident spill); latency mode: no cap (fastest single rollout)
   auto kern = k_stage1_f32<8>;
+  auto unom32 = [&] {  // float nominal table for the bulk smem copies of k_stage1_f32 / k_stage1_f32c
+    const int64_t n = SM * cfg.N;
+    k_unom32<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pl, n);
+  };
   if (total < 148 * 128 * 4 || kr <= 64) {
     // latency mode (few rollouts): one pass, warps spread over the SMs
     const int threads = total < 148 * 128 ? 32 : 128;
@@ -605,10 +631,12 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
                         st>>>(in, P, pl, cfg, iter);
       return cudaGetLastError();
     }
+    unom32();
     TimedRegion t(timer, "k_stage1_f32", st);
     kern<<<static_cast<unsigned>(SM * tiles), threads, 0, st>>>(in, P, pl, cfg, iter, 0, 0);
     return cudaGetLastError();
   }
+  unom32();
   const int k1 = 32;  // bound samples (best of 8-64 measured)
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);

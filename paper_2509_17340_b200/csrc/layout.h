@@ -132,6 +132,7 @@ struct Plan {
   double* guide64;             // [S*M*N*3]
   float4* guide32;             // [S*M*N]
   double* nominal;             // [S*M*N*4] current nominal (FP64 always)
+  float4* unom32;              // [S*M*N] the nominal in float for the screening kernels (bulk-copied to smem)
   // stage I
   float* cost32;               // [S*M*K]
   double* cost64;              // [S*M*K]
