@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
       }
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (threadIdx.x == 0) {
-      const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
+      const float window = static_cast<float>(kWindowLambdas * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
       // + 1e-6 |u| covers the float rounding of the threshold itself
       s_bound = (mode == 2 && u < 3.0e38f) ? u + window + (1e-6f * fabsf(u) + 1e-5f) : __int_as_float(0x7f800000);
     }
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       if (!signbit(out[k])) u = fminf(u, out[k]);  // U is an unflagged sample's cost
     for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
     if (tid == 0) {
-      const float window = static_cast<float>(64.0 * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
+      const float window = static_cast<float>(kWindowLambdas * cfg.lambda) + 1e-4f * fabsf(u) + 1e-2f;
       // + 1e-6 |u| covers the float rounding of the threshold itself
       s_bound = u < 3.0e38f ? u + window + (1e-6f * fabsf(u) + 1e-5f) : __int_as_float(0x7f800000);
     }

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(kSupportThreads) k_support(Plan pl, DevConfig 
     return;
   }
   const bool admit_all = rho_s <= -3.0e38;
-  const double window = precision == 32 ? 64.0 * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
+  const double window = precision == 32 ? kWindowLambdas * cfg.lambda + 1e-4 * fabs(rho_s) + 1e-2 : 746.0 * cfg.lambda;
   const int per = (kr + blockDim.x - 1) / blockDim.x;
   const int k0 = k_lo + min(tid * per, kr), k1 = min(k0 + per, cfg.k_hi);
   uint32_t mine = 0;

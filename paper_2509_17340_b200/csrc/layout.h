@@ -26,6 +26,12 @@ constexpr double kHorizonReach = 25.0;
 // {lo.x, hi.x, lo.y, hi.y}, {lo.z, hi.z, -, -} in float (outward-rounded).  The padded lattice (dims+2)^3 holds, per cell, the
 // 27-bit mask of its non-empty neighbours (bit i*9+j*3+k <-> offset
 // (i-1, j-1, k-1)); mask 0 = no point within one cell.
+#ifndef AMPPI_WINDOW_LAMBDAS
+#define AMPPI_WINDOW_LAMBDAS 64.0
+#endif
+// Softmin support window of the FP32 screening, in units of lambda (plus the
+// FP32 error terms): samples beyond it carry weight < e^-kWindowLambdas.
+constexpr double kWindowLambdas = AMPPI_WINDOW_LAMBDAS;
 constexpr int kGridAxis = 24;
 #ifndef AMPPI_LEAF_SIZE
 #define AMPPI_LEAF_SIZE 16
