@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "rollout-steps/s (anchors×samples×horizon); p50 plan-cycle latency ms"
 FLOPS_PER_STEP = 440  # algorithmic FP32 flops per rollout-step (FMA = 2)
-TRAFFIC_BYTES_PER_LAUNCH = 235.0e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
+TRAFFIC_BYTES_PER_LAUNCH = 197.2e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
 
 
 def parse():
