@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 METRIC = "rollout-steps/s (anchors×samples×horizon); p50 plan-cycle latency ms"
 FLOPS_PER_STEP = 440  # algorithmic FP32 flops per rollout-step (FMA = 2)
 TRAFFIC_BYTES_PER_LAUNCH = 197.2e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
+ISSUE_ACTIVE_FRAC = 0.724  # main screening pass issue-slot utilisation, same capture
 
 
 def parse():
@@ -438,7 +439,12 @@ def run_b200(args):
                          "peak_source": "measured FFMA probe (amppi_probe_fp32_peak) in this run; CUDA-core FP32, "
                                         "not a tensor-core path",
                          "algorithmic_flops_per_launch": per_launch_flops,
-                         "kernel_ms_per_launch": screen_ms, "kernel_share_of_step": share},
+                         "kernel_ms_per_launch": screen_ms, "kernel_share_of_step": share,
+                         # what actually bounds it (ncu, profiles/r01_c5_full.md): warp-instruction issue;
+                         # most issued instructions are the exact collision query, outside the 440 flops
+                         "issue_active_frac": ISSUE_ACTIVE_FRAC,
+                         "issue_source": "smsp__issue_active.avg.pct_of_peak_sustained_active of the main "
+                                         "pass, ncu --set full, profiles/r01_c5_full.md"},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": int(launches),
