@@ -20,8 +20,9 @@
 //   larger scenes: k_key_points (global 64-bit atomicMin + candidate log over
 //     many CTAs), k_resolve_ties, k_finalize_scene.
 // Finalize body (per scene): ranges / has_point, 6x6 argmax pooling, flat-order
-// compaction + world transform, collision grid (counting sort, dilated
-// occupancy, per-cell point boxes).
+// compaction + world transform, collision grid (bitonic sort by (cell, Morton
+// code), 16-point leaves with float boxes, cell records, padded neighbour
+// masks, FP32 point blocks for the packed query).
 #include <cuda_runtime.h>
 
 #include <cfloat>
