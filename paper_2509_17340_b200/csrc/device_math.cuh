@@ -394,6 +394,17 @@ __device__ __forceinline__ float screen_collision(float d2, float cs, float ca, 
   }
   return collision_term(d, cs, ca, dmin, dmax);
 }
+// The same with the band precomputed (ScreenConsts).
+__device__ __forceinline__ float screen_collision_b(float d2, float cs, float ca, float dmin, float dmax, float band,
+                                                    bool& amb) {
+  const float d = sqrtf(d2);
+  if (fabsf(d - dmax) < band) {
+    AMPPI_STAT(72, 1);
+    amb = true;
+    return 0.f;
+  }
+  return collision_term(d, cs, ca, dmin, dmax);
+}
 // Stored screening cost: a flagged (lower-bound) cost carries the sign bit.
 __device__ __forceinline__ float screen_store(float cost, bool amb) { return amb ? -cost : cost; }
 

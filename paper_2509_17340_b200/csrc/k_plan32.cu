@@ -177,13 +177,13 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   // Abort radius: a point closer than d_thr adds more than the remaining
   // budget (C exp(-a (d_thr - d_min)) = budget e^0.001), so finding one ends
   // the sample; otherwise the query returns the exact distance (>= d_thr).
-  const float lim2 = screen_reach2(env.cdmax);
+  const float lim2 = env.reach2;
   float stop2 = env.cdmin * env.cdmin;
   bool abortable = false;
   const float budget = env.abort_above - part;
   if (budget < env.cs) {
     float d_thr = env.cdmin + (__logf(env.cs / budget) - 1e-3f) / env.ca;
-    d_thr = fminf(d_thr, (env.cdmax - amb_band(env.cdmax)) * 0.9999995f);  // d < d_thr: a counted term
+    d_thr = fminf(d_thr, env.dthr_cap);  // (d_max - band)(1 - 5e-7): d < d_thr is a counted term
     if (d_thr > env.cdmin) {
       stop2 = d_thr * d_thr;
       abortable = true;
@@ -194,7 +194,7 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
                           : nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, lim2, stop2,
                                             &env.hint);
   if (abortable && d2 < stop2) return 1;
-  s.col = s.col + screen_collision(d2, env.cs, env.ca, env.cdmin, env.cdmax, s.amb);
+  s.col = s.col + screen_collision_b(d2, env.cs, env.ca, env.cdmin, env.cdmax, env.band, s.amb);
   if (((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col) >
       env.abort_above)
     return 1;
@@ -202,6 +202,52 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   if (!state_finite(nx)) return 2;
   x = nx;
   return 0;
+}
+
+// The main pass's float constants, converted once on the host and passed by
+// value: kernel parameters live in the constant bank, so the FP32 code reads
+// them as operands instead of re-converting the FP64 config (F2F) inside its
+// loops.
+struct ScreenConsts {
+  Dyn<float> dyn;
+  float q_p, q_v, q_q, cs, ca, cdmin, cdmax;
+  float wq_track, wq_vnorm, wq_c, wq_cd;
+  float sigma[4];
+  float reach2, band, dthr_cap;
+};
+
+ScreenConsts screen_consts(const DevConfig& c) {
+  ScreenConsts k{};
+  k.dyn.mass = static_cast<float>(c.mass);
+  k.dyn.inv_mass = static_cast<float>(1.0 / c.mass);
+  k.dyn.gx = static_cast<float>(c.gravity[0]);
+  k.dyn.gy = static_cast<float>(c.gravity[1]);
+  k.dyn.gz = static_cast<float>(c.gravity[2]);
+  k.dyn.dt = static_cast<float>(c.dyn_dt);
+  k.dyn.half_dt = static_cast<float>(0.5 * c.dyn_dt);
+  k.dyn.dt6 = static_cast<float>(c.dyn_dt / 6.0);
+  k.dyn.tmin = static_cast<float>(c.thrust_min);
+  k.dyn.tmax = static_cast<float>(c.thrust_max);
+  k.dyn.wxy = static_cast<float>(c.omega_xy_max);
+  k.dyn.wz = static_cast<float>(c.omega_z_max);
+  k.q_p = static_cast<float>(c.q_p);
+  k.q_v = static_cast<float>(c.q_v);
+  k.q_q = static_cast<float>(c.q_q);
+  k.cs = static_cast<float>(c.col_scale);
+  k.ca = static_cast<float>(c.col_slope);
+  k.cdmin = static_cast<float>(c.col_d_min);
+  k.cdmax = static_cast<float>(c.col_d_max);
+  k.wq_track = static_cast<float>(c.q_track);
+  k.wq_vnorm = static_cast<float>(c.q_vnorm);
+  k.wq_c = static_cast<float>(c.q_c);
+  k.wq_cd = static_cast<float>(c.q_c_delta);
+  for (int i = 0; i < 4; ++i) k.sigma[i] = static_cast<float>(c.sigma[i]);
+  // screen_reach2 / amb_band (device_math.cuh) with the same float operations
+  k.band = 1e-4f * k.cdmax + 1e-4f;
+  const float r = k.cdmax + k.band;
+  k.reach2 = r * r * 1.0001f;
+  k.dthr_cap = (k.cdmax - k.band) * 0.9999995f;
+  return k;
 }
 
 // Main screening pass with lane compaction: samples [k1, K) of one instance
@@ -228,7 +274,8 @@ constexpr int kStateWords = 22;  // p(3) q(4) v(3) trk vn mag rate goal col up(4
 // pass: kb0 = nb = 1, kend = 32).
 template <int kMinBlocks, int kCompact, int kT = kScreenThreads>
 __global__ void __launch_bounds__(kT, kMinBlocks)
-    k_stage1_f32c(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter, int kb0, int kend, int nb) {
+    k_stage1_f32c(BatchIn in, Perception P, Plan pl, DevConfig cfg, const ScreenConsts sc, int iter, int kb0, int kend,
+                  int nb) {
   __shared__ float4 s_unom[kMaxN];
   __shared__ float4 s_guide[kMaxN];
   __shared__ float s_bound;
@@ -277,18 +324,18 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   env.unom = reinterpret_cast<const float*>(s_unom);
   env.guide = s_guide;
   env.N = N;
-  env.dyn = make_dyn<float>(cfg);
+  env.dyn = sc.dyn;
   const double* gl = in.goals + 10 * s;
   env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
   env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
   env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
-  env.q_p = static_cast<float>(cfg.q_p);
-  env.q_v = static_cast<float>(cfg.q_v);
-  env.q_q = static_cast<float>(cfg.q_q);
-  env.cs = static_cast<float>(cfg.col_scale);
-  env.ca = static_cast<float>(cfg.col_slope);
-  env.cdmin = static_cast<float>(cfg.col_d_min);
-  env.cdmax = static_cast<float>(cfg.col_d_max);
+  env.q_p = sc.q_p;
+  env.q_v = sc.q_v;
+  env.q_q = sc.q_q;
+  env.cs = sc.cs;
+  env.ca = sc.ca;
+  env.cdmin = sc.cdmin;
+  env.cdmax = sc.cdmax;
   env.grid = P.grid[s];
   env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
   env.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
@@ -296,15 +343,17 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   env.has_guide = true;
   env.abort_above = s_bound;
-  env.wq_track = static_cast<float>(cfg.q_track);
-  env.wq_vnorm = static_cast<float>(cfg.q_vnorm);
-  env.wq_c = static_cast<float>(cfg.q_c);
-  env.wq_cd = static_cast<float>(cfg.q_c_delta);
+  env.wq_track = sc.wq_track;
+  env.wq_vnorm = sc.wq_vnorm;
+  env.wq_c = sc.wq_c;
+  env.wq_cd = sc.wq_cd;
+  env.reach2 = sc.reach2;
+  env.band = sc.band;
+  env.dthr_cap = sc.dthr_cap;
 
   const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
   const uint64_t seed = in.seeds[s];
-  PertRngF pr{0ull, static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
-              static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
+  PertRngF pr{0ull, sc.sigma[0], sc.sigma[1], sc.sigma[2], sc.sigma[3]};
   int k = cfg.k_lo + kb0 + tile * kT + tid;
   bool live = k < cfg.k_lo + kend;
   pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
@@ -320,7 +369,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     __shared__ uint32_t s_hint;
     if (tid == 0) {
       uint32_t h = kNoHint;
-      s_d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, screen_reach2(env.cdmax),
+      s_d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2,
                              env.cdmin * env.cdmin, &h);
       s_hint = h;
     }
@@ -647,6 +696,7 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
     kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
   } else {
+    const ScreenConsts sc = screen_consts(cfg);
     // Lane compaction every 10 steps at 56 registers.  The larger the CTA,
     // the better live samples pack: 224 threads (5 CTAs per SM; the whole
     // K = 256 main pass of an instance in one CTA) beat 128 (9 per SM) by 4%,
@@ -654,11 +704,11 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     if (kr - k1 > 128) {
       const int tiles = (kr - k1 + kMainThreads - 1) / kMainThreads;
       k_stage1_f32c<kMainMinBlocks, kMainCompact, kMainThreads>
-          <<<static_cast<unsigned>(SM * tiles), kMainThreads, 0, st>>>(in, P, pl, cfg, iter, k1, kr, k1);
+          <<<static_cast<unsigned>(SM * tiles), kMainThreads, 0, st>>>(in, P, pl, cfg, sc, iter, k1, kr, k1);
     } else {
       const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
       k_stage1_f32c<9, kMainCompact, kScreenThreads>
-          <<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, k1, kr, k1);
+          <<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, sc, iter, k1, kr, k1);
     }
   }
   return cudaGetLastError();

@@ -75,6 +75,7 @@ struct RolloutEnv<float> {
   float wq_track, wq_vnorm, wq_c, wq_cd;  // stage-I weights for the partial-cost bound
   mutable uint32_t hint = kNoHint;        // nearest point of the previous query (per rollout)
   float d2_x0 = 0.f;                      // squared clearance of x0 (screening kernels share it per CTA)
+  float reach2 = 0.f, band = 0.f, dthr_cap = 0.f;  // main pass: query reach, d_max band, abort-radius cap
 
   __device__ __forceinline__ V3<float> guide_at(int j) const {
     const float4 g = guide[j];
