@@ -24,6 +24,52 @@ namespace {
 
 constexpr int kMaxN = 64;
 
+// The screening kernels' float constants, converted once on the host and passed by
+// value: kernel parameters live in the constant bank, so the FP32 code reads
+// them as operands instead of re-converting the FP64 config (F2F) inside its
+// loops.
+struct ScreenConsts {
+  Dyn<float> dyn;
+  float q_p, q_v, q_q, cs, ca, cdmin, cdmax;
+  float wq_track, wq_vnorm, wq_c, wq_cd;
+  float sigma[4];
+  float reach2, band, dthr_cap;
+};
+
+ScreenConsts screen_consts(const DevConfig& c) {
+  ScreenConsts k{};
+  k.dyn.mass = static_cast<float>(c.mass);
+  k.dyn.inv_mass = static_cast<float>(1.0 / c.mass);
+  k.dyn.gx = static_cast<float>(c.gravity[0]);
+  k.dyn.gy = static_cast<float>(c.gravity[1]);
+  k.dyn.gz = static_cast<float>(c.gravity[2]);
+  k.dyn.dt = static_cast<float>(c.dyn_dt);
+  k.dyn.half_dt = static_cast<float>(0.5 * c.dyn_dt);
+  k.dyn.dt6 = static_cast<float>(c.dyn_dt / 6.0);
+  k.dyn.tmin = static_cast<float>(c.thrust_min);
+  k.dyn.tmax = static_cast<float>(c.thrust_max);
+  k.dyn.wxy = static_cast<float>(c.omega_xy_max);
+  k.dyn.wz = static_cast<float>(c.omega_z_max);
+  k.q_p = static_cast<float>(c.q_p);
+  k.q_v = static_cast<float>(c.q_v);
+  k.q_q = static_cast<float>(c.q_q);
+  k.cs = static_cast<float>(c.col_scale);
+  k.ca = static_cast<float>(c.col_slope);
+  k.cdmin = static_cast<float>(c.col_d_min);
+  k.cdmax = static_cast<float>(c.col_d_max);
+  k.wq_track = static_cast<float>(c.q_track);
+  k.wq_vnorm = static_cast<float>(c.q_vnorm);
+  k.wq_c = static_cast<float>(c.q_c);
+  k.wq_cd = static_cast<float>(c.q_c_delta);
+  for (int i = 0; i < 4; ++i) k.sigma[i] = static_cast<float>(c.sigma[i]);
+  // screen_reach2 / amb_band (device_math.cuh) with the same float operations
+  k.band = 1e-4f * k.cdmax + 1e-4f;
+  const float r = k.cdmax + k.band;
+  k.reach2 = r * r * 1.0001f;
+  k.dthr_cap = (k.cdmax - k.band) * 0.9999995f;
+  return k;
+}
+
 // The current nominal in float (one thread per instance step), the table the
 // screening kernels bulk-copy into shared memory.
 __global__ void k_unom32(Plan pl, int64_t n) {
@@ -43,7 +89,7 @@ __global__ void k_unom32(Plan pl, int64_t n) {
 // support k_support selects.  Aborted samples report FLT_MAX.
 template <int kMinBlocks>
 __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perception P, Plan pl, DevConfig cfg,
-                                                                int iter, int mode, int k1) {
+                                                                const ScreenConsts sc, int iter, int mode, int k1) {
   __shared__ float4 s_unom[kMaxN];
   __shared__ float4 s_guide[kMaxN];
   __shared__ float s_bound;
@@ -91,18 +137,18 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   env.unom = reinterpret_cast<const float*>(s_unom);
   env.guide = s_guide;
   env.N = N;
-  env.dyn = make_dyn<float>(cfg);
+  env.dyn = sc.dyn;
   const double* gl = in.goals + 10 * s;
   env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
   env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
   env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
-  env.q_p = static_cast<float>(cfg.q_p);
-  env.q_v = static_cast<float>(cfg.q_v);
-  env.q_q = static_cast<float>(cfg.q_q);
-  env.cs = static_cast<float>(cfg.col_scale);
-  env.ca = static_cast<float>(cfg.col_slope);
-  env.cdmin = static_cast<float>(cfg.col_d_min);
-  env.cdmax = static_cast<float>(cfg.col_d_max);
+  env.q_p = sc.q_p;
+  env.q_v = sc.q_v;
+  env.q_q = sc.q_q;
+  env.cs = sc.cs;
+  env.ca = sc.ca;
+  env.cdmin = sc.cdmin;
+  env.cdmax = sc.cdmax;
   env.grid = P.grid[s];
   env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
 
@@ -111,10 +157,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   env.has_guide = true;
   env.abort_above = s_bound;
-  env.wq_track = static_cast<float>(cfg.q_track);
-  env.wq_vnorm = static_cast<float>(cfg.q_vnorm);
-  env.wq_c = static_cast<float>(cfg.q_c);
-  env.wq_cd = static_cast<float>(cfg.q_c_delta);
+  env.wq_track = sc.wq_track;
+  env.wq_vnorm = sc.wq_vnorm;
+  env.wq_c = sc.wq_c;
+  env.wq_cd = sc.wq_cd;
+  env.reach2 = sc.reach2;
+  env.band = sc.band;
 
   const double* xs = in.states + 10 * s;
   St<float> x0;
@@ -129,8 +177,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   } else {
     const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
     const PertRngF pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
-                      static_cast<float>(cfg.sigma[0]), static_cast<float>(cfg.sigma[1]),
-                      static_cast<float>(cfg.sigma[2]), static_cast<float>(cfg.sigma[3])};
+                      sc.sigma[0], sc.sigma[1], sc.sigma[2], sc.sigma[3]};
     cs = rollout_costs(x0, env, pr);
   }
   *out = cs.aborted ? 3.4028234663852886e38f
@@ -202,52 +249,6 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   if (!state_finite(nx)) return 2;
   x = nx;
   return 0;
-}
-
-// The main pass's float constants, converted once on the host and passed by
-// value: kernel parameters live in the constant bank, so the FP32 code reads
-// them as operands instead of re-converting the FP64 config (F2F) inside its
-// loops.
-struct ScreenConsts {
-  Dyn<float> dyn;
-  float q_p, q_v, q_q, cs, ca, cdmin, cdmax;
-  float wq_track, wq_vnorm, wq_c, wq_cd;
-  float sigma[4];
-  float reach2, band, dthr_cap;
-};
-
-ScreenConsts screen_consts(const DevConfig& c) {
-  ScreenConsts k{};
-  k.dyn.mass = static_cast<float>(c.mass);
-  k.dyn.inv_mass = static_cast<float>(1.0 / c.mass);
-  k.dyn.gx = static_cast<float>(c.gravity[0]);
-  k.dyn.gy = static_cast<float>(c.gravity[1]);
-  k.dyn.gz = static_cast<float>(c.gravity[2]);
-  k.dyn.dt = static_cast<float>(c.dyn_dt);
-  k.dyn.half_dt = static_cast<float>(0.5 * c.dyn_dt);
-  k.dyn.dt6 = static_cast<float>(c.dyn_dt / 6.0);
-  k.dyn.tmin = static_cast<float>(c.thrust_min);
-  k.dyn.tmax = static_cast<float>(c.thrust_max);
-  k.dyn.wxy = static_cast<float>(c.omega_xy_max);
-  k.dyn.wz = static_cast<float>(c.omega_z_max);
-  k.q_p = static_cast<float>(c.q_p);
-  k.q_v = static_cast<float>(c.q_v);
-  k.q_q = static_cast<float>(c.q_q);
-  k.cs = static_cast<float>(c.col_scale);
-  k.ca = static_cast<float>(c.col_slope);
-  k.cdmin = static_cast<float>(c.col_d_min);
-  k.cdmax = static_cast<float>(c.col_d_max);
-  k.wq_track = static_cast<float>(c.q_track);
-  k.wq_vnorm = static_cast<float>(c.q_vnorm);
-  k.wq_c = static_cast<float>(c.q_c);
-  k.wq_cd = static_cast<float>(c.q_c_delta);
-  for (int i = 0; i < 4; ++i) k.sigma[i] = static_cast<float>(c.sigma[i]);
-  // screen_reach2 / amb_band (device_math.cuh) with the same float operations
-  k.band = 1e-4f * k.cdmax + 1e-4f;
-  const float r = k.cdmax + k.band;
-  k.reach2 = r * r * 1.0001f;
-  k.dthr_cap = (k.cdmax - k.band) * 0.9999995f;
-  return k;
 }
 
 // Main screening pass with lane compaction: samples [k1, K) of one instance
@@ -666,6 +667,7 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   // throughput mode: 64 registers (8 CTAs = 32 warps per SM, a few bytes of
   // L1-resident spill); latency mode: no cap (fastest single rollout)
   auto kern = k_stage1_f32<8>;
+  const ScreenConsts sc = screen_consts(cfg);
   auto unom32 = [&] {  // float nominal table for the bulk smem copies of k_stage1_f32 / k_stage1_f32c
     const int64_t n = SM * cfg.N;
     k_unom32<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pl, n);
@@ -682,21 +684,20 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     }
     unom32();
     TimedRegion t(timer, "k_stage1_f32", st);
-    kern<<<static_cast<unsigned>(SM * tiles), threads, 0, st>>>(in, P, pl, cfg, iter, 0, 0);
+    kern<<<static_cast<unsigned>(SM * tiles), threads, 0, st>>>(in, P, pl, cfg, sc, iter, 0, 0);
     return cudaGetLastError();
   }
   unom32();
   const int k1 = 32;  // bound samples (best of 8-64 measured)
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
-    kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, iter, 1, k1);
+    kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
   }
   TimedRegion t(timer, "k_stage1_f32", st);
   if (in.injected) {
     const int tiles = (kr - k1 + kScreenThreads - 1) / kScreenThreads;
-    kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, iter, 2, k1);
+    kern<<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, sc, iter, 2, k1);
   } else {
-    const ScreenConsts sc = screen_consts(cfg);
     // Lane compaction every 10 steps at 56 registers.  The larger the CTA,
     // the better live samples pack: 224 threads (5 CTAs per SM; the whole
     // K = 256 main pass of an instance in one CTA) beat 128 (9 per SM) by 4%,

@@ -83,9 +83,9 @@ struct RolloutEnv<float> {
   }
   __device__ __forceinline__ float unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ float attitude(Q4<float> q) const { return attitude_err_fast(q, qg); }
-  __device__ __forceinline__ float collision(V3<float> p, bool& amb) const {
-    const float d2 = nearest_sq_fast(grid, grec, gnbr, gleaf, gpts, p, screen_reach2(cdmax), cdmin * cdmin, &hint);
-    return screen_collision(d2, cs, ca, cdmin, cdmax, amb);
+  __device__ __forceinline__ float collision(V3<float> p, bool& amb) const {  // needs reach2 / band set
+    const float d2 = nearest_sq_fast(grid, grec, gnbr, gleaf, gpts, p, reach2, cdmin * cdmin, &hint);
+    return screen_collision_b(d2, cs, ca, cdmin, cdmax, band, amb);
   }
 };
 
