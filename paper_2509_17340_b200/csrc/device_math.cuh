@@ -48,9 +48,18 @@ __device__ __forceinline__ V3<R> operator*(R s, V3<R> a) { return {s * a.x, s * 
 template <typename R>
 __device__ __forceinline__ R sqnorm(V3<R> a) { return (a.x * a.x + a.y * a.y) + a.z * a.z; }
 
+// FP32 screening square root: the hardware approximation (MUFU.SQRT,
+// relative error < 2^-22; +inf -> +inf).  FP32 is only ever the screening
+// arithmetic; every FP64 path uses sqrt().
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 template <typename R>
 __device__ __forceinline__ R dsqrt(R x) {
-  if constexpr (std::is_same_v<R, double>) return sqrt(x); else return sqrtf(x);
+  if constexpr (std::is_same_v<R, double>) return sqrt(x); else return sqrt_approx(x);
 }
 
 template <typename R>
@@ -167,7 +176,7 @@ __device__ __forceinline__ float attitude_err_fast(Q4<float> q, Q4<float> g) {
   const float ex = g.w * q.x - q.w * g.x - (q.y * g.z - q.z * g.y);
   const float ey = g.w * q.y - q.w * g.y - (q.z * g.x - q.x * g.z);
   const float ez = g.w * q.z - q.w * g.z - (q.x * g.y - q.y * g.x);
-  return 2.8284271247461903f * sqrtf(ex * ex + ey * ey + ez * ez);
+  return 2.8284271247461903f * sqrt_approx(ex * ex + ey * ey + ez * ez);
 }
 
 // ---------------------------------------------------------------------------
@@ -215,7 +224,7 @@ __device__ __forceinline__ void normal_pair_f(uint64_t key, uint32_t p, float& n
   const uint64_t b = mix64(key + (2ull * p + 2ull) * kGamma);
   const uint64_t ma = a >> 11;
   const float lg = __logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
-  const float r = sqrtf(fmaxf(-2.0f * lg, 0.0f));  // (the approximate log may round above 0 next to 1)
+  const float r = sqrt_approx(fmaxf(-2.0f * lg, 0.0f));  // (the approximate log may round above 0 next to 1)
   // angle 2*pi*u2 in [0, 2pi): hardware sin/cos after reduction to [-pi, pi)
   // (abs error ~1e-6, far inside the screening window)
   const float u2 = static_cast<float>(b >> 11) * 0x1.0p-53f;
@@ -386,7 +395,7 @@ __device__ __forceinline__ float screen_reach2(float dmax) {
   return r * r * 1.0001f;
 }
 __device__ __forceinline__ float screen_collision(float d2, float cs, float ca, float dmin, float dmax, bool& amb) {
-  const float d = sqrtf(d2);
+  const float d = sqrt_approx(d2);
   if (fabsf(d - dmax) < amb_band(dmax)) {
     AMPPI_STAT(72, 1);
     amb = true;
@@ -397,7 +406,7 @@ __device__ __forceinline__ float screen_collision(float d2, float cs, float ca, 
 // The same with the band precomputed (ScreenConsts).
 __device__ __forceinline__ float screen_collision_b(float d2, float cs, float ca, float dmin, float dmax, float band,
                                                     bool& amb) {
-  const float d = sqrtf(d2);
+  const float d = sqrt_approx(d2);
   if (fabsf(d - dmax) < band) {
     AMPPI_STAT(72, 1);
     amb = true;

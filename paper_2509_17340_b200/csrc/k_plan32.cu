@@ -229,7 +229,8 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   bool abortable = false;
   const float budget = env.abort_above - part;
   if (budget < env.cs) {
-    float d_thr = env.cdmin + (__logf(env.cs / budget) - 1e-3f) / env.ca;
+    // (approximate division and log: their errors are far inside the 1e-3 slack)
+    float d_thr = env.cdmin + __fdividef(__logf(__fdividef(env.cs, budget)) - 1e-3f, env.ca);
     d_thr = fminf(d_thr, env.dthr_cap);  // (d_max - band)(1 - 5e-7): d < d_thr is a counted term
     if (d_thr > env.cdmin) {
       stop2 = d_thr * d_thr;
