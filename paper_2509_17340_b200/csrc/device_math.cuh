@@ -287,9 +287,13 @@ __device__ __forceinline__ Deriv<R> derivative(const St<R>& x, R thrust, V3<R> o
     const double a = thrust / d.mass;
     k.dv = V3<double>{a * dir.x, a * dir.y, a * dir.z} + V3<double>{d.gx, d.gy, d.gz};
   } else {
-    const V3<float> dir = qrot_ez_fast(qnormalized(x.q));
-    const float a = thrust * d.inv_mass;
-    k.dv = {a * dir.x + d.gx, a * dir.y + d.gy, a * dir.z + d.gz};
+    // R(q/|q|) e_z = R_raw(q) e_z / |q|^2: one reciprocal instead of a
+    // normalisation (screening arithmetic; the FP64 branch keeps Eigen's)
+    const Q4<float>& q = x.q;
+    const float n2 = ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w;
+    const float a = __fdividef(thrust * d.inv_mass, n2);
+    k.dv = {a * (2.f * (q.w * q.y + q.x * q.z)) + d.gx, a * (2.f * (q.y * q.z - q.w * q.x)) + d.gy,
+            a * ((q.w * q.w + q.z * q.z) - (q.x * q.x + q.y * q.y)) + d.gz};
   }
   return k;
 }
