@@ -1012,7 +1012,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   // keep the fused snapshot: >= 148 scenes).
   int chunks = static_cast<int>(std::min<int64_t>(6, std::max<int64_t>(1, total / (8 << 20))));
   chunks = std::max(1, std::min(chunks, S / 296));
-  double ratio = 1.3;  // C5 on a B200 over PCIe 5: best of 4-8 chunks x ratio 1.0-1.6 (tools/pipe_sweep.py)
+  double ratio = 1.2;  // C5 on a B200 over PCIe 5: best of 4-8 chunks x ratio 1.0-1.6 (tools/pipe_sweep.py)
   if (const char* f = std::getenv("AMPPI_PIPELINE_CHUNKS")) chunks = std::max(1, std::min(S, std::atoi(f)));  // tests
   if (const char* f = std::getenv("AMPPI_PIPELINE_RATIO")) ratio = std::max(1.0, std::atof(f));
   chunks = std::min(chunks, kMaxChunks);
