@@ -521,30 +521,37 @@ __global__ void __launch_bounds__(128) k_nominal(BatchIn in, Plan pl, DevConfig 
   // and clamped against u_j exactly as rollout_into rewrote them
   const Dyn<double> dy = make_dyn<double>(cfg);
   const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  // One thread per Box-Muller pair (components jc = 2p, 2p+1 share one
+  // normal_pair): the same per-component sums in support order, half the
+  // FP64 draws.
   double* nom = pl.nominal + smi * N * 4;
-  for (int jc = tid; jc < 4 * N; jc += blockDim.x) {
-    const int c = jc & 3;
-    const double u = nom[jc];
-    const double lo = c == 0 ? dy.tmin : (c == 3 ? -dy.wz : -dy.wxy);
-    const double hi = c == 0 ? dy.tmax : (c == 3 ? dy.wz : dy.wxy);
-    double du = 0.0;
+  for (int pj = tid; pj < 2 * N; pj += blockDim.x) {
+    const int jc0 = 2 * pj, c0 = jc0 & 3, c1 = c0 + 1;
+    const double ua = nom[jc0], ub = nom[jc0 + 1];
+    const double lo0 = c0 == 0 ? dy.tmin : -dy.wxy, hi0 = c0 == 0 ? dy.tmax : dy.wxy;
+    const double lo1 = c1 == 3 ? -dy.wz : -dy.wxy, hi1 = c1 == 3 ? dy.wz : dy.wxy;
+    double da = 0.0, db = 0.0;
     for (uint32_t ci = 0; ci < n; ++ci) {
       const double w = cand_w[ci];
       if (w == 0.0) continue;  // 0 * delta adds exactly nothing
       const int k = static_cast<int>(cand_k[ci]);
-      double draw;
+      double d0, d1;
       if (in.injected) {
-        draw = injected_row(in, cfg, s, iter, m, k)[jc];
+        const double* row = injected_row(in, cfg, s, iter, m, k);
+        d0 = row[jc0];
+        d1 = row[jc0 + 1];
       } else {
         const uint64_t key = stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
         double n0, n1;
-        normal_pair(key, static_cast<uint32_t>(jc >> 1), n0, n1);
-        draw = cfg.sigma[c] * ((jc & 1) ? n1 : n0);
+        normal_pair(key, static_cast<uint32_t>(pj), n0, n1);
+        d0 = cfg.sigma[c0] * n0;
+        d1 = cfg.sigma[c1] * n1;
       }
-      const double applied = clampv(u + draw, lo, hi) - u;
-      du = du + w * applied;
+      da = da + w * (clampv(ua + d0, lo0, hi0) - ua);
+      db = db + w * (clampv(ub + d1, lo1, hi1) - ub);
     }
-    nom[jc] = clampv(u + du, lo, hi);
+    nom[jc0] = clampv(ua + da, lo0, hi0);
+    nom[jc0 + 1] = clampv(ub + db, lo1, hi1);
   }
 }
 
