@@ -206,10 +206,13 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   s.goal = s.goal + env.q_q * env.attitude(x.q);
   float d[4];
   pert(j, d);
-  const float u0 = clampv(env.unom_at(j, 0) + d[0], dy.tmin, dy.tmax);
-  const float u1 = clampv(env.unom_at(j, 1) + d[1], -dy.wxy, dy.wxy);
-  const float u2 = clampv(env.unom_at(j, 2) + d[2], -dy.wxy, dy.wxy);
-  const float u3 = clampv(env.unom_at(j, 3) + d[3], -dy.wz, dy.wz);
+  // one 16-byte shared load of the step's nominal; min/max clamps (the
+  // screening's controls are finite, so std::clamp's NaN pass-through is moot)
+  const float4 un = reinterpret_cast<const float4*>(env.unom)[j];
+  const float u0 = fminf(fmaxf(un.x + d[0], dy.tmin), dy.tmax);
+  const float u1 = fminf(fmaxf(un.y + d[1], -dy.wxy), dy.wxy);
+  const float u2 = fminf(fmaxf(un.z + d[2], -dy.wxy), dy.wxy);
+  const float u3 = fminf(fmaxf(un.w + d[3], -dy.wz), dy.wz);
   if (j + 1 < N) {
     s.mag = s.mag + (((u0 * u0 + u1 * u1) + u2 * u2) + u3 * u3);
     if (j >= 1) {
