@@ -32,8 +32,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "rollout-steps/s (anchors×samples×horizon); p50 plan-cycle latency ms"
 FLOPS_PER_STEP = 440  # algorithmic FP32 flops per rollout-step (FMA = 2)
-TRAFFIC_BYTES_PER_LAUNCH = 193.7e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
-ISSUE_ACTIVE_FRAC = 0.723  # main screening pass issue-slot utilisation, same capture
+TRAFFIC_BYTES_PER_LAUNCH = 193.6e6  # bound + main screening pass DRAM bytes, profiles/r01_c5_full.md
+ISSUE_ACTIVE_FRAC = 0.722  # main screening pass issue-slot utilisation, same capture
 
 
 def parse():
