@@ -40,3 +40,16 @@ def test_best_sample_grazes_d_max(oracle, step):
         r, o = run_case(oracle, cfg, np.vstack([q, far]), x, x, goal_target=(20, 0, 2), cycle=0, seed=1,
                         injected=inj)
         assert r.sample_costs[0][0] <= o["sample_costs"][0][0] * (1 + 1e-4)
+
+
+def test_every_sample_flagged(oracle):
+    """All samples fly the same (zero-perturbation) trajectory past a point at
+    d_max (1 + 1e-7): every screening cost is flagged, so k_support has no
+    unflagged minimum and admits every finite sample; the FP64 refine then
+    decides, as in the oracle."""
+    cfg, inj, x, far, traj = _scenario(oracle)
+    zero = np.zeros_like(inj)
+    dmax = cfg.weights.collision.d_max
+    q = traj[12, 0:3] + np.array([0.0, 1.0, 0.0]) * dmax * (1.0 + 1e-7)
+    r, o = run_case(oracle, cfg, np.vstack([q, far]), x, x, goal_target=(20, 0, 2), cycle=0, seed=1, injected=zero)
+    assert np.all(r.sample_costs[0] <= o["sample_costs"][0] * (1 + 1e-4))
