@@ -92,7 +92,10 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
   const int s = gid / M, m = gid % M;
   const int64_t sm = static_cast<int64_t>(s) * M + m;
   const double T = static_cast<double>(N) * cfg.mppi_dt;
-  if (lane == 0) {
+  // Every lane of an instance's warp computes the inputs (identical values);
+  // the correctly rounded pass, when needed, splits its independent atan2 /
+  // sincos pairs over lanes 0 and 1 (the C1 anchors straight at the goal sit
+  // on cell boundaries, so this pass is on the latency path).
   const St<double> x = load_state(in.states + 10 * s);
   const double* gl = in.goals + 10 * s;
   const V3<double> goal_p{gl[0], gl[1], gl[2]};
@@ -102,11 +105,12 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
   const double horizon_s = static_cast<double>(N) * cfg.mppi_dt;
 
   V3<double> initial, refined, safe_dir;
-  double safe_range, terminal_speed;
+  double safe_range, terminal_speed = 0.0, lookahead = 0.0;
   int ci = 0, cj = 0;
   const double goal_dist = norm3(goal_p - x.p);
-  if (goal_dist > cfg.min_anchor_distance) {
-    const double lookahead = dmin(cfg.lookahead, goal_dist);
+  const bool far_goal = goal_dist > cfg.min_anchor_distance;
+  if (far_goal) {
+    lookahead = dmin(cfg.lookahead, goal_dist);
     terminal_speed = dmin(cfg.terminal_speed, goal_dist / horizon_s);
     // sample_initial_endpoints (index m = v*m_h + h) + refine_endpoints.
     // Pass 0 uses CUDA's libm (<= 2 ulp); if either refined-direction
@@ -116,15 +120,50 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
     const int v = m / cfg.m_h, h = m % cfg.m_h;
     const V3<double> tg = goal_p - x.p;
     const double spacing = cfg.spacing_deg * kPiD / 180.0;
+    // a pair of independent correctly rounded evaluations: lanes 0 and 1 in
+    // parallel for a warp per instance, in turn for a thread per instance
+    auto cr_pair = [&](auto f0, auto f1, double& r0, double& r1) {
+      if constexpr (kL > 1) {
+        const double mine = lane == 1 ? f1() : (lane == 0 ? f0() : 0.0);
+        r0 = __shfl_sync(0xffffffffu, mine, 0);
+        r1 = __shfl_sync(0xffffffffu, mine, 1);
+      } else {
+        r0 = f0();
+        r1 = f1();
+      }
+    };
     for (int pass = 0; pass < 2; ++pass) {
       const bool cr = pass == 1;
-      auto t_atan2 = [cr](double yy, double xx) { return cr ? crm::atan2_cr(yy, xx) : atan2(yy, xx); };
-      const double az0 = t_atan2(tg.y, tg.x);
-      const double el0 = t_atan2(tg.z, sqrt(tg.x * tg.x + tg.y * tg.y));
+      double az0, el0;
+      if (!cr) {
+        az0 = atan2(tg.y, tg.x);
+        el0 = atan2(tg.z, sqrt(tg.x * tg.x + tg.y * tg.y));
+      } else {
+        cr_pair([&] { return crm::atan2_cr(tg.y, tg.x); },
+                [&] { return crm::atan2_cr(tg.z, sqrt(tg.x * tg.x + tg.y * tg.y)); }, az0, el0);
+      }
       const double el_off = (static_cast<double>(v) - 0.5 * static_cast<double>(cfg.m_v - 1)) * spacing;
       const double el = clampv(el0 + el_off, -kMaxElevation, kMaxElevation);
       const double az = az0 + (static_cast<double>(h) - 0.5 * static_cast<double>(cfg.m_h - 1)) * spacing;
-      initial = x.p + lookahead * direction_from_angles(az, el, cr);
+      V3<double> dir_unit;
+      if (!cr) {
+        dir_unit = direction_from_angles(az, el, false);
+      } else {  // direction_from_angles(az, el, true): sincos_cr(el) and sincos_cr(az) in parallel
+        double se, ce, sa, ca;
+        if constexpr (kL > 1) {
+          double sn = 0.0, cs = 0.0;
+          if (lane < 2) crm::sincos_cr(lane == 0 ? el : az, sn, cs);
+          se = __shfl_sync(0xffffffffu, sn, 0);
+          ce = __shfl_sync(0xffffffffu, cs, 0);
+          sa = __shfl_sync(0xffffffffu, sn, 1);
+          ca = __shfl_sync(0xffffffffu, cs, 1);
+        } else {
+          crm::sincos_cr(el, se, ce);
+          crm::sincos_cr(az, sa, ca);
+        }
+        dir_unit = {ce * ca, ce * sa, se};
+      }
+      initial = x.p + lookahead * dir_unit;
       V3<double> dir_world = initial - pose_p;
       if (sqnorm(dir_world) < 1e-18) dir_world = {1.0, 0.0, 0.0};
       const double n2 = sqnorm(dir_world);
@@ -133,14 +172,23 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
         dir_world = {dir_world.x / n, dir_world.y / n, dir_world.z / n};
       }
       const V3<double> db = mat_t_vec(body_to_world, dir_world);
-      const double azb = t_atan2(db.y, db.x);
-      const double elb = t_atan2(db.z, sqrt(db.x * db.x + db.y * db.y));
+      double azb, elb;
+      if (!cr) {
+        azb = atan2(db.y, db.x);
+        elb = atan2(db.z, sqrt(db.x * db.x + db.y * db.y));
+      } else {
+        cr_pair([&] { return crm::atan2_cr(db.y, db.x); },
+                [&] { return crm::atan2_cr(db.z, sqrt(db.x * db.x + db.y * db.y)); }, azb, elb);
+      }
       const double qa = (azb + kPiD) / kAzStep, qe = (elb + kHalfPi) / kAzStep;
       if (!cr && (near_integer(qa) || near_integer(qe))) continue;
       ci = az_cell_exact(azb) / kPool;
       cj = el_cell_exact(elb) / kPool;
       break;
     }
+  }
+  if (lane == 0) {
+  if (far_goal) {
     const int64_t f = static_cast<int64_t>(s) * kCoarse + ci * kCEl + cj;
     safe_range = P.safe_range[f];
     safe_dir = mat_vec(body_to_world, V3<double>{P.safe_dir[3 * f], P.safe_dir[3 * f + 1], P.safe_dir[3 * f + 2]});
