@@ -100,6 +100,13 @@ def test_chunked_batches_equal_single_chunk(big_batch, monkeypatch):
     two = _host_call(planner, data)
     for k in one:
         assert np.array_equal(one[k], two[k]), k
+    # other chunk schedules (growth ratio) give the same results too
+    for ratio in ("1.0", "1.6"):
+        monkeypatch.setenv("AMPPI_PIPELINE_RATIO", ratio)
+        again = _host_call(planner, data)
+        for k in one:
+            assert np.array_equal(one[k], again[k]), (ratio, k)
+    monkeypatch.delenv("AMPPI_PIPELINE_RATIO")
     S = len(data["states"])
     dev = torch.device("cuda", 0)
     keep = {k: torch.from_numpy(np.ascontiguousarray(data[k])).to(dev)
