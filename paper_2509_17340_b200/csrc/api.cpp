@@ -170,6 +170,8 @@ struct amppi_ctx {
   uint2* pairs{nullptr};
   unsigned long long* pair_count{nullptr};
   unsigned char* d_gather{nullptr};
+  unsigned char* h_gather{nullptr};  // pinned mirror of d_gather (per-chunk result copies)
+  std::vector<cudaEvent_t> chunk_done;
   // single-scene snapshot bookkeeping
   bool have_snapshot{false};
   double snap_r_max{10.0};
@@ -695,6 +697,7 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->h_xyz) cudaFreeHost(ctx->h_xyz);
   if (ctx->h_in) cudaFreeHost(ctx->h_in);
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
+  if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
@@ -703,6 +706,7 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->inputs_read) cudaEventDestroy(ctx->inputs_read);
   for (cudaEvent_t e : ctx->join) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->chunk_ready) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->chunk_done) cudaEventDestroy(e);
   delete ctx;
   return AMPPI_OK;
 }
@@ -981,6 +985,9 @@ int amppi_shard_finish(amppi_ctx* ctx, amppi_plan_result* out) {
 int32_t amppi_shard_partials_stride(const amppi_ctx* ctx) { return ctx ? 3 + 4 * ctx->dc.N : 0; }
 
 static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, bool device_out);
+static int ensure_gather(amppi_ctx* ctx, bool pinned);
+static int gather_chunk(amppi_ctx* ctx, int s0, int s1, const amppi_batch_output* out, cudaStream_t st);
+static void collect_chunk(amppi_ctx* ctx, int s0, int s1, amppi_batch_output* out);
 
 int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_output* out) {
   if (!ctx || !in) return AMPPI_INVALID_ARGUMENT;
@@ -1045,6 +1052,22 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   const bool concurrent = chunks > 1;
   if (concurrent)
     if (int rc = fork_streams(ctx); rc != AMPPI_OK) return rc;
+  // each chunk's results are gathered and copied to the pinned mirror on its
+  // own stream as soon as it is planned; the host copies chunk c out while
+  // later chunks still run (C5: hides all but the last chunk's result tail)
+  static const bool chunk_gather = [] {
+    const char* f = std::getenv("AMPPI_CHUNK_GATHER");
+    return !f || std::atoi(f) != 0;
+  }();
+  const bool chunk_out = concurrent && out && chunk_gather;
+  if (chunk_out) {
+    if (int rc = ensure_gather(ctx, true); rc != AMPPI_OK) return rc;
+    while (static_cast<int>(ctx->chunk_done.size()) < chunks) {
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ctx->chunk_done.push_back(ev);
+    }
+  }
   // Chunk sizes grow geometrically: the first chunk's upload is the only one
   // not hidden behind planning, so it is the smallest; later chunks grow so
   // their uploads stay ahead of the planning.
@@ -1082,6 +1105,10 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     bin.seeds += s0;
     if (concurrent) {
       if (int rc = run_chunk(ctx, bin, max_chunk_scene, s0, c, cst); rc != AMPPI_OK) return rc;
+      if (chunk_out) {
+        if (int rc = gather_chunk(ctx, s0, s1, out, cst); rc != AMPPI_OK) return rc;
+        CK(cudaEventRecord(ctx->chunk_done[c], cst));
+      }
     } else if (int rc = run_cycle(ctx, bin, max_chunk_scene, true, true, false, s0); rc != AMPPI_OK) {
       return rc;
     }
@@ -1101,6 +1128,13 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
   (void)max_scene;
+  if (chunk_out) {
+    for (int c = 0; c < chunks; ++c) {
+      CK(cudaEventSynchronize(ctx->chunk_done[c]));
+      collect_chunk(ctx, bound[c], bound[c + 1], out);
+    }
+    return sync_and_collect(ctx);
+  }
   return batch_outputs_gather(ctx, S, out, false);
 }
 
@@ -1185,6 +1219,81 @@ int amppi_kernel_times_reset(amppi_ctx* ctx) {
 
 }  // extern "C"
 
+// Gathered results: one field-major block of S_cap scenes (device, and a
+// pinned host mirror for the per-chunk copies of the host pipeline).
+static int ensure_gather(amppi_ctx* ctx, bool pinned) {
+  const size_t Sc = static_cast<size_t>(ctx->S_cap);
+  const size_t bytes = Sc * (2 * sizeof(int32_t) + (4 + 5 + static_cast<size_t>(ctx->dc.N) * 4 + ctx->dc.M) * sizeof(double)) + 256;
+  void* p = nullptr;
+  if (!ctx->d_gather) {
+    CK(ctx->arena.alloc(&p, bytes));
+    ctx->d_gather = static_cast<unsigned char*>(p);
+  }
+  if (pinned && !ctx->h_gather) {
+    CK(cudaMallocHost(&p, bytes));
+    ctx->h_gather = static_cast<unsigned char*>(p);
+  }
+  return AMPPI_OK;
+}
+
+// The gather block's fields, shifted to scene s0.
+static GatherOut gather_view(const amppi_ctx* ctx, unsigned char* base, int64_t s0) {
+  const size_t Sc = static_cast<size_t>(ctx->S_cap);
+  const int64_t M = ctx->dc.M, N = ctx->dc.N;
+  unsigned char* cur = base;
+  GatherOut g{};
+  g.status = carve<int32_t>(cur, Sc) + s0;
+  g.winner = carve<int32_t>(cur, Sc) + s0;
+  g.control = carve<double>(cur, Sc * 4) + 4 * s0;
+  g.breakdown = carve<double>(cur, Sc * 5) + 5 * s0;
+  g.winner_nominal = carve<double>(cur, Sc * N * 4) + N * 4 * s0;
+  g.stage2 = carve<double>(cur, Sc * M) + M * s0;
+  return g;
+}
+
+// Scenes [s0, s1) of the host pipeline: gather on the chunk's stream and copy
+// the requested fields into the pinned mirror, so they cross PCIe while later
+// chunks are planned.  chunk_done[c] marks the copies.
+static int gather_chunk(amppi_ctx* ctx, int s0, int s1, const amppi_batch_output* out, cudaStream_t st) {
+  const int64_t M = ctx->dc.M, N = ctx->dc.N, n = s1 - s0;
+  GatherOut d = gather_view(ctx, ctx->d_gather, s0);
+  const GatherOut h = gather_view(ctx, ctx->h_gather, s0);
+  if (!out->status) d.status = nullptr;
+  if (!out->winner) d.winner = nullptr;
+  if (!out->control) d.control = nullptr;
+  if (!out->breakdown) d.breakdown = nullptr;
+  if (!out->winner_nominal) d.winner_nominal = nullptr;
+  if (!out->stage2) d.stage2 = nullptr;
+  cudaError_t e = launch_gather(shift_plan(ctx->pl, s0, ctx->dc), ctx->dc, static_cast<int>(n), d, st);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_gather");
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    return src ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+  };
+  CK(d2h(h.status, d.status, n * sizeof(int32_t)));
+  CK(d2h(h.winner, d.winner, n * sizeof(int32_t)));
+  CK(d2h(h.control, d.control, n * 4 * sizeof(double)));
+  CK(d2h(h.breakdown, d.breakdown, n * 5 * sizeof(double)));
+  CK(d2h(h.winner_nominal, d.winner_nominal, n * N * 4 * sizeof(double)));
+  CK(d2h(h.stage2, d.stage2, n * M * sizeof(double)));
+  return AMPPI_OK;
+}
+
+// Copy scenes [s0, s1) from the pinned mirror into the caller's buffers (after
+// the chunk's copies completed).
+static void collect_chunk(amppi_ctx* ctx, int s0, int s1, amppi_batch_output* out) {
+  const int64_t M = ctx->dc.M, N = ctx->dc.N, n = s1 - s0;
+  const GatherOut h = gather_view(ctx, ctx->h_gather, s0);
+  auto put = [](void* dst, const void* src, size_t bytes) {
+    if (dst) std::memcpy(dst, src, bytes);
+  };
+  put(out->status ? out->status + s0 : nullptr, h.status, n * sizeof(int32_t));
+  put(out->winner ? out->winner + s0 : nullptr, h.winner, n * sizeof(int32_t));
+  put(out->control ? out->control + 4 * s0 : nullptr, h.control, n * 4 * sizeof(double));
+  put(out->breakdown ? out->breakdown + 5 * s0 : nullptr, h.breakdown, n * 5 * sizeof(double));
+  put(out->winner_nominal ? out->winner_nominal + N * 4 * s0 : nullptr, h.winner_nominal, n * N * 4 * sizeof(double));
+  put(out->stage2 ? out->stage2 + M * s0 : nullptr, h.stage2, n * M * sizeof(double));
+}
+
 // Gather the per-scene winner outputs on the device; copy them out for the
 // host-pointer API.
 static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, bool device_out) {
@@ -1196,22 +1305,8 @@ static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, 
     if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_gather");
     return AMPPI_OK;
   }
-  if (!ctx->d_gather) {
-    const size_t Sc = static_cast<size_t>(ctx->S_cap);
-    const size_t bytes = Sc * (2 * sizeof(int32_t) + (4 + 5 + static_cast<size_t>(N) * 4 + M) * sizeof(double)) + 256;
-    void* p = nullptr;
-    CK(ctx->arena.alloc(&p, bytes));
-    ctx->d_gather = static_cast<unsigned char*>(p);
-  }
-  unsigned char* cur = ctx->d_gather;
-  const size_t Sc = static_cast<size_t>(ctx->S_cap);
-  GatherOut g{};
-  g.status = carve<int32_t>(cur, Sc);
-  g.winner = carve<int32_t>(cur, Sc);
-  g.control = carve<double>(cur, Sc * 4);
-  g.breakdown = carve<double>(cur, Sc * 5);
-  g.winner_nominal = carve<double>(cur, Sc * N * 4);
-  g.stage2 = carve<double>(cur, Sc * M);
+  if (int rc = ensure_gather(ctx, false); rc != AMPPI_OK) return rc;
+  const GatherOut g = gather_view(ctx, ctx->d_gather, 0);
   cudaError_t e = launch_gather(ctx->pl, ctx->dc, S, g, ctx->stream);
   if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_gather");
   const cudaStream_t st = ctx->stream;
