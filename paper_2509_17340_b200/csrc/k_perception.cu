@@ -123,15 +123,17 @@ __device__ __noinline__ int el_cell_slow(double z, double rho) {
 }
 
 // Flat cell f = i*60 + j of a body-frame point.
+// The FP32 stage takes rho in FP32 (relative error ~3e-7: < 1e-5 cells, inside
+// the same guard band); the exact FP64 rho is formed only for the FP64 stages.
 __device__ __forceinline__ int cell_key(V3<double> p) {
-  const double rho = sqrt(p.x * p.x + p.y * p.y);
   constexpr float kInvStepF = static_cast<float>(1.0 / 0x1.acee9f37bebd5p-5);
-  int i = fast_cell(static_cast<float>(p.y), static_cast<float>(p.x), 3.14159265358979f, kInvStepF);
+  const float xf = static_cast<float>(p.x), yf = static_cast<float>(p.y);
+  int i = fast_cell(yf, xf, 3.14159265358979f, kInvStepF);
   if (i < 0) i = az_cell_slow(p.y, p.x);
   if (i >= kAz) i -= kAz;  // +pi wraps onto -pi
   i = i < 0 ? 0 : (i > kAz - 1 ? kAz - 1 : i);
-  int j = fast_cell(static_cast<float>(p.z), static_cast<float>(rho), 1.57079632679490f, kInvStepF);
-  if (j < 0) j = el_cell_slow(p.z, rho);
+  int j = fast_cell(static_cast<float>(p.z), sqrtf(xf * xf + yf * yf), 1.57079632679490f, kInvStepF);
+  if (j < 0) j = el_cell_slow(p.z, sqrt(p.x * p.x + p.y * p.y));
   j = j < 0 ? 0 : (j > kEl - 1 ? kEl - 1 : j);  // pole belongs to the top cell
   return i * kEl + j;
 }
