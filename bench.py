@@ -291,8 +291,7 @@ def run_b200(args):
     # pass with the whole batch as one chunk.  (The timed steps above split it
     # into chunks on concurrent streams, where a kernel's events also span the
     # other streams' kernels.)
-    prev_chunks = os.environ.get("AMPPI_DEVICE_CHUNKS")
-    os.environ["AMPPI_DEVICE_CHUNKS"] = "1"
+    planner.set_schedule(device_chunks=1)
     step()
     torch.cuda.synchronize(dev)
     planner.kernel_times_reset()
@@ -300,10 +299,7 @@ def run_b200(args):
         step()
     planner.synchronize()
     ktimes = planner.kernel_times()
-    if prev_chunks is None:
-        del os.environ["AMPPI_DEVICE_CHUNKS"]
-    else:
-        os.environ["AMPPI_DEVICE_CHUNKS"] = prev_chunks
+    planner.set_schedule(device_chunks=0)
 
     # roofline of the dominant kernel (FP32 stage-I rollouts)
     lib = load()

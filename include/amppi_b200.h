@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define AMPPI_ABI_VERSION 1
+#define AMPPI_ABI_VERSION 2
 
 typedef enum {
   AMPPI_OK = 0,
@@ -90,6 +90,18 @@ typedef struct {
   double q_goal[4];
 } amppi_goal;
 
+/* Schedule knobs: they change how a call is split over streams and chunks,
+ * never its results (tests drive every path with them).  0 = automatic. */
+typedef struct {
+  int32_t pipeline_chunks;   /* amppi_cycle_batch: host-upload pipeline chunks (auto: up to 6) */
+  double pipeline_ratio;     /* growth ratio of successive pipeline chunks (auto: 1.2; >= 1) */
+  int32_t pipeline_streams;  /* compute streams chunks rotate over, 2..4 (auto: 3) */
+  int32_t device_chunks;     /* amppi_cycle_batch_device: concurrent chunks (auto: up to 3) */
+  int32_t chunk_gather;      /* host pipeline: gather each chunk's results as it finishes (auto/1) or once (-1) */
+  int32_t loop_graph;        /* closed loop: replay one captured cycle as a CUDA graph (auto/1) or launch (-1) */
+  int32_t trace;             /* 1: print the host pipeline's upload / compute timeline to stderr */
+} amppi_schedule;
+
 typedef struct {
   int32_t device;          /* CUDA ordinal */
   int32_t precision;       /* 32: FP32 stage-I screening + FP64 softmin support (default)
@@ -98,6 +110,9 @@ typedef struct {
   int64_t max_points;      /* total point capacity over a batch */
   int32_t profile;         /* 1: time every kernel with CUDA events */
   void* stream;            /* optional cudaStream_t to launch on; NULL: own stream */
+  int64_t refine_split_cap;/* FP64 refine: support pairs taken by the split (trajectory | collision)
+                              kernels before the fused overflow kernel; -1 = automatic (4 per instance) */
+  amppi_schedule schedule;
 } amppi_options;
 
 /* PlanResult (ensemble.hpp:33-41) as caller-owned buffers; any pointer may be
@@ -166,6 +181,17 @@ typedef struct {
 
 typedef struct amppi_ctx amppi_ctx;
 
+/* Limits of this implementation (the reference has none): horizon N <= 64
+ * (the screening kernels stage the nominal and guide tables in shared
+ * memory), anchors M = m_h*m_v <= 1024, at most 2^32-1 points per scene.
+ * amppi_create returns AMPPI_INVALID_ARGUMENT past them.
+ *
+ * Capacity contract: a context holds max_scenes scenes and max_points points
+ * per call.  The host-pointer entry points grow the point buffers as needed;
+ * amppi_cycle_batch_device cannot see its per-scene counts, so
+ * point_offsets[n_scenes] must not exceed max_points -- a batch past it is
+ * reported as AMPPI_INVALID_ARGUMENT at the next synchronising call. */
+
 void amppi_config_default(amppi_config* cfg);
 void amppi_options_default(amppi_options* opt);
 int amppi_abi_version(void);
@@ -175,6 +201,17 @@ int amppi_create(const amppi_config* cfg, const amppi_options* opt, amppi_ctx** 
 int amppi_destroy(amppi_ctx* ctx);
 const char* amppi_last_error(const amppi_ctx* ctx);
 int amppi_synchronize(amppi_ctx* ctx);
+
+/* Replace the context's configuration (plan_step takes cfg per call,
+ * ensemble.hpp:59-63): every weight, dynamics, anchor-grid spacing and
+ * sampling parameter may change; the sizes (m_h, m_v, rollouts, horizon,
+ * iterations) may not (AMPPI_INVALID_ARGUMENT: create a context for them).
+ * Takes effect for the next call; the current snapshot stays valid unless
+ * col_d_max changes (its collision grid is sized from d_max), in which case
+ * the snapshot must be rebuilt (amppi_plan returns AMPPI_NO_SNAPSHOT). */
+int amppi_set_config(amppi_ctx* ctx, const amppi_config* cfg);
+int amppi_get_config(const amppi_ctx* ctx, amppi_config* cfg);
+int amppi_set_schedule(amppi_ctx* ctx, const amppi_schedule* schedule);
 
 /* == build_snapshot(buffer, pose, r_max): the buffer's frames concatenated
  * oldest-first (PointCloudBuffer::body_points order, perception.cpp:55-62). */

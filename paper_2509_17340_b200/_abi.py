@@ -64,10 +64,21 @@ class Goal(ctypes.Structure):
     _fields_ = [("p_goal", ctypes.c_double * 3), ("v_goal", ctypes.c_double * 3), ("q_goal", ctypes.c_double * 4)]
 
 
+class Schedule(ctypes.Structure):
+    """amppi_schedule: how a call is split over streams / chunks (never its results); 0 = automatic."""
+
+    _fields_ = [
+        ("pipeline_chunks", ctypes.c_int32), ("pipeline_ratio", ctypes.c_double),
+        ("pipeline_streams", ctypes.c_int32), ("device_chunks", ctypes.c_int32),
+        ("chunk_gather", ctypes.c_int32), ("loop_graph", ctypes.c_int32), ("trace", ctypes.c_int32),
+    ]
+
+
 class Options(ctypes.Structure):
     _fields_ = [
         ("device", ctypes.c_int32), ("precision", ctypes.c_int32), ("max_scenes", ctypes.c_int32),
         ("max_points", ctypes.c_int64), ("profile", ctypes.c_int32), ("stream", ctypes.c_void_p),
+        ("refine_split_cap", ctypes.c_int64), ("schedule", Schedule),
     ]
 
 
@@ -129,6 +140,9 @@ EXPORTS = {
     "amppi_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "amppi_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
     "amppi_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "amppi_set_config": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Config)]),
+    "amppi_get_config": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Config)]),
+    "amppi_set_schedule": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule)]),
     "amppi_snapshot": (ctypes.c_int, [ctypes.c_void_p, c_float_p, ctypes.c_int64, ctypes.POINTER(State), ctypes.c_double]),
     "amppi_snapshot_f64": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int64, ctypes.POINTER(State), ctypes.c_double]),
     "amppi_snapshot_download": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SnapshotView)]),
@@ -184,7 +198,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.amppi_abi_version() != 1:
+    if lib.amppi_abi_version() != 2:
         raise RuntimeError("libamppi_b200 ABI version mismatch")
     if path is None:
         _lib = lib

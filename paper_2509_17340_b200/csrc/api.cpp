@@ -172,8 +172,11 @@ struct amppi_ctx {
   unsigned char* d_gather{nullptr};
   unsigned char* h_gather{nullptr};  // pinned mirror of d_gather (per-chunk result copies)
   std::vector<cudaEvent_t> chunk_done;
+  uint32_t* h_flags{nullptr};  // mapped device error word (Perception::flags)
+  uint64_t points_gen{0};      // bumped when the point buffers are reallocated (captured graphs refer to them)
   // single-scene snapshot bookkeeping
   bool have_snapshot{false};
+  double snap_d_max{0.0};      // col_d_max the snapshot's collision grid was sized with
   double snap_r_max{10.0};
   double snap_pose[10]{};
   int64_t snap_points{0};
@@ -289,6 +292,7 @@ int alloc_points(amppi_ctx* ctx, int64_t P) {
   CK(cudaMallocHost(&ctx->h_xyz, ctx->h_xyz_bytes));
   ctx->P.cand_cap = cap;
   ctx->P_cap = cap;
+  ++ctx->points_gen;
   return AMPPI_OK;
 }
 
@@ -349,6 +353,15 @@ int create_impl(amppi_ctx* ctx) {
   CK(cudaMemset(P.cell_idx, 0xFF, static_cast<size_t>(S) * kCells * sizeof(uint32_t)));
   CK(A.alloc(&p, sizeof(unsigned long long)));
   P.cand_count = static_cast<unsigned long long*>(p);
+  {
+    void* hf = nullptr;
+    CK(cudaHostAlloc(&hf, sizeof(uint32_t), cudaHostAllocMapped));
+    ctx->h_flags = static_cast<uint32_t*>(hf);
+    *ctx->h_flags = 0u;
+    void* df = nullptr;
+    CK(cudaHostGetDevicePointer(&df, hf, 0));
+    P.flags = static_cast<uint32_t*>(df);
+  }
   {
     const std::vector<double> dirs = cell_direction_table();
     CK(A.alloc(&p, dirs.size() * sizeof(double)));
@@ -421,8 +434,8 @@ int create_impl(amppi_ctx* ctx) {
     // (~4 support samples per instance; more spill to the fused k_refine)
     const size_t jobs = std::max<size_t>(4 * SM, static_cast<size_t>(kLatencyRollouts));
     pl.pos_cap = static_cast<int64_t>(jobs);
-    if (const char* f = std::getenv("AMPPI_REFINE_SPLIT_CAP"))  // tests: force the fused-refine overflow path
-      pl.pos_cap = std::max<int64_t>(0, std::min<int64_t>(pl.pos_cap, std::atoll(f)));
+    if (ctx->opt.refine_split_cap >= 0)  // tests: force the fused-refine overflow path
+      pl.pos_cap = std::min<int64_t>(pl.pos_cap, ctx->opt.refine_split_cap);
     CK(A.alloc(&p, jobs * N * 4 * sizeof(double)));
     pl.pos64 = static_cast<double*>(p);
     CK(A.alloc(&p, jobs * sizeof(TrajSums)));
@@ -502,32 +515,27 @@ Plan shift_plan(const Plan& p, int64_t s0, const DevConfig& c) {
   return q;
 }
 
-// Perception arrays of scenes [s0, ...) (the candidate log is indexed by
-// absolute point and needs no shift).
-// Compute streams that pipelined chunks rotate over (AMPPI_PIPELINE_STREAMS,
+// Compute streams that pipelined chunks rotate over (schedule.pipeline_streams,
 // 2..4, default 3: best measured with tools/pipe_sweep.py).
-int pipeline_streams() {
-  static const int n = [] {
-    const char* f = std::getenv("AMPPI_PIPELINE_STREAMS");
-    return f ? std::max(2, std::min(2 + kExtraStreams, std::atoi(f))) : 3;
-  }();
-  return n;
+int pipeline_streams(const amppi_ctx* ctx) {
+  const int n = ctx->opt.schedule.pipeline_streams;
+  return n > 0 ? std::max(2, std::min(2 + kExtraStreams, n)) : 3;
 }
 
 cudaStream_t compute_stream(amppi_ctx* ctx, int c) {
-  const int i = c % pipeline_streams();
+  const int i = c % pipeline_streams(ctx);
   return i == 0 ? ctx->stream : (i == 1 ? ctx->stream2 : ctx->xstream[i - 2]);
 }
 
 // Fork the compute streams off ctx->stream / join them back into it.
 int fork_streams(amppi_ctx* ctx) {
   CK(cudaEventRecord(ctx->join[0], ctx->stream));
-  for (int i = 1; i < pipeline_streams(); ++i) CK(cudaStreamWaitEvent(compute_stream(ctx, i), ctx->join[0], 0));
+  for (int i = 1; i < pipeline_streams(ctx); ++i) CK(cudaStreamWaitEvent(compute_stream(ctx, i), ctx->join[0], 0));
   return AMPPI_OK;
 }
 
 int join_streams(amppi_ctx* ctx) {
-  for (int i = 1; i < pipeline_streams(); ++i) {
+  for (int i = 1; i < pipeline_streams(ctx); ++i) {
     CK(cudaEventRecord(ctx->join[i], compute_stream(ctx, i)));
     CK(cudaStreamWaitEvent(ctx->stream, ctx->join[i], 0));
   }
@@ -593,6 +601,11 @@ int run_cycle(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, bool do_
 int sync_and_collect(amppi_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->timer.enabled) ctx->timer.collect();
+  if (ctx->h_flags && *ctx->h_flags) {
+    *ctx->h_flags = 0u;
+    return ctx->fail(AMPPI_INVALID_ARGUMENT,
+                     "a batch exceeded the context's point capacity (max_points); its results are invalid");
+  }
   return AMPPI_OK;
 }
 
@@ -654,6 +667,8 @@ void amppi_options_default(amppi_options* o) {
   o->max_points = 1 << 20;
   o->profile = 0;
   o->stream = nullptr;
+  o->refine_split_cap = -1;
+  o->schedule = amppi_schedule{};
 }
 
 int amppi_create(const amppi_config* cfg, const amppi_options* opt, amppi_ctx** out) {
@@ -698,6 +713,7 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->h_in) cudaFreeHost(ctx->h_in);
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
   if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
+  if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
@@ -716,6 +732,36 @@ const char* amppi_last_error(const amppi_ctx* ctx) { return ctx ? ctx->err.c_str
 int amppi_synchronize(amppi_ctx* ctx) {
   if (!ctx) return AMPPI_INVALID_ARGUMENT;
   return sync_and_collect(ctx);
+}
+
+int amppi_set_config(amppi_ctx* ctx, const amppi_config* cfg) {
+  if (!ctx || !cfg) return ctx ? ctx->fail(AMPPI_INVALID_ARGUMENT, "null config") : AMPPI_INVALID_ARGUMENT;
+  const std::string bad = validate(*cfg);
+  if (!bad.empty()) return ctx->fail(AMPPI_INVALID_ARGUMENT, bad);
+  const amppi_config& c = ctx->cfg;
+  if (cfg->m_h != c.m_h || cfg->m_v != c.m_v || cfg->rollouts != c.rollouts || cfg->horizon != c.horizon ||
+      cfg->iterations != c.iterations)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "amppi_set_config cannot change m_h, m_v, rollouts, horizon or "
+                                             "iterations (the device arenas are sized from them)");
+  if (ctx->shard_active) return ctx->fail(AMPPI_INVALID_ARGUMENT, "a sharded plan is in progress");
+  // kernels take the configuration by value at launch: work already queued
+  // keeps the old one, the next call uses the new one
+  ctx->cfg = *cfg;
+  ctx->dc = to_dev(*cfg);
+  return AMPPI_OK;
+}
+
+int amppi_get_config(const amppi_ctx* ctx, amppi_config* cfg) {
+  if (!ctx || !cfg) return AMPPI_INVALID_ARGUMENT;
+  *cfg = ctx->cfg;
+  return AMPPI_OK;
+}
+
+int amppi_set_schedule(amppi_ctx* ctx, const amppi_schedule* schedule) {
+  if (!ctx || !schedule) return AMPPI_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->opt.schedule = *schedule;
+  return AMPPI_OK;
 }
 
 int amppi_set_stream(amppi_ctx* ctx, void* stream) {
@@ -759,6 +805,7 @@ static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n,
   BatchIn in = batch_from_block(ctx, 1, r_max, f64);
   if (int rc = run_cycle(ctx, in, n, true, false, false); rc != AMPPI_OK) return rc;
   ctx->have_snapshot = true;
+  ctx->snap_d_max = ctx->dc.col_d_max;
   ctx->snap_r_max = r_max;
   ctx->snap_points = n;
   std::memcpy(ctx->snap_pose, pose, sizeof(ctx->snap_pose));
@@ -811,6 +858,8 @@ int stage_plan_inputs(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* go
                       const double* injected, BatchIn* in_out) {
   if (!x || !goal || !last_applied) return ctx->fail(AMPPI_INVALID_ARGUMENT, "null argument");
   if (!ctx->have_snapshot) return ctx->fail(AMPPI_NO_SNAPSHOT, "amppi_plan before amppi_snapshot");
+  if (ctx->snap_d_max != ctx->dc.col_d_max)
+    return ctx->fail(AMPPI_NO_SNAPSHOT, "the snapshot's collision grid was built for another col_d_max");
   const DevConfig& dc = ctx->dc;
   const int M = dc.M, K = dc.K, N = dc.N;
   InputBlock& h = ctx->hin;
@@ -994,10 +1043,20 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   const int S = in->n_scenes;
   if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
   const int N = ctx->dc.N;
+  if (!in->point_offsets || !in->xyz || !in->poses || !in->states || !in->goals || !in->last_applied ||
+      !in->cycles || !in->seeds)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "null batch input array");
+  if (in->point_offsets[0] != 0) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point_offsets[0] must be 0");
+  int64_t max_scene = 0;
+  for (int s = 0; s < S; ++s) {
+    const int64_t n = in->point_offsets[s + 1] - in->point_offsets[s];
+    if (n < 0) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point_offsets must be non-decreasing");
+    if (n > 0xFFFFFFFFll) return ctx->fail(AMPPI_INVALID_ARGUMENT, "at most 2^32-1 points per scene");
+    max_scene = std::max(max_scene, n);
+  }
   const int64_t total = in->point_offsets[S];
   if (int rc = alloc_points(ctx, total); rc != AMPPI_OK) return rc;
-  int64_t max_scene = 0;
-  for (int s = 0; s < S; ++s) max_scene = std::max(max_scene, in->point_offsets[s + 1] - in->point_offsets[s]);
+  ctx->have_snapshot = false;  // the batch overwrites the single-scene perception slot
   // inputs: points straight from the caller's buffer, per-scene arrays via the
   // pinned block
   InputBlock& h = ctx->hin;
@@ -1020,9 +1079,13 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   int chunks = static_cast<int>(std::min<int64_t>(6, std::max<int64_t>(1, total / (8 << 20))));
   chunks = std::max(1, std::min(chunks, S / 296));
   double ratio = 1.2;  // C5 on a B200 over PCIe 5: best of 4-8 chunks x ratio 1.0-1.6 (tools/pipe_sweep.py)
-  if (const char* f = std::getenv("AMPPI_PIPELINE_CHUNKS")) chunks = std::max(1, std::min(S, std::atoi(f)));  // tests
-  if (const char* f = std::getenv("AMPPI_PIPELINE_RATIO")) ratio = std::max(1.0, std::atof(f));
+  const amppi_schedule& sched = ctx->opt.schedule;
+  if (sched.pipeline_chunks > 0) chunks = std::max(1, std::min(S, sched.pipeline_chunks));  // tests
+  if (sched.pipeline_ratio > 0.0) ratio = std::max(1.0, sched.pipeline_ratio);
   chunks = std::min(chunks, kMaxChunks);
+  // the many-CTA snapshot of a scene past kFusedMaxPoints shares one candidate
+  // log and counter per launch: such a batch is not split into concurrent chunks
+  if (max_scene > kFusedMaxPoints) chunks = 1;
   auto first_chunk = [&](int n) { return ratio > 1.0 ? S * (ratio - 1.0) / (std::pow(ratio, n) - 1.0) : 1.0 * S / n; };
   while (chunks > 1 && first_chunk(chunks) < 148) --chunks;  // smallest chunk >= 148
   while (static_cast<int>(ctx->chunk_ready.size()) < chunks) {
@@ -1036,7 +1099,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   CK(cudaEventRecord(ctx->chunk_ready[0], ctx->stream));
   CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ready[0], 0));
   CK(cudaMemcpyAsync(ctx->din.poses, h.poses, span, cudaMemcpyHostToDevice, ctx->copy_stream));
-  static const bool trace = std::getenv("AMPPI_PIPELINE_TRACE") != nullptr;  // diagnostics
+  const bool trace = sched.trace != 0;  // diagnostics
   std::vector<cudaEvent_t> tev;
   auto tmark = [&](cudaStream_t st) {
     if (!trace) return;
@@ -1055,10 +1118,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
   // each chunk's results are gathered and copied to the pinned mirror on its
   // own stream as soon as it is planned; the host copies chunk c out while
   // later chunks still run (C5: hides all but the last chunk's result tail)
-  static const bool chunk_gather = [] {
-    const char* f = std::getenv("AMPPI_CHUNK_GATHER");
-    return !f || std::atoi(f) != 0;
-  }();
+  const bool chunk_gather = sched.chunk_gather >= 0;
   const bool chunk_out = concurrent && out && chunk_gather;
   if (chunk_out) {
     if (int rc = ensure_gather(ctx, true); rc != AMPPI_OK) return rc;
@@ -1142,6 +1202,10 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
   if (!ctx || !in) return AMPPI_INVALID_ARGUMENT;
   const int S = in->n_scenes;
   if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
+  if (!in->point_offsets || !in->xyz || !in->poses || !in->states || !in->goals || !in->last_applied ||
+      !in->cycles || !in->seeds)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "null batch input array");
+  ctx->have_snapshot = false;  // the batch overwrites the single-scene perception slot
   BatchIn bin{};
   bin.xyz = in->xyz;
   bin.xyz64 = nullptr;
@@ -1165,10 +1229,13 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
   // compute streams still overlap one chunk's latency-bound tail kernels with
   // the others' work (C5: 3 chunks 18.9 ms, 2 chunks 19.0, 1 chunk 19.3,
   // 4 chunks 20.9).
-  int chunks = std::min(pipeline_streams(), S / (2 * 148));
+  int chunks = std::min(pipeline_streams(ctx), S / (2 * 148));
   chunks = std::max(1, std::min(chunks, 3));
-  if (const char* f = std::getenv("AMPPI_DEVICE_CHUNKS")) chunks = std::max(1, std::min(kMaxChunks, std::atoi(f)));
+  if (ctx->opt.schedule.device_chunks > 0) chunks = std::max(1, std::min(kMaxChunks, ctx->opt.schedule.device_chunks));
   if (chunks > 1 && S / chunks < 148) chunks = 1;
+  // scenes past kFusedMaxPoints take the many-CTA snapshot (shared candidate
+  // log): no concurrent chunks
+  if (max_scene > kFusedMaxPoints) chunks = 1;
   if (chunks == 1) {
     if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
     return batch_outputs_gather(ctx, S, out, true);
@@ -1333,6 +1400,7 @@ struct amppi_loop {
   void* mem{nullptr};
   int64_t max_cycles{0};
   cudaGraphExec_t cycle_graph{nullptr};  // one captured cycle, replayed (all state lives on the device)
+  uint64_t graph_points_gen{0};          // ctx->points_gen at capture
 };
 
 static_assert(sizeof(amppi_loop_record) == sizeof(amppi_dev::LoopRecord), "record layout");
@@ -1465,7 +1533,14 @@ int amppi_loop_run(amppi_loop* lp, int64_t cycles, int64_t* ran) {
   // Every cycle launches the same kernels on device-resident state, so one
   // captured cycle is replayed as a CUDA graph (no per-kernel launch cost);
   // with per-kernel profiling on, the cycles are launched individually.
-  const bool graph = !ctx->timer.enabled && std::getenv("AMPPI_LOOP_NO_GRAPH") == nullptr;
+  const bool graph = !ctx->timer.enabled && ctx->opt.schedule.loop_graph >= 0;
+  ctx->have_snapshot = false;  // the loop overwrites the single-scene perception slot
+  // the captured cycle refers to the context's point buffers: capture again
+  // after they were reallocated (a larger snapshot or batch in between)
+  if (lp->cycle_graph && lp->graph_points_gen != ctx->points_gen) {
+    cudaGraphExecDestroy(lp->cycle_graph);
+    lp->cycle_graph = nullptr;
+  }
   if (graph && !lp->cycle_graph && cycles > 0) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -1476,6 +1551,7 @@ int amppi_loop_run(amppi_loop* lp, int64_t cycles, int64_t* ran) {
     const cudaError_t ie = cudaGraphInstantiate(&lp->cycle_graph, g, 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) return ctx->cuda_fail(ie, "graph instantiate");
+    lp->graph_points_gen = ctx->points_gen;
   }
   for (int64_t i = 0; i < cycles; ++i) {
     if (graph) {

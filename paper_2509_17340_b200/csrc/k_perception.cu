@@ -59,7 +59,6 @@ constexpr double kAzStep = 0x1.acee9f37bebd5p-5;   // 2*pi/120 == pi/60
 constexpr double kElStep = 0x1.acee9f37bebd5p-5;
 constexpr double kGuard = 1e-9;   // cells, FP64 stage
 constexpr float kGuardF = 1e-3f;  // cells, FP32 stage
-constexpr int kFusedMaxPoints = 1 << 16;
 
 // Correctly-rounded recomputation, kept out of line: taken only for keys
 // within 1e-9 of a cell boundary.
@@ -192,12 +191,14 @@ __global__ void __launch_bounds__(256) k_key_points(BatchIn in, Perception P) {
       const unsigned long long slot = atomicAdd(P.cand_count, 1ull);
       if (slot < static_cast<unsigned long long>(P.cand_cap))
         P.cand[slot] = Candidate{static_cast<uint32_t>(s * kCells + f), static_cast<uint32_t>(g - b), bits};
+      else
+        atomicOr(P.flags, kFlagCandOverflow);  // a lost candidate could drop a cell's point
     }
   }
 }
 
 __global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
-  const unsigned long long n = *P.cand_count;
+  const unsigned long long n = min(*P.cand_count, static_cast<unsigned long long>(P.cand_cap));
   for (unsigned long long c = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
        c += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
     const Candidate cd = P.cand[c];
@@ -651,6 +652,9 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
   uint32_t* __restrict__ log = reinterpret_cast<uint32_t*>(P.cand) + b;  // [points of this scene]
   if (tid == 0) sm.n_cand = 0u;
   __syncthreads();
+  // the log holds the scene's candidates at [b, e) of the context's candidate
+  // buffer; a scene past 2^16 points or past that buffer re-keys in pass B
+  const bool rekey = e - b > 0x10000 || e > 4 * P.cand_cap;
   const int lane = tid & 31;
   constexpr int kUnroll = 4;  // points per thread per iteration
   // software pipeline: the next iteration's points are loaded before this
@@ -689,7 +693,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
         uint32_t base = 0;
         if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
         base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
-        if (cand && g - b < 0x10000)
+        if (cand && !rekey)
           log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
       }
     }
@@ -699,8 +703,9 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
   // pass B: lowest point index among the logged points at the minimum
   // ("strict <, first point wins", perception.cpp:80-86).  The log packs the
   // index in 16 bits; a scene past that (possible on the device entry point,
-  // whose per-scene counts the host cannot see) re-keys all its points.
-  if (e - b > 0x10000) {
+  // whose per-scene counts the host cannot see), or one whose points lie past
+  // the log's capacity, re-keys all its points.
+  if (rekey) {
     for (int64_t g = b + tid; g < e; g += blockDim.x) {
       int f;
       uint64_t bits;
@@ -708,7 +713,7 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
         atomicMin(sm.idx + f, static_cast<uint32_t>(g - b));
     }
   }
-  const uint32_t n_cand = e - b > 0x10000 ? 0u : sm.n_cand;
+  const uint32_t n_cand = rekey ? 0u : sm.n_cand;
   for (uint32_t c = tid; c < n_cand; c += blockDim.x) {
     const uint32_t en = log[c];
     const int f = static_cast<int>(en >> 16);

@@ -47,6 +47,15 @@ constexpr uint32_t kNbrFaces = (1u << 4) | (1u << 10) | (1u << 12) | (1u << 14) 
 
 constexpr uint64_t kEmptyCell = 0xFFFFFFFFFFFFFFFFull;  // > bits of any finite positive double
 
+// Scenes of at most this many points take the fused per-scene snapshot
+// (k_snapshot_scene); larger ones the many-CTA keying, whose candidate log
+// and counter are shared by every scene of a launch (so a batch containing
+// such a scene runs as one chunk).
+constexpr int64_t kFusedMaxPoints = 1 << 16;
+
+// Bits of the device error word (Perception::flags, host-mapped).
+constexpr uint32_t kFlagCandOverflow = 1u;  // a candidate log ran past its capacity: results invalid
+
 // Flat copy of amppi_config plus derived sizes.
 struct DevConfig {
   int m_h, m_v, M, K, N, iterations;
@@ -98,7 +107,8 @@ struct Perception {
   uint32_t* cell_idx;          // [S*7200] argmin point index
   Candidate* cand;             // [cap]
   unsigned long long* cand_count;
-  int64_t cand_cap;
+  int64_t cand_cap;            // Candidate slots; the fused kernel's uint32 log holds 4 * cand_cap entries
+  uint32_t* flags;             // device error word (kFlag*), mapped host memory
   const double* cell_dir;      // [7200*3] cell-centre directions (host libm)
   // outputs
   double* ranges;              // [S*7200] or null (verification)

@@ -308,7 +308,12 @@ class Planner:
     """One amppi_ctx: device arenas + stream for one host thread."""
 
     def __init__(self, cfg: EnsembleConfig | None = None, *, device: int = 0, precision: int = 32,
-                 max_points: int = 1 << 20, max_scenes: int = 1, profile: bool = False, stream: int | None = None):
+                 max_points: int = 1 << 20, max_scenes: int = 1, profile: bool = False, stream: int | None = None,
+                 refine_split_cap: int = -1, **schedule):
+        """``schedule``: amppi_schedule fields (pipeline_chunks, pipeline_ratio,
+        pipeline_streams, device_chunks, chunk_gather, loop_graph, trace);
+        they change how calls are split over streams and chunks, never their
+        results."""
         self.cfg = cfg or EnsembleConfig()
         self.lib = _abi.load()
         opt = _abi.Options()
@@ -316,6 +321,13 @@ class Planner:
         opt.device, opt.precision, opt.max_scenes = device, precision, max_scenes
         opt.max_points, opt.profile = max_points, 1 if profile else 0
         opt.stream = stream
+        opt.refine_split_cap = refine_split_cap
+        self._schedule = {}
+        for k, v in schedule.items():
+            if k not in dict(_abi.Schedule._fields_):
+                raise TypeError(f"unknown schedule field {k!r}")
+            setattr(opt.schedule, k, v)
+            self._schedule[k] = v
         self._ccfg = self.cfg.to_c()
         h = ctypes.c_void_p()
         rc = self.lib.amppi_create(ctypes.byref(self._ccfg), ctypes.byref(opt), ctypes.byref(h))
@@ -565,6 +577,26 @@ class Planner:
 
     def synchronize(self) -> None:
         self._check(self.lib.amppi_synchronize(self._h))
+
+    def set_schedule(self, **fields) -> None:
+        """Replace schedule fields (unnamed ones keep their current value)."""
+        for k in fields:
+            if k not in dict(_abi.Schedule._fields_):
+                raise TypeError(f"unknown schedule field {k!r}")
+        self._schedule.update(fields)
+        sch = _abi.Schedule()
+        for k, v in self._schedule.items():
+            setattr(sch, k, v)
+        self._check(self.lib.amppi_set_schedule(self._h, ctypes.byref(sch)))
+
+    def set_config(self, cfg: EnsembleConfig) -> None:
+        """plan_step takes cfg per call (ensemble.hpp:59-63): weights, dynamics
+        and sampling parameters may change between calls; sizes may not."""
+        c = cfg.to_c()
+        self._check(self.lib.amppi_set_config(self._h, ctypes.byref(c)))
+        if cfg.weights.collision.d_max != self.cfg.weights.collision.d_max:
+            self._gen += 1  # the snapshot's collision grid was sized for the old d_max
+        self.cfg, self._ccfg = cfg, c
 
     def set_stream(self, stream: int) -> None:
         self._check(self.lib.amppi_set_stream(self._h, ctypes.c_void_p(stream)))

@@ -96,17 +96,17 @@ def test_chunked_batches_equal_single_chunk(big_batch, monkeypatch):
 
     cfg, data, planner = big_batch
     one = _host_call(planner, data)
-    monkeypatch.setenv("AMPPI_PIPELINE_CHUNKS", "2")
+    planner.set_schedule(pipeline_chunks=2)
     two = _host_call(planner, data)
     for k in one:
         assert np.array_equal(one[k], two[k]), k
     # other chunk schedules (growth ratio) give the same results too
-    for ratio in ("1.0", "1.6"):
-        monkeypatch.setenv("AMPPI_PIPELINE_RATIO", ratio)
+    for ratio in (1.0, 1.6):
+        planner.set_schedule(pipeline_ratio=ratio)
         again = _host_call(planner, data)
         for k in one:
             assert np.array_equal(one[k], again[k]), (ratio, k)
-    monkeypatch.delenv("AMPPI_PIPELINE_RATIO")
+    planner.set_schedule(pipeline_ratio=0.0, pipeline_chunks=0)
     S = len(data["states"])
     dev = torch.device("cuda", 0)
     keep = {k: torch.from_numpy(np.ascontiguousarray(data[k])).to(dev)
@@ -114,8 +114,8 @@ def test_chunked_batches_equal_single_chunk(big_batch, monkeypatch):
     keep["cycles"] = torch.from_numpy(data["cycles"].view(np.int64)).to(dev)
     keep["seeds"] = torch.from_numpy(data["seeds"].view(np.int64)).to(dev)
     N, M = cfg.mppi.horizon, cfg.grid.count()
-    for chunks in ("2", "3"):
-        monkeypatch.setenv("AMPPI_DEVICE_CHUNKS", chunks)
+    for chunks in (2, 3):
+        planner.set_schedule(device_chunks=chunks)
         dout = {"status": torch.zeros(S, dtype=torch.int32, device=dev),
                 "winner": torch.zeros(S, dtype=torch.int32, device=dev),
                 "control": torch.zeros(S, 4, dtype=torch.float64, device=dev),

@@ -249,9 +249,8 @@ def test_refine_overflow_path(oracle, monkeypatch):
     re-rollout (k_refine); forced here with a 5-pair split capacity."""
     from paper_2509_17340_b200 import Planner
 
-    monkeypatch.setenv("AMPPI_REFINE_SPLIT_CAP", "5")
     cfg = make_cfg(4, 2, K=256, N=30)
-    planner = Planner(cfg, precision=32, max_points=1 << 20)
+    planner = Planner(cfg, precision=32, max_points=1 << 20, refine_split_cap=5)
     key = (repr(cfg), 32)
     saved = _planners.get(key)
     _planners[key] = planner

@@ -28,7 +28,7 @@ def run(xyz, steps=5):
 
 
 for chunks in ("1", "2", "4", "8"):
-    os.environ["AMPPI_PIPELINE_CHUNKS"] = chunks
+    planner.set_schedule(pipeline_chunks=int(chunks))
     planner.kernel_times_reset()
     t = run(pinned.numpy())
     kt = planner.kernel_times()

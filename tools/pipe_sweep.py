@@ -1,5 +1,5 @@
 """Host-API (amppi_cycle_batch) C5 step time over pipeline chunk counts and
-chunk growth ratios (AMPPI_PIPELINE_CHUNKS / AMPPI_PIPELINE_RATIO), pinned
+chunk growth ratios (schedule pipeline_chunks / pipeline_ratio), pinned
 caller buffers.  Usage: python tools/pipe_sweep.py "4:1.6 8:1.1 ..." """
 import os
 import sys
@@ -19,7 +19,7 @@ pinned = torch.from_numpy(data["xyz"]).pin_memory()
 args = [data["offsets"], pinned.numpy(), data["poses"], data["states"], data["goals"], data["last"]]
 for spec in sys.argv[1].split():
     c, r = spec.split(":")
-    os.environ["AMPPI_PIPELINE_CHUNKS"], os.environ["AMPPI_PIPELINE_RATIO"] = c, r
+    planner.set_schedule(pipeline_chunks=int(c), pipeline_ratio=float(r))
     planner.cycle_batch(*args, data["cycles"], data["seeds"])
     best = []
     for rep in range(3):
