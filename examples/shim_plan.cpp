@@ -20,12 +20,12 @@ int main() {
   State x;
   x.p = {0, 0, 2};
   const GoalSpec goal = GoalSpec::facing(x.p, {25, -3, 2});
-  Planner planner(cfg);
   NominalSequence previous;
+  PlanScratch scratch;  // reused across cycles, as execute_cycle does
   for (std::uint64_t cycle = 0; cycle < 5; ++cycle) {
-    const PerceptionSnapshot snap = build_snapshot(planner, buffer, x, cfg.r_max);
+    const PerceptionSnapshot snap = build_snapshot(buffer, x, cfg.r_max);
     try {
-      const PlanResult plan = plan_step(x, goal, snap, cfg, previous, cfg.dynamics.hover(), cycle, 31);
+      const PlanResult plan = plan_step(x, goal, snap, cfg, previous, cfg.dynamics.hover(), cycle, 31, scratch);
       std::printf("{\"cycle\": %llu, \"winner\": %d, \"control\": [%.17g, %.17g, %.17g, %.17g], \"stage2\": %.17g}\n",
                   static_cast<unsigned long long>(cycle), plan.winner, plan.control.thrust, plan.control.omega[0],
                   plan.control.omega[1], plan.control.omega[2], plan.per_instance[plan.winner].stage2);
