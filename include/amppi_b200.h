@@ -255,6 +255,23 @@ int amppi_shard_update(amppi_ctx* ctx, int32_t iter, const double* all_partials,
 int amppi_shard_finish(amppi_ctx* ctx, amppi_plan_result* out);
 int32_t amppi_shard_partials_stride(const amppi_ctx* ctx);
 
+/* Native NCCL form of the same protocol (the caller owns the communicator,
+ * one rank per GPU, every rank calls with the same inputs and gets the same
+ * result): shard range = balanced split of [0, rollouts) by rank, the
+ * all-reduce MIN and all-gather run on the context's stream.  NCCL is loaded
+ * at run time (dlopen libnccl.so.2); without it these return AMPPI_NCCL_ERROR.
+ * The comm helpers let a host program without NCCL headers create a
+ * communicator: rank 0 calls amppi_nccl_unique_id, ships the 128 bytes to
+ * every rank, and each rank calls amppi_nccl_comm_init. */
+int amppi_nccl_version(int32_t* version);
+int amppi_nccl_unique_id(void* id_out /* 128 bytes */);
+int amppi_nccl_comm_init(void** comm_out, int32_t nranks, const void* id /* 128 bytes */, int32_t rank,
+                         int32_t device);
+int amppi_nccl_comm_destroy(void* comm);
+int amppi_plan_sharded(amppi_ctx* ctx, void* nccl_comm, int32_t rank, int32_t nranks, const amppi_state* x,
+                       const amppi_goal* goal, const double* previous, int32_t previous_len,
+                       const amppi_control* last_applied, uint64_t cycle, uint64_t seed, amppi_plan_result* out);
+
 /* GPU-resident closed loop (execute_cycle, ensemble.cpp:245-305; SURVEY.md
  * §8f row 1): the reference's scenario family `scene_kind` (0 empty,
  * 1 forest, 2 verticals, 3 inclines, 4 two_gap; generate_scenario seed
@@ -316,6 +333,7 @@ int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* 
                        int32_t cap, int32_t* count);
 int amppi_kernel_times_reset(amppi_ctx* ctx);
 int amppi_set_stream(amppi_ctx* ctx, void* stream);
+void* amppi_get_stream(const amppi_ctx* ctx);  /* the cudaStream_t the context launches on */
 
 /* Synthetic input generator (not on the plan path):
  * scenario families of sim_world.cpp:174-246 (kind 0 empty, 1 forest,

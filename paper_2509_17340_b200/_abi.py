@@ -155,6 +155,16 @@ EXPORTS = {
                                           ctypes.c_int32, c_int32_p]),
     "amppi_kernel_times_reset": (ctypes.c_int, [ctypes.c_void_p]),
     "amppi_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "amppi_get_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "amppi_nccl_version": (ctypes.c_int, [c_int32_p]),
+    "amppi_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "amppi_nccl_comm_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_void_p,
+                                            ctypes.c_int32, ctypes.c_int32]),
+    "amppi_nccl_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "amppi_plan_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.POINTER(State), ctypes.POINTER(Goal), c_double_p, ctypes.c_int32,
+                                          ctypes.POINTER(Control), ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.POINTER(PlanResult)]),
     "amppi_sim_scan": (ctypes.c_int, [ctypes.c_int32, c_int32_p, c_uint64_p, ctypes.c_int32, ctypes.c_void_p,
                                       c_uint64_p, ctypes.c_double, ctypes.c_int64, c_float_p, c_int64_p,
                                       ctypes.c_int32]),

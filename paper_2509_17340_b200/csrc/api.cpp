@@ -764,6 +764,8 @@ int amppi_set_schedule(amppi_ctx* ctx, const amppi_schedule* schedule) {
   return AMPPI_OK;
 }
 
+void* amppi_get_stream(const amppi_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
 int amppi_set_stream(amppi_ctx* ctx, void* stream) {
   if (!ctx) return AMPPI_INVALID_ARGUMENT;
   CK(cudaStreamSynchronize(ctx->stream));

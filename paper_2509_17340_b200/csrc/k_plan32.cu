@@ -369,13 +369,18 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
   CostSums<float> cs{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, true, false, false};
   float up[4] = {0.f, 0.f, 0.f, 0.f};
-  {  // the step-0 collision query (exact; every sample starts at x0): every
-     // thread answers the same query (uniform, no divergence) instead of one
-     // thread while the CTA waits at a barrier
-    uint32_t h = kNoHint;
-    env.d2_x0 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2,
-                                env.cdmin * env.cdmin, &h);
-    env.hint = h;
+  {  // the step-0 collision query (exact; every sample starts at x0)
+    __shared__ float s_d2;
+    __shared__ uint32_t s_hint;
+    if (tid == 0) {
+      uint32_t h = kNoHint;
+      s_d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2,
+                             env.cdmin * env.cdmin, &h);
+      s_hint = h;
+    }
+    __syncthreads();
+    env.d2_x0 = s_d2;
+    env.hint = s_hint;
   }
   int round = 0;
   for (int j0 = 0; j0 < N; j0 += kCompact, ++round) {

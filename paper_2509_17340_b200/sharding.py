@@ -157,3 +157,66 @@ def plan_step_sharded_local(planners, snaps, x, goal, previous, last_applied, cy
             p.shard_update(it, allp.data_ptr(), G)
             p.synchronize()
     return [p.shard_finish(want_rollout) for p in planners]
+
+
+# ---------------------------------------------------------------------------
+# Native NCCL path (amppi_plan_sharded): the same protocol driven from C++,
+# with a communicator created through the C ABI (amppi_nccl_*).
+# ---------------------------------------------------------------------------
+class NcclComm:
+    """An NCCL communicator made by the library's own NCCL entry points.
+
+    Rank 0 calls ``NcclComm.unique_id()`` and ships the 128 bytes to every
+    rank (e.g. torch.distributed.broadcast_object_list); each rank then
+    builds ``NcclComm(uid, rank, world, device)``."""
+
+    def __init__(self, uid: bytes, rank: int, world: int, device: int):
+        import ctypes
+
+        from . import _abi
+
+        self.lib = _abi.load()
+        self.rank, self.world = rank, world
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        h = ctypes.c_void_p()
+        rc = self.lib.amppi_nccl_comm_init(ctypes.byref(h), world, buf, rank, device)
+        if rc != _abi.AMPPI_OK:
+            raise RuntimeError(f"amppi_nccl_comm_init failed ({rc})")
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+
+        from . import _abi
+
+        buf = ctypes.create_string_buffer(128)
+        rc = _abi.load().amppi_nccl_unique_id(buf)
+        if rc != _abi.AMPPI_OK:
+            raise RuntimeError(f"amppi_nccl_unique_id failed ({rc}): NCCL not loadable")
+        return buf.raw
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.amppi_nccl_comm_destroy(self.h)
+            self.h = None
+
+
+def plan_step_sharded_native(planner, comm: NcclComm, x, goal, snap, previous, last_applied, cycle: int,
+                             seed: int, want_rollout: bool = True):
+    """plan_step_sharded with the collectives issued by the library itself
+    (ncclAllReduce / ncclAllGather on the planner's stream)."""
+    import ctypes
+
+    if snap.planner is not planner or snap.generation != planner._gen:
+        raise ValueError("snapshot does not belong to this planner's current device state")
+    prev, prev_len = planner._prev(previous)
+    bufs, r = planner._result_buffers(want_rollout, False)
+    xs, gs, lc = x.to_c(), goal.to_c(), last_applied.to_c()
+    from .planner import _ptr
+
+    planner._check(planner.lib.amppi_plan_sharded(
+        planner._h, comm.h, comm.rank, comm.world, ctypes.byref(xs), ctypes.byref(gs),
+        None if prev is None else _ptr(prev, ctypes.c_double), prev_len, ctypes.byref(lc), ctypes.c_uint64(cycle),
+        ctypes.c_uint64(seed), ctypes.byref(r)))
+    return planner._make_result(r, bufs)

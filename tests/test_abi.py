@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "amppi_b200.h")
 
 def declared_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int32_t|void|const char\*)\s+(amppi_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|void\*?|const char\*)\s+(amppi_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_boundary():
@@ -43,7 +43,7 @@ def test_struct_layouts_match_ctypes(tmp_path):
     from paper_2509_17340_b200 import _abi
 
     structs = {"amppi_config": _abi.Config, "amppi_state": _abi.State, "amppi_control": _abi.Control,
-               "amppi_goal": _abi.Goal, "amppi_options": _abi.Options, "amppi_plan_result": _abi.PlanResult,
+               "amppi_goal": _abi.Goal, "amppi_options": _abi.Options, "amppi_schedule": _abi.Schedule, "amppi_plan_result": _abi.PlanResult,
                "amppi_snapshot_view": _abi.SnapshotView, "amppi_batch_input": _abi.BatchInput,
                "amppi_batch_output": _abi.BatchOutput}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]

@@ -84,3 +84,23 @@ def test_c4_shape_two_shards_vs_oracle(oracle):
         assert rel(st1[valid], o["stage1"][valid]) <= 1e-9
         for m in np.flatnonzero(valid):
             assert rel(r.per_instance[m].nominal, o["nominal"][m]) <= 1e-9
+
+
+def test_native_nccl_single_rank_equals_unsharded(oracle):
+    """amppi_plan_sharded through a 1-rank NCCL communicator made by the C ABI
+    (amppi_nccl_unique_id / amppi_nccl_comm_init): the NCCL all-reduce and
+    all-gather run on the context stream and the result equals plan_step."""
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.sharding import NcclComm, plan_step_sharded_native
+
+    cfg = make_cfg(8, 8, K=1024, N=30, iterations=2)
+    cloud, pose, x, goal, prev, la = _inputs(oracle)
+    comm = NcclComm(NcclComm.unique_id(), 0, 1, 0)
+    try:
+        with Planner(cfg, precision=32, max_points=1 << 16) as p:
+            snap = p.build_snapshot(cloud, x, cfg.r_max)
+            ref = p.plan_step(x, goal, snap, prev, la, 21, 5)
+            nat = plan_step_sharded_native(p, comm, x, goal, snap, prev, la, 21, 5)
+    finally:
+        comm.close()
+    _same(nat, ref, 1e-12)
