@@ -346,6 +346,13 @@ int amppi_sim_scan(int32_t n_scenes, const int32_t* kinds, const uint64_t* scene
                    const amppi_state* poses, const uint64_t* frame_seeds, double r_max, int64_t cap_per_scene,
                    float* xyz_out, int64_t* offsets_out, int32_t device);
 
+/* The same scans computed on the host (no GPU needed): the kernel's FP32
+ * arithmetic is shared source (sim_ray.h) built without FMA contraction on
+ * both sides, so the output bytes are identical to amppi_sim_scan's. */
+int amppi_sim_scan_host(int32_t n_scenes, const int32_t* kinds, const uint64_t* scene_seeds, int32_t frames,
+                        const amppi_state* poses, const uint64_t* frame_seeds, double r_max, int64_t cap_per_scene,
+                        float* xyz_out, int64_t* offsets_out);
+
 /* Measured FP32 FMA-pipe throughput of the device (TFLOP/s, FMA = 2 flops):
  * the roofline denominator for the CUDA-core rollout kernel. */
 int amppi_probe_fp32_peak(int32_t device, double* tflops, double* ms);

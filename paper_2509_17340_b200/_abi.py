@@ -168,6 +168,8 @@ EXPORTS = {
     "amppi_sim_scan": (ctypes.c_int, [ctypes.c_int32, c_int32_p, c_uint64_p, ctypes.c_int32, ctypes.c_void_p,
                                       c_uint64_p, ctypes.c_double, ctypes.c_int64, c_float_p, c_int64_p,
                                       ctypes.c_int32]),
+    "amppi_sim_scan_host": (ctypes.c_int, [ctypes.c_int32, c_int32_p, c_uint64_p, ctypes.c_int32, ctypes.c_void_p,
+                                           c_uint64_p, ctypes.c_double, ctypes.c_int64, c_float_p, c_int64_p]),
     "amppi_probe_fp32_peak": (ctypes.c_int, [ctypes.c_int32, c_double_p, c_double_p]),
     "amppi_shard_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(State), ctypes.POINTER(Goal), c_double_p,
                                          ctypes.c_int32, ctypes.POINTER(Control), ctypes.c_uint64, ctypes.c_uint64,

@@ -128,3 +128,48 @@ extern "C" int amppi_sim_scan(int32_t n_scenes, const int32_t* kinds, const uint
   cudaStreamDestroy(st);
   return AMPPI_OK;
 }
+
+// Host form of amppi_sim_scan (same arithmetic as the kernel, sim_ray.h):
+// identical output bytes without a GPU -- the CPU baseline plans exactly the
+// scenes the device planned.  Threads over scenes.
+extern "C" int amppi_sim_scan_host(int32_t n_scenes, const int32_t* kinds, const uint64_t* scene_seeds,
+                                   int32_t frames, const amppi_state* poses, const uint64_t* frame_seeds,
+                                   double r_max, int64_t cap_per_scene, float* xyz_out, int64_t* offsets_out) {
+  if (n_scenes < 1 || frames < 1 || !kinds || !scene_seeds || !poses || !frame_seeds || !xyz_out || !offsets_out ||
+      cap_per_scene < 0)
+    return AMPPI_INVALID_ARGUMENT;
+  const float el_min = static_cast<float>(-45.0 * 3.141592653589793 / 180.0);
+  const float el_max = static_cast<float>(45.0 * 3.141592653589793 / 180.0);
+  std::vector<std::vector<float>> pts(n_scenes);
+  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      for (int s = static_cast<int>(t); s < n_scenes; s += static_cast<int>(nt)) {
+        const std::vector<Prim> sc = generate_scenario(kinds[s], scene_seeds[s]);
+        std::vector<DevPrim> dp;
+        for (const auto& p : sc) dp.push_back(to_device(p));
+        std::vector<Frame> fr(frames);
+        for (int f = 0; f < frames; ++f) {
+          const amppi_state& ps = poses[static_cast<int64_t>(s) * frames + f];
+          fr[f].scene = s;
+          for (int i = 0; i < 3; ++i) fr[f].p[i] = static_cast<float>(ps.p[i]);
+          for (int i = 0; i < 4; ++i) fr[f].q[i] = static_cast<float>(ps.q[i]);
+          fr[f].seed = frame_seeds[static_cast<int64_t>(s) * frames + f];
+        }
+        std::vector<float> out(static_cast<size_t>(cap_per_scene) * 3);
+        const int64_t n = scan_host(dp.data(), static_cast<int>(dp.size()), fr.data(), frames,
+                                    static_cast<float>(r_max), el_min, el_max, 0.01f, cap_per_scene, out.data());
+        out.resize(static_cast<size_t>(n) * 3);
+        pts[s] = std::move(out);
+      }
+    });
+  for (auto& th : pool) th.join();
+  offsets_out[0] = 0;
+  for (int s = 0; s < n_scenes; ++s) {
+    const int64_t n = static_cast<int64_t>(pts[s].size() / 3);
+    std::memcpy(xyz_out + 3 * offsets_out[s], pts[s].data(), pts[s].size() * sizeof(float));
+    offsets_out[s + 1] = offsets_out[s] + n;
+  }
+  return AMPPI_OK;
+}

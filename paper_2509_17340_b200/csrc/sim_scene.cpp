@@ -166,3 +166,48 @@ DevPrim to_device(const Prim& p) {
 }
 
 }  // namespace amppi_sim
+
+namespace amppi_sim {
+
+// Host twin of k_lidar + k_compact (same sim_ray.h arithmetic, built with
+// -ffp-contract=off): frames in order, rays row-major, hits kept up to cap.
+int64_t scan_host(const DevPrim* prims, int n_prims, const Frame* frames, int n_frames, float r_max, float el_min,
+                  float el_max, float range_sigma, int64_t cap, float* xyz) {
+  int j0 = -1, n_rows = 0;
+  lidar_rows(el_min, el_max, &j0, &n_rows);
+  int64_t n = 0;
+  std::vector<int> near;
+  std::vector<std::vector<int>> cols(kLidarAz);
+  for (int f = 0; f < n_frames && n < cap; ++f) {
+    const Frame& fr = frames[f];
+    near.clear();
+    for (int i = 0; i < n_prims; ++i)
+      if (prim_near(prims[i], fr, r_max)) near.push_back(i);
+    for (auto& c : cols) c.clear();
+    for (int k = 0; k < static_cast<int>(near.size()); ++k) {
+      int i0, i1;
+      prim_columns(prims[near[k]], fr, &i0, &i1);
+      for (int ii = i0; ii <= i1 && ii - i0 < kLidarAz; ++ii) cols[((ii % kLidarAz) + kLidarAz) % kLidarAz].push_back(k);
+    }
+    for (int j = j0; j < j0 + n_rows && n < cap; ++j)
+      for (int i = 0; i < kLidarAz && n < cap; ++i) {
+        const uint64_t key = ray_key(fr, i, j);
+        float dir[3];
+        ray_dir(fr, key, i, j, dir);
+        float best = kInfF;
+        const int c = ray_column(dir);
+        if (c >= 0) {
+          for (int k : cols[c]) best = fmin_d(best, ray_hit(prims[near[k]], fr.p, dir, r_max));
+        } else {
+          for (int idx : near) best = fmin_d(best, ray_hit(prims[idx], fr.p, dir, r_max));
+        }
+        if (best < kInfF) {
+          ray_return(fr, key, dir, best, range_sigma, xyz + 3 * n);
+          ++n;
+        }
+      }
+  }
+  return n;
+}
+
+}  // namespace amppi_sim

@@ -56,23 +56,53 @@ def scan_scenes(kinds, seeds, frames: int, frame_poses: np.ndarray, frame_seeds:
     return xyz[: off[-1]].copy(), off
 
 
+def scan_scenes_host(kinds, seeds, frames: int, frame_poses: np.ndarray, frame_seeds: np.ndarray, r_max: float,
+                     cap_per_scene: int):
+    """The same scans on the host (amppi_sim_scan_host, identical bytes)."""
+    lib = _abi.load()
+    S = len(kinds)
+    k = np.ascontiguousarray(kinds, dtype=np.int32)
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    poses = np.ascontiguousarray(frame_poses, dtype=np.float64).reshape(S * frames, 10)
+    fs = np.ascontiguousarray(frame_seeds, dtype=np.uint64).reshape(S * frames)
+    xyz = np.zeros((S * cap_per_scene, 3), dtype=np.float32)
+    off = np.zeros(S + 1, dtype=np.int64)
+    rc = lib.amppi_sim_scan_host(S, k.ctypes.data_as(_abi.c_int32_p), sd.ctypes.data_as(_abi.c_uint64_p), frames,
+                                 poses.ctypes.data, fs.ctypes.data_as(_abi.c_uint64_p), r_max, cap_per_scene,
+                                 xyz.ctypes.data_as(_abi.c_float_p), off.ctypes.data_as(_abi.c_int64_p))
+    if rc != 0:
+        raise RuntimeError(f"amppi_sim_scan_host failed ({rc})")
+    return xyz[: off[-1]].copy(), off
+
+
+def scene_start(scene_id: int) -> np.ndarray:
+    """Where the vehicle enters scene `scene_id` (a function of the id alone,
+    so any subset of a batch -- a rank's shard, the CPU baseline's sample --
+    sees exactly the bytes the whole batch does)."""
+    rng = np.random.default_rng([12345, scene_id])
+    return np.array([rng.uniform(1.0, 30.0), rng.uniform(-8.0, 8.0), 2.0])
+
+
 def scenes(n_scenes: int, points: int = 20000, frames: int = 20, first: int = 0, device: int = 0,
-           kinds=None, r_max: float = 10.0) -> dict:
+           kinds=None, r_max: float = 10.0, host: bool = False) -> dict:
     """Scenes first..first+n_scenes-1 of the C5 family (scene s: kind 1 + s % 3,
-    seed s + 1).  The vehicle flies +x at 3 m/s through the scene; the last
-    frame's pose is the snapshot pose and the plan state."""
+    seed s + 1; every array row is a function of the scene id only).  The
+    vehicle flies +x at 3 m/s through the scene; the last frame's pose is the
+    snapshot pose and the plan state.  host=True scans on the CPU
+    (amppi_sim_scan_host): the same bytes without a GPU."""
     ids = np.arange(first, first + n_scenes)
     kinds = (1 + ids % 3).astype(np.int32) if kinds is None else np.full(n_scenes, kinds, dtype=np.int32)
-    rng = np.random.default_rng(12345 + first)
-    start = np.stack([rng.uniform(1.0, 30.0, n_scenes), rng.uniform(-8.0, 8.0, n_scenes),
-                      np.full(n_scenes, 2.0)], axis=1)
+    start = np.stack([scene_start(int(i)) for i in ids]) if n_scenes else np.zeros((0, 3))
     f = np.arange(frames)
     poses = np.zeros((n_scenes, frames, 10))
     poses[:, :, 0:3] = start[:, None, :] + np.stack([0.06 * f, 0 * f, 0 * f], axis=1)[None]
     poses[:, :, 3] = 1.0
     poses[:, :, 7] = 3.0
     fseeds = np.array([[(_mix64(int(s) + 1) + int(i)) & ((1 << 64) - 1) for i in f] for s in ids], dtype=np.uint64)
-    xyz, off = scan_scenes(kinds, ids + 1, frames, poses, fseeds, r_max, points, device)
+    if host:
+        xyz, off = scan_scenes_host(kinds, ids + 1, frames, poses, fseeds, r_max, points)
+    else:
+        xyz, off = scan_scenes(kinds, ids + 1, frames, poses, fseeds, r_max, points, device)
     state = poses[:, -1, :].copy()
     goal = np.zeros((n_scenes, 10))
     goal[:, 0:3] = (45.0, 0.0, 2.0)
