@@ -219,6 +219,11 @@ int amppi_snapshot(amppi_ctx* ctx, const float* world_xyz, int64_t n_points,
                    const amppi_state* pose, double r_max);
 int amppi_snapshot_f64(amppi_ctx* ctx, const double* world_xyz, int64_t n_points,
                        const amppi_state* pose, double r_max);
+/* The same from a device-resident float32 cloud (read in place, enqueued on
+ * the context stream; the buffer must stay valid until the snapshot kernels
+ * ran, i.e. until the next synchronising call). */
+int amppi_snapshot_device(amppi_ctx* ctx, const float* d_world_xyz, int64_t n_points, const amppi_state* pose,
+                          double r_max);
 int amppi_snapshot_download(amppi_ctx* ctx, amppi_snapshot_view* view);
 
 /* == plan_step(x, goal, snapshot, cfg, previous, last_applied, cycle, seed).

@@ -145,6 +145,8 @@ EXPORTS = {
     "amppi_set_schedule": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule)]),
     "amppi_snapshot": (ctypes.c_int, [ctypes.c_void_p, c_float_p, ctypes.c_int64, ctypes.POINTER(State), ctypes.c_double]),
     "amppi_snapshot_f64": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int64, ctypes.POINTER(State), ctypes.c_double]),
+    "amppi_snapshot_device": (ctypes.c_int, [ctypes.c_void_p, c_float_p, ctypes.c_int64, ctypes.POINTER(State),
+                                             ctypes.c_double]),
     "amppi_snapshot_download": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SnapshotView)]),
     "amppi_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(State), ctypes.POINTER(Goal), c_double_p,
                                   ctypes.c_int32, ctypes.POINTER(Control), ctypes.c_uint64, ctypes.c_uint64,

@@ -776,14 +776,14 @@ int amppi_set_stream(amppi_ctx* ctx, void* stream) {
 }
 
 static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n, const amppi_state* pose,
-                           double r_max) {
+                           double r_max, bool on_device = false) {
   if (!ctx || (!pts && n > 0) || !pose || n < 0) return ctx ? ctx->fail(AMPPI_INVALID_ARGUMENT, "bad arguments")
                                                             : AMPPI_INVALID_ARGUMENT;
   if (!(r_max > 0.0)) return ctx->fail(AMPPI_INVALID_ARGUMENT, "r_max must be positive");
   if (n > 0xFFFFFFFFll) return ctx->fail(AMPPI_INVALID_ARGUMENT, "at most 2^32-1 points per scene");
   if (int rc = alloc_points(ctx, n); rc != AMPPI_OK) return rc;
   const size_t bytes = static_cast<size_t>(n) * 3 * (f64 ? sizeof(double) : sizeof(float));
-  if (n > 0) {
+  if (n > 0 && !on_device) {
     // page-locked caller memory is read by the DMA engine directly; anything
     // else goes through the context's pinned staging buffer
     cudaPointerAttributes attr{};
@@ -805,6 +805,7 @@ static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n,
   CK(cudaMemcpyAsync(ctx->din.offsets, ctx->hin.offsets, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->inputs_read, ctx->stream));
   BatchIn in = batch_from_block(ctx, 1, r_max, f64);
+  if (on_device) in.xyz = static_cast<const float*>(pts);  // read straight from the caller's device buffer
   if (int rc = run_cycle(ctx, in, n, true, false, false); rc != AMPPI_OK) return rc;
   ctx->have_snapshot = true;
   ctx->snap_d_max = ctx->dc.col_d_max;
@@ -826,6 +827,10 @@ int amppi_snapshot(amppi_ctx* ctx, const float* xyz, int64_t n, const amppi_stat
 
 int amppi_snapshot_f64(amppi_ctx* ctx, const double* xyz, int64_t n, const amppi_state* pose, double r_max) {
   return snapshot_common(ctx, xyz, true, n, pose, r_max);
+}
+
+int amppi_snapshot_device(amppi_ctx* ctx, const float* d_xyz, int64_t n, const amppi_state* pose, double r_max) {
+  return snapshot_common(ctx, d_xyz, false, n, pose, r_max, true);
 }
 
 int amppi_snapshot_download(amppi_ctx* ctx, amppi_snapshot_view* v) {

@@ -84,18 +84,18 @@ def scene_start(scene_id: int) -> np.ndarray:
 
 
 def scenes(n_scenes: int, points: int = 20000, frames: int = 20, first: int = 0, device: int = 0,
-           kinds=None, r_max: float = 10.0, host: bool = False) -> dict:
+           kinds=None, r_max: float = 10.0, host: bool = False, frame_step: float = 0.06) -> dict:
     """Scenes first..first+n_scenes-1 of the C5 family (scene s: kind 1 + s % 3,
     seed s + 1; every array row is a function of the scene id only).  The
-    vehicle flies +x at 3 m/s through the scene; the last frame's pose is the
-    snapshot pose and the plan state.  host=True scans on the CPU
+    vehicle advances frame_step metres along +x per frame (0.06: 3 m/s at
+    50 Hz); the last frame's pose is the snapshot pose and the plan state.  host=True scans on the CPU
     (amppi_sim_scan_host): the same bytes without a GPU."""
     ids = np.arange(first, first + n_scenes)
     kinds = (1 + ids % 3).astype(np.int32) if kinds is None else np.full(n_scenes, kinds, dtype=np.int32)
     start = np.stack([scene_start(int(i)) for i in ids]) if n_scenes else np.zeros((0, 3))
     f = np.arange(frames)
     poses = np.zeros((n_scenes, frames, 10))
-    poses[:, :, 0:3] = start[:, None, :] + np.stack([0.06 * f, 0 * f, 0 * f], axis=1)[None]
+    poses[:, :, 0:3] = start[:, None, :] + np.stack([frame_step * f, 0 * f, 0 * f], axis=1)[None]
     poses[:, :, 3] = 1.0
     poses[:, :, 7] = 3.0
     fseeds = np.array([[(_mix64(int(s) + 1) + int(i)) & ((1 << 64) - 1) for i in f] for s in ids], dtype=np.uint64)

@@ -64,7 +64,7 @@ def test_device_scan_1m_point_accumulation_equals_host():
     from paper_2509_17340_b200.workloads import scenes
 
     for kind in (2, 3):
-        dev = scenes(1, points=1_000_000, frames=450, first=7, kinds=kind)
-        host = scenes(1, points=1_000_000, frames=450, first=7, kinds=kind, host=True)
+        dev = scenes(1, points=1_000_000, frames=600, first=7, kinds=kind, frame_step=0.004)
+        host = scenes(1, points=1_000_000, frames=600, first=7, kinds=kind, host=True, frame_step=0.004)
         assert dev["offsets"][-1] == 1_000_000
         assert np.array_equal(dev["xyz"].view(np.uint32), host["xyz"].view(np.uint32))
