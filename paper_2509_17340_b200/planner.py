@@ -518,6 +518,20 @@ class Planner:
         previous: [S,N,4] or None (hover warm start)."""
         S = int(len(offsets) - 1)
         N, M = self.cfg.mppi.horizon, self.cfg.grid.count()
+        off = np.asarray(offsets)
+        if S < 1 or off[0] != 0 or np.any(np.diff(off) < 0):
+            raise ValueError("offsets must start at 0 and be non-decreasing, with at least one scene")
+        if np.asarray(xyz).reshape(-1, 3).shape[0] != int(off[-1]):
+            raise ValueError(f"xyz holds {np.asarray(xyz).reshape(-1, 3).shape[0]} points, offsets[-1] = {off[-1]}")
+        for name, a, w in (("poses", poses, 10), ("states", states, 10), ("goals", goals, 10),
+                           ("last_applied", last_applied, 4)):
+            if np.asarray(a).shape != (S, w):
+                raise ValueError(f"{name} must have shape ({S}, {w})")
+        for name, a in (("cycles", cycles), ("seeds", seeds)):
+            if np.asarray(a).shape != (S,):
+                raise ValueError(f"{name} must have shape ({S},)")
+        if previous is not None and np.asarray(previous).shape != (S, N, 4):
+            raise ValueError(f"previous must have shape ({S}, {N}, 4)")
         arrs = dict(
             offsets=np.ascontiguousarray(offsets, dtype=np.int64), xyz=np.ascontiguousarray(xyz, dtype=np.float32),
             poses=np.ascontiguousarray(poses, dtype=np.float64), states=np.ascontiguousarray(states, dtype=np.float64),
@@ -548,6 +562,7 @@ class Planner:
         bo.winner_nominal = _ptr(out["winner_nominal"], ctypes.c_double)
         bo.stage2 = _ptr(out["stage2"], ctypes.c_double)
         bo.breakdown = _ptr(out["breakdown"], ctypes.c_double)
+        self._gen += 1  # the batch overwrites the single-scene snapshot slot
         self._check(self.lib.amppi_cycle_batch(self._h, ctypes.byref(bi), ctypes.byref(bo)))
         return out
 
@@ -573,6 +588,7 @@ class Planner:
                       ("breakdown", ctypes.c_double)):
             if out.get(k):
                 setattr(bo, k, ctypes.cast(ctypes.c_void_p(out[k]), ctypes.POINTER(ct)))
+        self._gen += 1  # the batch overwrites the single-scene snapshot slot
         self._check(self.lib.amppi_cycle_batch_device(self._h, ctypes.byref(bi), ctypes.byref(bo)))
 
     def synchronize(self) -> None:
@@ -633,6 +649,7 @@ class ClosedLoop:
         self._h = h
 
     def run(self, cycles: int) -> int:
+        self.planner._gen += 1  # the loop overwrites the single-scene snapshot slot
         ran = ctypes.c_int64()
         self.planner._check(self.lib.amppi_loop_run(self._h, cycles, ctypes.byref(ran)))
         return int(ran.value)

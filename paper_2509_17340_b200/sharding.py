@@ -90,7 +90,12 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
 
     def allgather(self, out, t):
-        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        try:
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+        except (RuntimeError, NotImplementedError):  # backends without the fused form (gloo on some builds)
+            parts = list(out.chunk(self.world))
+            self.dist.all_gather(parts, t, group=self.group)
+            out.copy_(__import__("torch").cat(parts))
 
 
 def plan_step_sharded(planner, x, goal, snap, previous, last_applied, cycle: int, seed: int, comm,

@@ -122,3 +122,74 @@ def test_scene_past_65536_points_device_entry(oracle, ragged):
     host = _host(planner, huge)
     for k in out:
         assert np.array_equal(out[k], host[k]), k
+
+
+def test_chunked_batches_with_a_scene_past_65536_points(oracle):
+    """A batch large enough to be split into concurrent chunks that contains a
+    scene past the fused snapshot's limit: that scene takes the many-CTA
+    keying, whose candidate log is shared per launch, so the batch must run
+    as one chunk (host entry, forced pipeline chunks; device entry with a
+    capacity that selects the many-CTA keying) -- results equal the plain run."""
+    import torch
+
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.workloads import plan_config, scenes
+
+    cfg = plan_config()
+    S2 = 320
+    data = scenes(S2, points=20000, frames=20, first=5000)
+    off = data["offsets"]
+    parts = [data["xyz"][off[s]:off[s + 1]] for s in range(S2)]
+    parts[200] = np.concatenate(parts[200:205])  # > 65536 points
+    big = dict(data)
+    big["xyz"] = np.concatenate(parts).astype(np.float32)
+    big["offsets"] = np.concatenate([[0], np.cumsum([len(p) for p in parts])]).astype(np.int64)
+    assert big["offsets"][201] - big["offsets"][200] > 65536
+    with Planner(cfg, precision=32, max_scenes=S2, max_points=int(big["offsets"][-1])) as p:
+        ref = _host(p, big)
+        p.set_schedule(pipeline_chunks=4)
+        chunked = _host(p, big)
+    for k in ref:
+        assert np.array_equal(ref[k], chunked[k]), k
+    _check(oracle, cfg, big, ref, [199, 200, 201])
+    # device entry: capacity / scenes > 65536 selects the many-CTA keying
+    with Planner(cfg, precision=32, max_scenes=S2, max_points=S2 * 70000, device_chunks=3) as p:
+        dev = torch.device("cuda", 0)
+        keep = {k: torch.from_numpy(np.ascontiguousarray(big[k])).to(dev)
+                for k in ("xyz", "offsets", "poses", "states", "goals", "last")}
+        keep["cycles"] = torch.from_numpy(big["cycles"].view(np.int64)).to(dev)
+        keep["seeds"] = torch.from_numpy(big["seeds"].view(np.int64)).to(dev)
+        N, M = cfg.mppi.horizon, cfg.grid.count()
+        dout = {"status": torch.zeros(S2, dtype=torch.int32, device=dev),
+                "winner": torch.zeros(S2, dtype=torch.int32, device=dev),
+                "control": torch.zeros(S2, 4, dtype=torch.float64, device=dev),
+                "winner_nominal": torch.zeros(S2, N, 4, dtype=torch.float64, device=dev),
+                "stage2": torch.zeros(S2, M, dtype=torch.float64, device=dev),
+                "breakdown": torch.zeros(S2, 5, dtype=torch.float64, device=dev)}
+        p.cycle_batch_device({k: v.data_ptr() for k, v in keep.items()}, {k: v.data_ptr() for k, v in dout.items()},
+                             S2, cfg.r_max)
+        p.synchronize()
+        for k in dout:
+            assert np.array_equal(dout[k].cpu().numpy(), ref[k]), k
+
+
+def test_batch_invalidates_the_single_scene_snapshot(ragged):
+    """cycle_batch overwrites the single-scene perception slot: planning on a
+    snapshot built before it is refused (the Python generation check, and the
+    C ABI's AMPPI_NO_SNAPSHOT underneath), not silently planned on another
+    scene's perception."""
+    import ctypes
+
+    from paper_2509_17340_b200 import ControlInput, GoalSpec, State, _abi
+
+    cfg, rag, _, planner = ragged
+    pts = rag["xyz"][rag["offsets"][10]:rag["offsets"][11]]
+    x = State.from_array(rag["states"][10])
+    snap = planner.build_snapshot(pts, x, cfg.r_max)
+    _host(planner, rag)
+    with pytest.raises(ValueError):
+        planner.plan_step(x, GoalSpec((45, 0, 2)), snap, None, ControlInput(9.81), 1, 1)
+    xs, gs, lc = x.to_c(), GoalSpec((45, 0, 2)).to_c(), ControlInput(9.81).to_c()
+    rc = planner.lib.amppi_plan(planner._h, ctypes.byref(xs), ctypes.byref(gs), None, 0, ctypes.byref(lc),
+                                ctypes.c_uint64(1), ctypes.c_uint64(1), None, None)
+    assert rc == _abi.AMPPI_NO_SNAPSHOT

@@ -143,3 +143,111 @@ def test_merge_raises_when_every_rank_is_empty():
     e = (np.inf, 0.0, 0.0, np.zeros((3, 4)))
     with pytest.raises(RuntimeError, match="no valid rollout"):
         merge_softmin([e, e], 0.1)
+
+
+# ---------------------------------------------------------------------------
+# the same decompositions with the device planner: two processes on cuda:0,
+# host-side gloo collectives (on CUDA tensors for the sample-sharded plan);
+# no kernel waits on another process, so sharing one GPU is safe
+# ---------------------------------------------------------------------------
+def _device_sample_worker(rank, world, port, out):
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
+    from test_sample_sharding import _inputs
+
+    from oracle_py import Oracle
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.sharding import TorchComm, plan_step_sharded
+    from test_plan_parity import make_cfg
+
+    _init(rank, world, port)
+    torch.cuda.set_device(0)
+    cfg = make_cfg(8, 8, K=2048, N=30, iterations=2)
+    cloud, pose, x, goal, prev, la = _inputs(Oracle())
+    with Planner(cfg, precision=32, max_points=1 << 16) as p:
+        snap = p.build_snapshot(cloud, x, cfg.r_max)
+        r = plan_step_sharded(p, x, goal, snap, prev, la, 13, 4, TorchComm())
+    out.put((rank, r.winner, r.control.vec(), [pi.stage1 for pi in r.per_instance],
+             [pi.nominal if pi.valid else None for pi in r.per_instance]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sample_sharded_plan_two_ranks_gloo_device(oracle):
+    """plan_step_sharded through a real torch.distributed communicator
+    (TorchComm over gloo, CUDA tensors), 2 ranks x 1024 samples per instance:
+    both ranks return the unsharded plan."""
+    from paper_2509_17340_b200 import Planner
+    from test_plan_parity import make_cfg, rel
+    from test_sample_sharding import _inputs
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_device_sample_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = make_cfg(8, 8, K=2048, N=30, iterations=2)
+    cloud, pose, x, goal, prev, la = _inputs(oracle)
+    with Planner(cfg, precision=32, max_points=1 << 16) as p:
+        snap = p.build_snapshot(cloud, x, cfg.r_max)
+        ref = p.plan_step(x, goal, snap, prev, la, 13, 4)
+    for rank, winner, control, st1, nominal in got:
+        assert winner == ref.winner
+        assert rel(control, ref.control.vec()) <= 1e-12
+        assert rel(st1, [pi.stage1 for pi in ref.per_instance]) <= 1e-12
+        for m, pi in enumerate(ref.per_instance):
+            if pi.valid:
+                assert rel(nominal[m], pi.nominal) <= 1e-12
+
+
+def _device_scene_worker(rank, world, port, out):
+    _init(rank, world, port)
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.workloads import plan_config, scenes
+
+    S = 300
+    first, n = shard_ranges(S, world)[rank]
+    d = scenes(n, points=20000, frames=20, first=first)
+    cfg = plan_config()
+    with Planner(cfg, max_scenes=n, max_points=int(d["offsets"][-1])) as p:
+        r = p.cycle_batch(d["offsets"], d["xyz"], d["poses"], d["states"], d["goals"], d["last"], d["cycles"],
+                          d["seeds"])
+    local = torch.zeros(S, 5, dtype=torch.float64)
+    local[first:first + n, 0] = torch.from_numpy(r["winner"].astype(np.float64))
+    local[first:first + n, 1:] = torch.from_numpy(r["control"])
+    dist.all_reduce(local)  # disjoint rows
+    if rank == 0:
+        out.put(local.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_scene_sharded_batch_two_ranks_gloo_device():
+    """C5 scene sharding with the device planner: 2 ranks plan halves of a
+    300-scene batch; the gathered results equal one process planning it all
+    (scenes are a function of their id, so a rank's shard is the batch's)."""
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.workloads import plan_config, scenes
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_device_scene_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    d = scenes(300, points=20000, frames=20, first=0)
+    with Planner(plan_config(), max_scenes=300, max_points=int(d["offsets"][-1])) as p:
+        r = p.cycle_batch(d["offsets"], d["xyz"], d["poses"], d["states"], d["goals"], d["last"], d["cycles"],
+                          d["seeds"])
+    assert np.array_equal(got[:, 0].astype(np.int32), r["winner"])
+    assert np.array_equal(got[:, 1:], r["control"])
