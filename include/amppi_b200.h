@@ -99,6 +99,7 @@ typedef struct {
   int32_t device_chunks;     /* amppi_cycle_batch_device: concurrent chunks (auto: up to 3) */
   int32_t chunk_gather;      /* host pipeline: gather each chunk's results as it finishes (auto/1) or once (-1) */
   int32_t loop_graph;        /* closed loop: replay one captured cycle as a CUDA graph (auto/1) or launch (-1) */
+  int32_t plan_graph;        /* amppi_plan: replay the plan kernels as a cached CUDA graph (auto/1) or launch (-1) */
   int32_t trace;             /* 1: print the host pipeline's upload / compute timeline to stderr */
 } amppi_schedule;
 

@@ -70,7 +70,8 @@ class Schedule(ctypes.Structure):
     _fields_ = [
         ("pipeline_chunks", ctypes.c_int32), ("pipeline_ratio", ctypes.c_double),
         ("pipeline_streams", ctypes.c_int32), ("device_chunks", ctypes.c_int32),
-        ("chunk_gather", ctypes.c_int32), ("loop_graph", ctypes.c_int32), ("trace", ctypes.c_int32),
+        ("chunk_gather", ctypes.c_int32), ("loop_graph", ctypes.c_int32), ("plan_graph", ctypes.c_int32),
+        ("trace", ctypes.c_int32),
     ]
 
 

@@ -173,6 +173,17 @@ struct amppi_ctx {
   unsigned char* h_gather{nullptr};  // pinned mirror of d_gather (per-chunk result copies)
   std::vector<cudaEvent_t> chunk_done;
   uint32_t* h_flags{nullptr};  // mapped device error word (Perception::flags)
+  // single-scene plan captured as a CUDA graph (the plan kernels of one
+  // amppi_plan call), replayed while its key matches
+  struct PlanGraphKey {
+    bool want_states{false};
+    bool injected{false};
+    double r_max{0.0};
+    uint64_t points_gen{0};
+    amppi_config cfg{};
+  };
+  cudaGraphExec_t plan_graph{nullptr};
+  PlanGraphKey plan_graph_key{};
   uint64_t points_gen{0};      // bumped when the point buffers are reallocated (captured graphs refer to them)
   // single-scene snapshot bookkeeping
   bool have_snapshot{false};
@@ -714,6 +725,7 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
   if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  if (ctx->plan_graph) cudaGraphExecDestroy(ctx->plan_graph);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
@@ -974,7 +986,39 @@ int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, con
       rc != AMPPI_OK)
     return rc;
   const bool want_states = out && (out->winner_states || out->winner_controls);
-  if (int rc = run_cycle(ctx, in, ctx->snap_points, false, true, want_states); rc != AMPPI_OK) return rc;
+  // The plan kernels of a single-scene call depend only on the sizes, the
+  // configuration, r_max and the context's (fixed) arrays: they are captured
+  // once as a CUDA graph and replayed (one launch instead of ~12).
+  const bool graph = !ctx->timer.enabled && ctx->opt.schedule.plan_graph >= 0;
+  if (graph) {
+    amppi_ctx::PlanGraphKey key;
+    key.want_states = want_states;
+    key.injected = in.injected != nullptr;
+    key.r_max = in.r_max;
+    key.points_gen = ctx->points_gen;
+    key.cfg = ctx->cfg;
+    const amppi_ctx::PlanGraphKey& k0 = ctx->plan_graph_key;
+    const bool hit = ctx->plan_graph && k0.want_states == key.want_states && k0.injected == key.injected &&
+                     k0.r_max == key.r_max && k0.points_gen == key.points_gen &&
+                     std::memcmp(&k0.cfg, &key.cfg, sizeof(key.cfg)) == 0;
+    if (!hit) {
+      if (ctx->plan_graph) cudaGraphExecDestroy(ctx->plan_graph);
+      ctx->plan_graph = nullptr;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      const int rc = run_cycle(ctx, in, ctx->snap_points, false, true, want_states);
+      const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+      if (rc != AMPPI_OK) return rc;
+      if (ce != cudaSuccess) return ctx->cuda_fail(ce, "plan graph capture");
+      const cudaError_t ie = cudaGraphInstantiate(&ctx->plan_graph, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) return ctx->cuda_fail(ie, "plan graph instantiate");
+      ctx->plan_graph_key = key;
+    }
+    CK(cudaGraphLaunch(ctx->plan_graph, ctx->stream));
+  } else if (int rc = run_cycle(ctx, in, ctx->snap_points, false, true, want_states); rc != AMPPI_OK) {
+    return rc;
+  }
   return collect_plan_result(ctx, out, want_states);
 }
 

@@ -192,10 +192,17 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
 // to find one point inside the radius whose collision term would exhaust the
 // remaining budget (then the sample aborts); otherwise it returns the exact
 // distance.  Same sums in the same order as rollout_costs for every sample
-// that is not aborted.
+// that is not aborted.  Split in two around the query (screen_pre /
+// screen_post) so a warp can answer its lanes' queries together.
+struct StepCtl {
+  float u[4];      // the step's clamped control
+  float stop2;     // the query may stop below this squared distance
+  bool abortable;  // a point closer than sqrt(stop2) aborts the sample
+};
+
 template <typename Pert>
-__device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, float (&up)[4], int j,
-                                           const RolloutEnv<float>& env, const Pert& pert) {
+__device__ __forceinline__ int screen_pre(const St<float>& x, CostSums<float>& s, float (&up)[4], int j,
+                                          const RolloutEnv<float>& env, const Pert& pert, StepCtl& c) {
   const Dyn<float>& dy = env.dyn;
   const int N = env.N;
   AMPPI_STAT(8 + j, 1);
@@ -221,38 +228,193 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
     }
   }
   up[0] = u0; up[1] = u1; up[2] = u2; up[3] = u3;
+  c.u[0] = u0; c.u[1] = u1; c.u[2] = u2; c.u[3] = u3;
   const float part =
       ((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col);
   if (part > env.abort_above) return 1;
   // Abort radius: a point closer than d_thr adds more than the remaining
   // budget (C exp(-a (d_thr - d_min)) = budget e^0.001), so finding one ends
   // the sample; otherwise the query returns the exact distance (>= d_thr).
-  const float lim2 = env.reach2;
-  float stop2 = env.cdmin * env.cdmin;
-  bool abortable = false;
+  c.stop2 = env.cdmin * env.cdmin;
+  c.abortable = false;
   const float budget = env.abort_above - part;
   if (budget < env.cs) {
     // (approximate division and log: their errors are far inside the 1e-3 slack)
     float d_thr = env.cdmin + __fdividef(__logf(__fdividef(env.cs, budget)) - 1e-3f, env.ca);
     d_thr = fminf(d_thr, env.dthr_cap);  // (d_max - band)(1 - 5e-7): d < d_thr is a counted term
     if (d_thr > env.cdmin) {
-      stop2 = d_thr * d_thr;
-      abortable = true;
+      c.stop2 = d_thr * d_thr;
+      c.abortable = true;
     }
   }
-  // step 0 is x0 for every sample: its query was answered once per CTA
-  const float d2 = j == 0 ? env.d2_x0
-                          : nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, lim2, stop2,
-                                            &env.hint);
-  if (abortable && d2 < stop2) return 1;
+  return 0;
+}
+
+// The rest of the step once the query answered d2: collision term, bound, RK4.
+__device__ __forceinline__ int screen_post(St<float>& x, CostSums<float>& s, const StepCtl& c, float d2,
+                                           const RolloutEnv<float>& env) {
+  if (c.abortable && d2 < c.stop2) return 1;
   s.col = s.col + screen_collision_b(d2, env.cs, env.ca, env.cdmin, env.cdmax, env.band, s.amb);
   if (((env.wq_track * s.trk + env.wq_vnorm * s.vn) + (env.wq_c * s.mag + env.wq_cd * s.rate)) + (s.goal + s.col) >
       env.abort_above)
     return 1;
-  const St<float> nx = rk4_normalized(x, u0, V3<float>{u1, u2, u3}, dy);
+  const St<float> nx = rk4_normalized(x, c.u[0], V3<float>{c.u[1], c.u[2], c.u[3]}, env.dyn);
   if (!state_finite(nx)) return 2;
   x = nx;
   return 0;
+}
+
+template <typename Pert>
+__device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, float (&up)[4], int j,
+                                           const RolloutEnv<float>& env, const Pert& pert) {
+  StepCtl c;
+  if (screen_pre(x, s, up, j, env, pert, c)) return 1;
+  // step 0 is x0 for every sample: its query was answered once per CTA
+  const float d2 = j == 0 ? env.d2_x0
+                          : nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2,
+                                            c.stop2, &env.hint);
+  return screen_post(x, s, c, d2, env);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-shared neighbourhood (main pass): the lanes of a warp step in lockstep
+// and, after the cell-ordered repack, sit close together.  Per step the warp
+// gathers, once, every filtered point within query reach of the bounding box
+// of its live lanes' positions into a shared-memory list (the grid cells
+// overlapping the box, their point blocks read with coalesced 16-byte loads
+// by all 32 lanes), and every live lane scans that list with packed FP32x2
+// arithmetic -- the same distances, in the same sq3f shape, as the per-lane
+// branch-and-bound query, so the result is the same exact minimum (with the
+// same early stop below stop2) and every screening cost is unchanged.  No
+// data-dependent per-lane tree walk: the scan is warp-uniform.  A list past
+// kListCap points falls back to the per-lane query for that step.
+#ifndef AMPPI_WARP_LIST
+#define AMPPI_WARP_LIST 0
+#endif
+#ifndef AMPPI_LIST_CAP
+#define AMPPI_LIST_CAP 256
+#endif
+constexpr int kListCap = AMPPI_LIST_CAP;
+constexpr int kListStride = kListCap + 2;  // (+ one +inf pad for an odd count)
+
+// float -> int with the same order (for the integer warp reductions)
+__device__ __forceinline__ int ford(float f) {
+  const int b = __float_as_int(f);
+  return b >= 0 ? b : b ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float iford(int b) { return __int_as_float(b >= 0 ? b : b ^ 0x7FFFFFFF); }
+
+// Returns false when the neighbourhood overflows the list (every lane then
+// answers its own query); else d2 holds each live lane's squared clearance.
+__device__ __forceinline__ bool warp_list_query(const RolloutEnv<float>& env, bool live, V3<float> p, float stop2,
+                                                float* __restrict__ lx, float* __restrict__ ly,
+                                                float* __restrict__ lz, float& d2) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const float kInf = __int_as_float(0x7f800000);
+  d2 = kInf;
+  const GridMeta& g = env.grid;
+  if (g.dims[0] == 0) return true;  // no points: every query returns +inf
+  // bounding box of the live lanes' positions
+  const int blx = __reduce_min_sync(kFull, live ? ford(p.x) : 0x7FFFFFFF);
+  const int bly = __reduce_min_sync(kFull, live ? ford(p.y) : 0x7FFFFFFF);
+  const int blz = __reduce_min_sync(kFull, live ? ford(p.z) : 0x7FFFFFFF);
+  const int bhx = __reduce_max_sync(kFull, live ? ford(p.x) : static_cast<int>(0x80000000));
+  const int bhy = __reduce_max_sync(kFull, live ? ford(p.y) : static_cast<int>(0x80000000));
+  const int bhz = __reduce_max_sync(kFull, live ? ford(p.z) : static_cast<int>(0x80000000));
+  const float lox = iford(blx), loy = iford(bly), loz = iford(blz);
+  const float hix = iford(bhx), hiy = iford(bhy), hiz = iford(bhz);
+  // a point belongs to the list when its squared gap to the box is below the
+  // query reach (with a relative margin far above FP32 rounding: extra points
+  // never change a minimum)
+  const float lim2m = env.reach2 * 1.0001f;
+  const float reach = sqrt_approx(lim2m) * 1.001f + 1e-3f * g.h_f;
+  auto cell_lo = [&](float v, int a) {
+    return max(0, __float2int_rd((v - reach - g.origin_f[a]) * g.inv_h_f));
+  };
+  auto cell_hi = [&](float v, int a) {
+    return min(g.dims[a] - 1, __float2int_rd((v + reach - g.origin_f[a]) * g.inv_h_f));
+  };
+  const int cx0 = cell_lo(lox, 0), cx1 = cell_hi(hix, 0);
+  const int cy0 = cell_lo(loy, 1), cy1 = cell_hi(hiy, 1);
+  const int cz0 = cell_lo(loz, 2), cz1 = cell_hi(hiz, 2);
+  if (cx0 > cx1 || cy0 > cy1 || cz0 > cz1) return true;  // the region misses the grid
+  const int ny = cy1 - cy0 + 1, nz = cz1 - cz0 + 1;
+  const int ncells = (cx1 - cx0 + 1) * ny * nz;
+  const int p1 = g.dims[1] + 2, p2 = g.dims[2] + 2;
+  int n = 0;  // warp-uniform list length
+  for (int c0 = 0; c0 < ncells; c0 += 32) {
+    const int c = c0 + lane;
+    bool occ = false;
+    int cell = 0;
+    if (c < ncells) {
+      const int cz = cz0 + c % nz, cy = cy0 + (c / nz) % ny, cx = cx0 + c / (nz * ny);
+      occ = (__ldg(env.gnbr + ((cx + 1) * p1 + (cy + 1)) * p2 + (cz + 1)) & kNbrCenter) != 0u;
+      cell = (cx * g.dims[1] + cy) * g.dims[2] + cz;
+    }
+    unsigned m = __ballot_sync(kFull, occ);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int cc = __shfl_sync(kFull, cell, src);
+      const uint32_t r0 = __ldg(&env.grec[2 * cc].x);
+      const uint32_t k0 = r0 & 0xFFFFu, k1 = k0 + (r0 >> 16);
+      const uint32_t bmax = (k1 - 1) / kPointBlock;
+      for (uint32_t b0 = k0 / kPointBlock; b0 <= bmax; b0 += 32) {
+        const uint32_t b = b0 + lane;
+        float4 X = make_float4(0.f, 0.f, 0.f, 0.f), Y = X, Z = X;
+        if (b <= bmax) {
+          X = __ldg(env.gpts + 3 * b);
+          Y = __ldg(env.gpts + 3 * b + 1);
+          Z = __ldg(env.gpts + 3 * b + 2);
+        }
+        const float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w}, zs[4] = {Z.x, Z.y, Z.z, Z.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t idx = kPointBlock * b + t;
+          bool in = b <= bmax && idx >= k0 && idx < k1;
+          if (in) {
+            const float gx = fmaxf(fmaxf(lox - xs[t], xs[t] - hix), 0.f);
+            const float gy = fmaxf(fmaxf(loy - ys[t], ys[t] - hiy), 0.f);
+            const float gz = fmaxf(fmaxf(loz - zs[t], zs[t] - hiz), 0.f);
+            in = sq3f(gx, gy, gz) < lim2m;
+          }
+          const unsigned bal = __ballot_sync(kFull, in);
+          const int pos = n + __popc(bal & ((1u << lane) - 1u));
+          if (in && pos < kListCap) {
+            lx[pos] = xs[t];
+            ly[pos] = ys[t];
+            lz[pos] = zs[t];
+          }
+          n += __popc(bal);
+        }
+      }
+    }
+  }
+  AMPPI_STAT(75, lane == 0 ? 1 : 0);
+  AMPPI_STAT(76, lane == 0 ? n : 0);
+  if (n > kListCap) {
+    AMPPI_STAT(77, lane == 0 ? 1 : 0);
+    __syncwarp();
+    return false;
+  }
+  if (lane == 0 && (n & 1)) lx[n] = ly[n] = lz[n] = kInf;  // pad to whole pairs
+  __syncwarp();
+  if (live) {
+    const float2 npx = make_float2(-p.x, -p.x), npy = make_float2(-p.y, -p.y), npz = make_float2(-p.z, -p.z);
+    float best = kInf;
+    for (int i = 0; i < n; i += 2) {
+      const float2 dx = __fadd2_rn(*reinterpret_cast<const float2*>(lx + i), npx);
+      const float2 dy = __fadd2_rn(*reinterpret_cast<const float2*>(ly + i), npy);
+      const float2 dz = __fadd2_rn(*reinterpret_cast<const float2*>(lz + i), npz);
+      const float2 dd = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+      best = fminf(best, fminf(dd.x, dd.y));
+      if (best < stop2) break;
+    }
+    d2 = best;
+  }
+  __syncwarp();  // the list is rewritten by the next step's gather
+  return true;
 }
 
 // Main screening pass with lane compaction: samples [k1, K) of one instance
@@ -289,6 +451,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   __shared__ int s_k[kT];
   __shared__ int s_wcount[2][kT / 32];
   __shared__ uint32_t s_bcnt[64], s_boff[64];  // cell-order buckets of the repack
+#if AMPPI_WARP_LIST
+  __shared__ __align__(16) float s_list[kT / 32][3][kListStride];  // per-warp neighbourhood lists (x | y | z)
+#endif
   if (threadIdx.x < 64) s_bcnt[threadIdx.x] = 0u;
   const int k_n = kend - kb0;
   const int tiles = (k_n + kT - 1) / kT;
@@ -385,6 +550,30 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   int round = 0;
   for (int j0 = 0; j0 < N; j0 += kCompact, ++round) {
     const int j1 = min(j0 + kCompact, N);
+#if AMPPI_WARP_LIST
+    // warp-synchronous steps: every lane runs the loop (dead lanes idle) so
+    // the warp can gather one neighbourhood list per step for its live lanes
+    float* wl = &s_list[warp][0][0];
+    for (int j = j0; j < j1; ++j) {
+      if (!__any_sync(0xffffffffu, live)) break;
+      StepCtl c;
+      if (live && screen_pre(x, cs, up, j, env, pr, c)) {
+        out[k] = 3.4028234663852886e38f;
+        live = false;
+      }
+      float d2 = env.d2_x0;  // step 0 is x0 for every sample: answered once per CTA
+      if (j > 0 && !warp_list_query(env, live, x.p, c.stop2, wl, wl + kListStride, wl + 2 * kListStride, d2) &&
+          live)
+        d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2, c.stop2, &env.hint);
+      if (live) {
+        const int st = screen_post(x, cs, c, d2, env);
+        if (st) {
+          out[k] = st == 1 ? 3.4028234663852886e38f : __int_as_float(0x7f800000);
+          live = false;
+        }
+      }
+    }
+#else
     if (live) {
       for (int j = j0; j < j1; ++j) {
         const int st = screen_step(x, cs, up, j, env, pr);
@@ -395,6 +584,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         }
       }
     }
+#endif
     if (j1 >= N) break;
     const unsigned bal = __ballot_sync(0xffffffffu, live);
     int* wc = s_wcount[round & 1];

@@ -1,6 +1,7 @@
 """Formats around the plan path (amppi_cloud_* and the
 debug dumps): byte-for-byte against restatements of the reference writers
-(io.cpp:24-99) and exact round trips.  CPU only (no device needed)."""
+(io.cpp:24-99) and exact round trips; the last test runs them through the
+device path (frames -> files -> buffer -> device snapshot + plan -> dumps)."""
 import numpy as np
 import pytest
 
@@ -94,3 +95,55 @@ def test_anchors_csv_matches_reference_writer(oracle, tmp_path):
                 pt.append(v)
             ref.append("5,%d,%.17g,%.17g,%.17g" % (a, *pt))
     assert p.read_text() == "\n".join(ref) + "\n"  # write_anchors_csv (io.cpp:78-99)
+
+
+@pytest.mark.gpu
+def test_cloud_files_through_the_device_path(oracle, tmp_path):
+    """The formats in the device job: LiDAR frames written as text and binary
+    cloud files, read back into a PointCloudBuffer, planned on the device; the
+    device snapshot's partition.csv is byte-equal to the one written from the
+    oracle's snapshot of the same frames, and the anchors.csv dump of the
+    device plan matches the oracle plan's dump to 1e-12."""
+    from paper_2509_17340_b200 import ControlInput, GoalSpec, Planner, PointCloudBuffer, State
+    from test_plan_parity import make_cfg
+
+    sc = oracle.scene(1, 3)
+    pose = np.array([6.0, 0.5, 2.0, 1, 0, 0, 0, 2.0, 0, 0], dtype=np.float64)
+    buf = PointCloudBuffer(8)
+    for f in range(8):
+        pts = sc.lidar(pose, 900 + f)
+        p = tmp_path / f"frame{f}.{'bin' if f % 2 else 'cloud'}"
+        aio.write_cloud(str(p), pts, frame_id=f, binary=bool(f % 2))
+        back, fid = aio.read_cloud(str(p))
+        assert fid == f and np.array_equal(back, pts)
+        buf.push(back)
+    cloud = buf.points()
+    cfg = make_cfg(4, 2, K=128, N=25)
+    x = State.from_array(pose)
+    goal = GoalSpec.facing(tuple(pose[:3]), (40.0, 0.0, 2.0))
+    with Planner(cfg, max_points=1 << 16) as planner:
+        snap = planner.build_snapshot(buf, x, cfg.r_max, f64=True)
+        dev = snap.download()
+        plan = planner.plan_step(x, goal, snap, None, ControlInput(9.81), 7, 3)
+    osnap = oracle.snapshot(cloud, pose, cfg.r_max)
+    orng = osnap.get()["ranges"]
+    aio.write_partition_csv(str(tmp_path / "dev.csv"), dev["ranges"])
+    aio.write_partition_csv(str(tmp_path / "ora.csv"), orng)
+    assert (tmp_path / "dev.csv").read_bytes() == (tmp_path / "ora.csv").read_bytes()
+    o = oracle.plan(osnap, oracle.config(cfg), pose, goal.p_goal, goal.v_goal, goal.q_goal, None,
+                    [9.81, 0, 0, 0], 7, 3)
+
+    class OPlan:
+        anchors = [type("A", (), {"refined_endpoint": r}) for r in o["anchor_refined"]]
+        guides = o["guide_coeffs"].reshape(-1, 3, 6)
+
+    T = cfg.mppi.horizon * cfg.mppi.dt
+    aio.write_anchors_csv(str(tmp_path / "dev_a.csv"), 7, plan, T, 10)
+    aio.write_anchors_csv(str(tmp_path / "ora_a.csv"), 7, OPlan, T, 10)
+    dl = (tmp_path / "dev_a.csv").read_text().splitlines()
+    ol = (tmp_path / "ora_a.csv").read_text().splitlines()
+    assert dl[0] == ol[0] and len(dl) == len(ol)
+    dv = np.array([[float(v) for v in ln.split(",")] for ln in dl[1:]])
+    ov = np.array([[float(v) for v in ln.split(",")] for ln in ol[1:]])
+    assert np.array_equal(dv[:, :2], ov[:, :2])
+    assert np.max(np.abs(dv[:, 2:] - ov[:, 2:]) / np.maximum(1.0, np.abs(ov[:, 2:]))) <= 1e-12
