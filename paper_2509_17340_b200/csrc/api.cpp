@@ -451,6 +451,12 @@ int create_impl(amppi_ctx* ctx) {
     pl.pos64 = static_cast<double*>(p);
     CK(A.alloc(&p, jobs * sizeof(TrajSums)));
     pl.tsum = static_cast<TrajSums*>(p);
+    CK(A.alloc(&p, jobs * N * sizeof(double)));
+    pl.col_terms = static_cast<double*>(p);
+    CK(A.alloc(&p, jobs * N * sizeof(uint32_t)));
+    pl.col_work = static_cast<uint32_t*>(p);
+    CK(A.alloc(&p, kMaxChunks * sizeof(unsigned int)));
+    pl.col_count = static_cast<unsigned int*>(p);
   }
   CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(int32_t)));
   pl.done = static_cast<int32_t*>(p);
@@ -585,6 +591,9 @@ int run_chunk(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, int64_t 
   const int64_t sm0 = s0 * dc.M, smc = static_cast<int64_t>(in.S) * dc.M;
   pl.pos64 += 4 * sm0 * dc.N * 4;
   pl.tsum += 4 * sm0;
+  pl.col_terms += 4 * sm0 * dc.N;
+  pl.col_work += 4 * sm0 * dc.N;
+  pl.col_count += chunk;
   pl.pos_cap = std::min<int64_t>(4 * smc, ctx->pl.pos_cap);
   cudaError_t e = launch_snapshot(in, P, dc, max_pts_scene, st, &ctx->timer);
   if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_snapshot");

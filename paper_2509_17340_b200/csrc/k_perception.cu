@@ -23,6 +23,7 @@
 // compaction + world transform, collision grid (bitonic sort by (cell, Morton
 // code), 16-point leaves with float boxes, cell records, padded neighbour
 // masks, FP32 point blocks for the packed query).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -195,6 +196,79 @@ __global__ void __launch_bounds__(256) k_key_points(BatchIn in, Perception P) {
         atomicOr(P.flags, kFlagCandOverflow);  // a lost candidate could drop a cell's point
     }
   }
+}
+
+// The same keying with the per-cell minimum first reduced inside a thread-block
+// cluster: every CTA keeps the scene's whole 7200-cell table in shared memory
+// (shared-memory 64-bit atomicMin per point, on chip), and after a cluster
+// barrier CTA r of the cluster reduces cells [900 r, 900 r + 900) over the 8
+// tables through distributed shared memory (remote loads) and merges the
+// non-empty ones into the global table.  A scene of P points then costs P
+// on-chip atomics and 7200 global ones per cluster instead of P contended
+// global atomics.  (A 64-bit atomicMin on a remote CTA's shared memory is not
+// a native operation on sm_100a: the compiler's fallback applies it to the
+// issuing CTA's own table -- measured, lost updates -- hence local tables and
+// remote loads.)  Candidates for the index tie-break are logged as in
+// k_key_points: a point that was not <= its CTA's running minimum cannot be
+// the global minimum.
+__device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total);
+
+constexpr int kKeyCluster = 8;
+constexpr int kKeyCellsPerRank = kCells / kKeyCluster;  // 900
+constexpr int kKeyThreads = 512;
+static_assert(kCells % kKeyCluster == 0, "cells split evenly over the cluster");
+
+__global__ void __cluster_dims__(kKeyCluster, 1, 1) __launch_bounds__(kKeyThreads)
+    k_key_points_cluster(BatchIn in, Perception P, int clusters_per_scene) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char key_smem[];
+  unsigned long long* tab = reinterpret_cast<unsigned long long*>(key_smem);  // [kCells]
+  __shared__ PoseFrame pose;
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  const int s = blockIdx.y;
+  for (int c = threadIdx.x; c < kCells; c += blockDim.x) tab[c] = kEmptyCell;
+  if (threadIdx.x == 0) pose = load_pose(in.poses + 10 * s);
+  __syncthreads();
+  const int64_t b = in.offsets[s], e = in.offsets[s + 1];
+  const int64_t stride = static_cast<int64_t>(clusters_per_scene) * kKeyCluster * blockDim.x;
+  // block-uniform loop: each iteration's candidates get their log slots from
+  // one atomicAdd per CTA (a block scan), not one per warp
+  __shared__ uint32_t warp_sums[kKeyThreads / 32];
+  __shared__ uint32_t n_iter;
+  __shared__ unsigned long long log_base;
+  for (int64_t g0 = b + static_cast<int64_t>(blockIdx.x) * blockDim.x; g0 < e; g0 += stride) {
+    const int64_t g = g0 + threadIdx.x;
+    int f = 0;
+    uint64_t bits = 0;
+    bool cand = false;
+    if (g < e && key_point(pose, load_point(in, g), in.r_max, f, bits))
+      cand = atomicMin(tab + f, bits) >= bits;  // may be the cell minimum: log for the index tie-break
+    const uint32_t pos = block_exclusive_scan(cand ? 1u : 0u, warp_sums, &n_iter);
+    if (threadIdx.x == 0) log_base = n_iter ? atomicAdd(P.cand_count, static_cast<unsigned long long>(n_iter)) : 0ull;
+    __syncthreads();
+    if (cand) {
+      const unsigned long long slot = log_base + pos;
+      if (slot < static_cast<unsigned long long>(P.cand_cap))
+        P.cand[slot] = Candidate{static_cast<uint32_t>(s * kCells + f), static_cast<uint32_t>(g - b), bits};
+      else
+        atomicOr(P.flags, kFlagCandOverflow);  // a lost candidate could drop a cell's point
+    }
+    __syncthreads();  // log_base / n_iter are rewritten next iteration
+  }
+  cl.sync();  // every table of the cluster is final
+  uint64_t* __restrict__ cell_r = P.cell_r + static_cast<int64_t>(s) * kCells;
+  for (int c = rank * kKeyCellsPerRank + threadIdx.x; c < static_cast<int>(rank + 1) * kKeyCellsPerRank;
+       c += blockDim.x) {
+    unsigned long long m = tab[c];
+#pragma unroll
+    for (int q = 1; q < kKeyCluster; ++q) {
+      const unsigned long long v = cl.map_shared_rank(tab, (rank + q) % kKeyCluster)[c];
+      m = v < m ? v : m;
+    }
+    if (m != kEmptyCell) atomicMin(reinterpret_cast<unsigned long long*>(cell_r + c), m);
+  }
+  cl.sync();  // no CTA leaves while the others read its table
 }
 
 __global__ void __launch_bounds__(256) k_resolve_ties(Perception P) {
@@ -751,6 +825,9 @@ cudaError_t init_kernel_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_finalize_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(FinalizeSmem)));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_key_points_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kCells * sizeof(unsigned long long)));
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_snapshot_scene, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(sizeof(FinalizeSmem)));
 }
@@ -766,13 +843,13 @@ cudaError_t launch_snapshot(const BatchIn& in, const Perception& P, const DevCon
   }
   cudaError_t err = cudaMemsetAsync(P.cand_count, 0, sizeof(unsigned long long), st);
   if (err != cudaSuccess) return err;
-  const int threads = 256;
-  int64_t blocks_x = (max_points_per_scene + threads - 1) / threads;
-  if (blocks_x < 1) blocks_x = 1;
-  if (blocks_x > 4096) blocks_x = 4096;
   {
+    // clusters per scene: ~8 points per thread, at most ~2 waves of clusters
+    int64_t cps = (max_points_per_scene + 8 * kKeyCluster * kKeyThreads - 1) / (8 * kKeyCluster * kKeyThreads);
+    cps = cps < 1 ? 1 : (cps > 64 ? 64 : cps);
     TimedRegion t(timer, "k_key_points", st);
-    k_key_points<<<dim3(static_cast<unsigned>(blocks_x), in.S), threads, 0, st>>>(in, P);
+    k_key_points_cluster<<<dim3(static_cast<unsigned>(cps * kKeyCluster), in.S), kKeyThreads,
+                           kCells * sizeof(unsigned long long), st>>>(in, P, static_cast<int>(cps));
   }
   {
     TimedRegion t(timer, "k_resolve_ties", st);

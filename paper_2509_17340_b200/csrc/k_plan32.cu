@@ -185,6 +185,85 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
                                : __int_as_float(0x7f800000);
 }
 
+// Bound pass: samples [k_lo, k_lo + B) of G instances per warp (B = 32 / G
+// lanes each), full horizon, no abort -- their minimum is the abort bound of
+// the main pass.  Packing several instances into a warp cuts the warps of the
+// pass by G: every lane's collision queries diverge anyway (each lane walks
+// its own cells and leaves), so a warp's time hardly depends on whether its
+// lanes share an instance.
+template <int G>
+__global__ void __launch_bounds__(32) k_stage1_bound(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                     const ScreenConsts sc, int iter) {
+  constexpr int B = 32 / G;
+  __shared__ float4 s_unom[G][kMaxN];
+  __shared__ float4 s_guide[G][kMaxN];
+  __shared__ uint64_t s_bar;
+  const int lane = threadIdx.x, g = lane / B;
+  const int64_t SMn = static_cast<int64_t>(in.S) * cfg.M;
+  const int64_t smi0 = static_cast<int64_t>(blockIdx.x) * G;
+  const int n_inst = static_cast<int>(SMn - smi0 < G ? SMn - smi0 : G);
+  const int N = cfg.N;
+  if (lane == 0) {  // the instances' nominal and guide tables: bulk async copies into smem
+    mbar_init(&s_bar, 1);
+    mbar_expect_tx(&s_bar, 2u * 16u * static_cast<uint32_t>(N) * static_cast<uint32_t>(n_inst));
+    for (int i = 0; i < n_inst; ++i) {
+      bulk_copy_g2s(s_unom[i], pl.unom32 + (smi0 + i) * N, 16u * N, &s_bar);
+      bulk_copy_g2s(s_guide[i], pl.guide32 + (smi0 + i) * N, 16u * N, &s_bar);
+    }
+  }
+  __syncwarp();
+  mbar_wait(&s_bar, 0);
+  if (g >= n_inst) return;
+  const int64_t smi = smi0 + g;
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  const int k = cfg.k_lo + lane % B;
+  float* out = pl.cost32 + smi * cfg.K + k;
+  if (!pl.alive[smi]) {
+    *out = __int_as_float(0x7f800000);
+    return;
+  }
+  RolloutEnv<float> env;
+  env.unom = reinterpret_cast<const float*>(s_unom[g]);
+  env.guide = s_guide[g];
+  env.N = N;
+  env.dyn = sc.dyn;
+  const double* gl = in.goals + 10 * s;
+  env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
+  env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
+  env.q_p = sc.q_p;
+  env.q_v = sc.q_v;
+  env.q_q = sc.q_q;
+  env.cs = sc.cs;
+  env.ca = sc.ca;
+  env.cdmin = sc.cdmin;
+  env.cdmax = sc.cdmax;
+  env.grid = P.grid[s];
+  env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+  env.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  env.gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
+  env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
+  env.has_guide = true;
+  env.abort_above = __int_as_float(0x7f800000);
+  env.wq_track = sc.wq_track;
+  env.wq_vnorm = sc.wq_vnorm;
+  env.wq_c = sc.wq_c;
+  env.wq_cd = sc.wq_cd;
+  env.reach2 = sc.reach2;
+  env.band = sc.band;
+  const double* xs = in.states + 10 * s;
+  St<float> x0;
+  x0.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x0.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
+  x0.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  const PertRngF pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                    sc.sigma[0], sc.sigma[1], sc.sigma[2], sc.sigma[3]};
+  const CostSums<float> cs = rollout_costs(x0, env, pr);
+  *out = cs.valid ? screen_store(stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd), cs.amb)
+                  : __int_as_float(0x7f800000);
+}
+
 // One screening step j of a rollout (the loop body of rollout_costs<float>):
 // costs on states[j], perturbed clamped control, control costs, the
 // partial-cost bound, RK4.  Returns 0 (continue), 1 (aborted), 2 (invalid).
@@ -433,6 +512,11 @@ constexpr int kScreenThreads = 128;
 #define AMPPI_MAIN_COMPACT 10
 #endif
 constexpr int kMainThreads = AMPPI_MAIN_THREADS, kMainMinBlocks = AMPPI_MAIN_MINBLOCKS;
+#ifndef AMPPI_BOUND_SAMPLES
+#define AMPPI_BOUND_SAMPLES 32
+#endif
+constexpr int kBoundSamples = AMPPI_BOUND_SAMPLES;  // 32, 16, 8 or 4
+static_assert(32 % kBoundSamples == 0, "bound samples divide a warp");
 constexpr int kMainCompact = AMPPI_MAIN_COMPACT;
 constexpr int kStateWords = 22;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint amb
 
@@ -882,10 +966,17 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     return cudaGetLastError();
   }
   unom32();
-  const int k1 = 32;  // bound samples (best of 8-64 measured)
+  // bound samples per instance: AMPPI_BOUND_SAMPLES of every instance, 32 / that
+  // instances per warp (injected perturbations: 32, one instance per warp)
+  const int k1 = in.injected ? 32 : kBoundSamples;
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
-    kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
+    if (in.injected || kBoundSamples == 32) {
+      kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
+    } else {
+      constexpr int G = 32 / kBoundSamples;
+      k_stage1_bound<G><<<static_cast<unsigned>((SM + G - 1) / G), 32, 0, st>>>(in, P, pl, cfg, sc, iter);
+    }
   }
   TimedRegion t(timer, "k_stage1_f32", st);
   if (in.injected) {
@@ -896,7 +987,10 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     // the better live samples pack: 224 threads (5 CTAs per SM; the whole
     // K = 256 main pass of an instance in one CTA) beat 128 (9 per SM) by 4%,
     // 64 threads lose 15% (C5, measured); 128 when that covers the samples.
-    if (kr - k1 > 128) {
+    if (kBoundSamples < 32 && kr - k1 > kMainThreads && kr - k1 <= 256) {  // (experiment builds) one 256-thread CTA
+      k_stage1_f32c<4, kMainCompact, 256><<<static_cast<unsigned>(SM), 256, 0, st>>>(in, P, pl, cfg, sc, iter, k1,
+                                                                                    kr, k1);
+    } else if (kr - k1 > 128) {
       const int tiles = (kr - k1 + kMainThreads - 1) / kMainThreads;
       k_stage1_f32c<kMainMinBlocks, kMainCompact, kMainThreads>
           <<<static_cast<unsigned>(SM * tiles), kMainThreads, 0, st>>>(in, P, pl, cfg, sc, iter, k1, kr, k1);

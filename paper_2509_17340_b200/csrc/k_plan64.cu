@@ -384,6 +384,11 @@ __global__ void __launch_bounds__(128) k_stage1_f64(BatchIn in, Perception P, Pl
 // ---------------------------------------------------------------------------
 constexpr int kSupportThreads = 128;
 
+#ifndef AMPPI_COL_PASSES
+#define AMPPI_COL_PASSES 1
+#endif
+constexpr bool kColPasses = AMPPI_COL_PASSES != 0;  // classify / query / sum form of the FP64 collision terms
+
 struct UpdateScratch {  // global, per (scene, instance): [K] each
   uint32_t* cand_k;
   double* cand_s;
@@ -1038,6 +1043,159 @@ __global__ void __launch_bounds__(128, AMPPI_COL_MINB) k_refine_col(BatchIn in, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Collision terms of deferred FP64 trajectories (the refined support and the
+// stage-II re-rollouts), as three passes over (trajectory, step) queries:
+//   k_col_classify  one thread per trajectory: a step whose padded neighbour
+//                   mask is empty has nothing within d_max (term 0); the
+//                   others join a work list as runs of <= kColRun steps;
+//   k_col_query     one thread per run: the exact FP64 nearest distances
+//                   (nearest_sq_exact, hint-chained) and collision terms;
+//   k_*_col_sum     one thread per trajectory: the N terms summed in step
+//                   order (the reference's sum over states[0..N-1]).
+// Every lane of the query pass carries a real query; the former warp per
+// trajectory (lane = step) idled beside the trajectory's empty steps and ran
+// 4.4 of 32 lanes per instruction.  Terms and sums are the same FP64 values.
+struct ColJobs {
+  const uint2* pairs;                    // refine: (instance, slot) per trajectory; stage II: null (w = instance)
+  const unsigned long long* pair_count;  // refine: trajectories listed
+  int64_t cap;                           // trajectories with deferred positions
+};
+
+__device__ __forceinline__ bool col_traj(const ColJobs& J, const Plan& pl, int64_t w, int64_t* smi) {
+  if (J.pairs) {
+    if (w >= static_cast<int64_t>(min(*J.pair_count, static_cast<unsigned long long>(J.cap)))) return false;
+    *smi = J.pairs[w].x;
+    return pl.tsum[w].valid != 0;
+  }
+  if (w >= J.cap) return false;
+  *smi = w;
+  return pl.alive[w] && pl.tsum[w].valid;
+}
+
+#ifndef AMPPI_COL_RUN
+#define AMPPI_COL_RUN 4
+#endif
+constexpr int kColRun = AMPPI_COL_RUN;  // consecutive steps per query work item (hint chained)
+
+// One thread per trajectory: steps with an empty neighbour mask get term 0;
+// the others are listed as runs of up to kColRun consecutive steps, packed
+// (trajectory << 10 | first step << 4 | run length).
+__global__ void __launch_bounds__(128) k_col_classify(Perception P, Plan pl, DevConfig cfg, ColJobs J,
+                                                      uint32_t* __restrict__ work, unsigned int* __restrict__ count) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t smi;
+  if (!col_traj(J, pl, w, &smi)) return;
+  const int s = static_cast<int>(smi / cfg.M);
+  const GridMeta g = P.grid[s];
+  const uint32_t* nbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  int run0 = -1, run_len = 0;
+  auto flush = [&]() {
+    if (run_len > 0) work[atomicAdd(count, 1u)] = (static_cast<uint32_t>(w) << 10) | (run0 << 4) | run_len;
+    run_len = 0;
+  };
+  for (int j = 0; j < cfg.N; ++j) {
+    const int64_t i = w * cfg.N + j;
+    bool near = false;
+    if (g.dims[0] != 0) {  // the cell test of nearest_sq_exact
+      const double* q = pl.pos64 + 4 * i;
+      const int cx = static_cast<int>(floor((q[0] - g.origin[0]) * g.inv_h));
+      const int cy = static_cast<int>(floor((q[1] - g.origin[1]) * g.inv_h));
+      const int cz = static_cast<int>(floor((q[2] - g.origin[2]) * g.inv_h));
+      near = nbr_mask(g, nbr, cx, cy, cz) != 0u;
+    }
+    if (!near) {
+      pl.col_terms[i] = 0.0;  // no point within d_max: collision_term(+inf) = 0
+      flush();
+      continue;
+    }
+    if (run_len == 0) run0 = j;
+    if (++run_len == kColRun) flush();
+  }
+  flush();
+}
+
+// One thread per listed run: the exact FP64 queries of consecutive steps, each
+// seeded with the previous step's nearest point (an upper bound that prunes
+// most boxes; the result is the exact minimum either way).
+__global__ void __launch_bounds__(128) k_col_query(Perception P, Plan pl, DevConfig cfg, ColJobs J,
+                                                   const uint32_t* __restrict__ work,
+                                                   const unsigned int* __restrict__ count) {
+  const unsigned int n = *count;
+  for (unsigned int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const uint32_t item = work[q];
+    const int64_t w = item >> 10;
+    const int j0 = (item >> 4) & 63, len = item & 15;
+    const int64_t smi = J.pairs ? static_cast<int64_t>(J.pairs[w].x) : w;
+    const int s = static_cast<int>(smi / cfg.M);
+    const GridMeta g = P.grid[s];
+    const uint4* rec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+    const uint32_t* nbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+    const uint4* leaves = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
+    const double* pts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
+    uint32_t hint = kNoHint;
+    for (int j = j0; j < j0 + len; ++j) {
+      const int64_t i = w * cfg.N + j;
+      const double* pp = pl.pos64 + 4 * i;
+      const double d2 = nearest_sq_exact(g, rec, nbr, leaves, pts, V3<double>{pp[0], pp[1], pp[2]},
+                                         cfg.col_d_max * cfg.col_d_max, cfg.col_d_min * cfg.col_d_min, &hint);
+      pl.col_terms[i] = collision_term(sqrt(d2), cfg.col_scale, cfg.col_slope, cfg.col_d_min, cfg.col_d_max);
+    }
+  }
+}
+
+__device__ __forceinline__ double col_sum(const Plan& pl, int64_t w, int N) {
+  double col = 0.0;
+  for (int j = 0; j < N; ++j) col = col + pl.col_terms[w * N + j];
+  return col;
+}
+
+__global__ void __launch_bounds__(128) k_refine_col_sum(Plan pl, DevConfig cfg, UpdateScratch us, int64_t cap) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= static_cast<int64_t>(min(*us.pair_count, static_cast<unsigned long long>(cap)))) return;
+  const uint2 pr = us.pairs[w];
+  const TrajSums t = pl.tsum[w];
+  double val = __longlong_as_double(0x7ff0000000000000ll);
+  if (t.valid) {
+    const double col = col_sum(pl, w, cfg.N);
+    val = ((cfg.q_track * t.trk + cfg.q_vnorm * t.vn) + (cfg.q_c * t.mag + cfg.q_c_delta * t.rate)) + (t.goal + col);
+  }
+  us.cand_s[static_cast<int64_t>(pr.x) * cfg.K + pr.y] = val;
+}
+
+__global__ void __launch_bounds__(128) k_stage2_col_sum(BatchIn in, Plan pl, DevConfig cfg) {
+  const int64_t smi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
+  const TrajSums t = pl.tsum[smi];
+  double st2 = __longlong_as_double(0x7ff0000000000000ll);
+  bool valid = false;
+  double bd[5] = {0, 0, 0, 0, 0};
+  if (pl.alive[smi] && t.valid) {
+    const double col = col_sum(pl, smi, cfg.N);
+    st2 = t.goal + col;  // stage2_cost (costs.hpp:139-147)
+    valid = isfinite(st2);
+    bd[0] = cfg.q_track * t.trk;
+    bd[1] = cfg.q_vnorm * t.vn;
+    bd[2] = cfg.q_c * t.mag + cfg.q_c_delta * t.rate;
+    bd[3] = t.goal;
+    bd[4] = col;
+  }
+  pl.stage2[smi] = st2;
+  pl.valid[smi] = valid ? 1 : 0;
+  for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
+}
+
+// classify + query passes for `jobs` (an upper bound of the) trajectories
+void launch_col_queries(const Perception& P, const Plan& pl, const DevConfig& cfg, const ColJobs& J, int64_t jobs,
+                        cudaStream_t st) {
+  cudaMemsetAsync(pl.col_count, 0, sizeof(unsigned int), st);
+  if (jobs == 0) return;
+  k_col_classify<<<static_cast<unsigned>((jobs + 127) / 128), 128, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
+  const int64_t q = jobs * ((cfg.N + kColRun - 1) / kColRun + 1);  // work items (upper bound)
+  const int64_t b = std::min<int64_t>((q + 127) / 128, static_cast<int64_t>(device_sms()) * 16);
+  k_col_query<<<static_cast<unsigned>(b), 128, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
+}
+
 __global__ void k_select(Plan pl, DevConfig cfg, int S) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
@@ -1146,8 +1304,13 @@ static void launch_support_refine(const BatchIn& in, const Perception& P, const 
   }
   {
     TimedRegion t(timer, "k_refine_col", st);
-    const int64_t b = (jobs * 32 + 127) / 128;
-    k_refine_col<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 128, 0, st>>>(in, P, pl, cfg, us);
+    if (kColPasses) {
+      launch_col_queries(P, pl, cfg, ColJobs{us.pairs, us.pair_count, pl.pos_cap}, jobs, st);
+      k_refine_col_sum<<<static_cast<unsigned>((jobs + 127) / 128), 128, 0, st>>>(pl, cfg, us, pl.pos_cap);
+    } else {
+      const int64_t b = (jobs * 32 + 127) / 128;
+      k_refine_col<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 128, 0, st>>>(in, P, pl, cfg, us);
+    }
   }
   if (total > pl.pos_cap) {
     TimedRegion t(timer, "k_refine", st);
@@ -1169,7 +1332,12 @@ cudaError_t launch_plan_finish(const BatchIn& in, const Perception& P, const Pla
   }
   {
     TimedRegion t(timer, "k_stage2_col", st);
-    k_stage2_col<<<(SM * 32 + 127) / 128, 128, 0, st>>>(in, P, pl, cfg);
+    if (kColPasses) {
+      launch_col_queries(P, pl, cfg, ColJobs{nullptr, nullptr, SM}, SM, st);
+      k_stage2_col_sum<<<(SM + 127) / 128, 128, 0, st>>>(in, pl, cfg);
+    } else {
+      k_stage2_col<<<(SM * 32 + 127) / 128, 128, 0, st>>>(in, P, pl, cfg);
+    }
   }
   {
     TimedRegion t(timer, "k_select", st);

@@ -164,6 +164,9 @@ struct Plan {
   double* pos64;               // [pos_cap*N*4]
   TrajSums* tsum;              // [pos_cap]
   int64_t pos_cap;             // support pairs the split refine handles (pos64/tsum hold max(4*S*M, kLatencyRollouts))
+  double* col_terms;           // [pos_cap*N] per-step collision terms of the deferred trajectories
+  uint32_t* col_work;          // [pos_cap*N] (trajectory*N + step) queries with a point within d_max
+  unsigned int* col_count;     // work-list length (one counter per concurrent chunk)
   // per scene
   int32_t* done;               // [S] arrival counter (self-resetting)
   int32_t* winner;             // [S]
