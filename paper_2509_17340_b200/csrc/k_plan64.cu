@@ -1046,11 +1046,11 @@ __global__ void __launch_bounds__(128, AMPPI_COL_MINB) k_refine_col(BatchIn in, 
 // ---------------------------------------------------------------------------
 // Collision terms of deferred FP64 trajectories (the refined support and the
 // stage-II re-rollouts), as three passes over (trajectory, step) queries:
-//   k_col_classify  one thread per trajectory: a step whose padded neighbour
-//                   mask is empty has nothing within d_max (term 0); the
-//                   others join a work list as runs of <= kColRun steps;
-//   k_col_query     one thread per run: the exact FP64 nearest distances
-//                   (nearest_sq_exact, hint-chained) and collision terms;
+//   k_col_classify  one thread per query: a step whose padded neighbour mask
+//                   is empty has nothing within d_max (term 0); the others
+//                   join a work list;
+//   k_col_query     one thread per listed query: the exact FP64 nearest
+//                   distance (nearest_sq_exact) and the collision term;
 //   k_*_col_sum     one thread per trajectory: the N terms summed in step
 //                   order (the reference's sum over states[0..N-1]).
 // Every lane of the query pass carries a real query; the former warp per
@@ -1073,74 +1073,46 @@ __device__ __forceinline__ bool col_traj(const ColJobs& J, const Plan& pl, int64
   return pl.alive[w] && pl.tsum[w].valid;
 }
 
-#ifndef AMPPI_COL_RUN
-#define AMPPI_COL_RUN 4
-#endif
-constexpr int kColRun = AMPPI_COL_RUN;  // consecutive steps per query work item (hint chained)
-
-// One thread per trajectory: steps with an empty neighbour mask get term 0;
-// the others are listed as runs of up to kColRun consecutive steps, packed
-// (trajectory << 10 | first step << 4 | run length).
-__global__ void __launch_bounds__(128) k_col_classify(Perception P, Plan pl, DevConfig cfg, ColJobs J,
+__global__ void __launch_bounds__(256) k_col_classify(Perception P, Plan pl, DevConfig cfg, ColJobs J,
                                                       uint32_t* __restrict__ work, unsigned int* __restrict__ count) {
-  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t w = i / cfg.N;
   int64_t smi;
   if (!col_traj(J, pl, w, &smi)) return;
   const int s = static_cast<int>(smi / cfg.M);
   const GridMeta g = P.grid[s];
-  const uint32_t* nbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
-  int run0 = -1, run_len = 0;
-  auto flush = [&]() {
-    if (run_len > 0) work[atomicAdd(count, 1u)] = (static_cast<uint32_t>(w) << 10) | (run0 << 4) | run_len;
-    run_len = 0;
-  };
-  for (int j = 0; j < cfg.N; ++j) {
-    const int64_t i = w * cfg.N + j;
-    bool near = false;
-    if (g.dims[0] != 0) {  // the cell test of nearest_sq_exact
-      const double* q = pl.pos64 + 4 * i;
-      const int cx = static_cast<int>(floor((q[0] - g.origin[0]) * g.inv_h));
-      const int cy = static_cast<int>(floor((q[1] - g.origin[1]) * g.inv_h));
-      const int cz = static_cast<int>(floor((q[2] - g.origin[2]) * g.inv_h));
-      near = nbr_mask(g, nbr, cx, cy, cz) != 0u;
-    }
-    if (!near) {
-      pl.col_terms[i] = 0.0;  // no point within d_max: collision_term(+inf) = 0
-      flush();
-      continue;
-    }
-    if (run_len == 0) run0 = j;
-    if (++run_len == kColRun) flush();
+  bool near = false;
+  if (g.dims[0] != 0) {  // the cell test of nearest_sq_exact
+    const double* q = pl.pos64 + 4 * i;
+    const int cx = static_cast<int>(floor((q[0] - g.origin[0]) * g.inv_h));
+    const int cy = static_cast<int>(floor((q[1] - g.origin[1]) * g.inv_h));
+    const int cz = static_cast<int>(floor((q[2] - g.origin[2]) * g.inv_h));
+    near = nbr_mask(g, P.grid_nbr + static_cast<int64_t>(s) * kPadCells, cx, cy, cz) != 0u;
   }
-  flush();
+  if (near)
+    work[atomicAdd(count, 1u)] = static_cast<uint32_t>(i);
+  else
+    pl.col_terms[i] = 0.0;  // no point within d_max: collision_term(+inf) = 0
 }
 
-// One thread per listed run: the exact FP64 queries of consecutive steps, each
-// seeded with the previous step's nearest point (an upper bound that prunes
-// most boxes; the result is the exact minimum either way).
 __global__ void __launch_bounds__(128) k_col_query(Perception P, Plan pl, DevConfig cfg, ColJobs J,
                                                    const uint32_t* __restrict__ work,
                                                    const unsigned int* __restrict__ count) {
   const unsigned int n = *count;
   for (unsigned int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-    const uint32_t item = work[q];
-    const int64_t w = item >> 10;
-    const int j0 = (item >> 4) & 63, len = item & 15;
+    const uint32_t i = work[q];
+    const int64_t w = i / cfg.N;
     const int64_t smi = J.pairs ? static_cast<int64_t>(J.pairs[w].x) : w;
     const int s = static_cast<int>(smi / cfg.M);
-    const GridMeta g = P.grid[s];
-    const uint4* rec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
-    const uint32_t* nbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
-    const uint4* leaves = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
-    const double* pts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
+    const double* pp = pl.pos64 + 4 * static_cast<int64_t>(i);
     uint32_t hint = kNoHint;
-    for (int j = j0; j < j0 + len; ++j) {
-      const int64_t i = w * cfg.N + j;
-      const double* pp = pl.pos64 + 4 * i;
-      const double d2 = nearest_sq_exact(g, rec, nbr, leaves, pts, V3<double>{pp[0], pp[1], pp[2]},
-                                         cfg.col_d_max * cfg.col_d_max, cfg.col_d_min * cfg.col_d_min, &hint);
-      pl.col_terms[i] = collision_term(sqrt(d2), cfg.col_scale, cfg.col_slope, cfg.col_d_min, cfg.col_d_max);
-    }
+    const double d2 = nearest_sq_exact(P.grid[s], P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2,
+                                       P.grid_nbr + static_cast<int64_t>(s) * kPadCells,
+                                       P.grid_leaf + static_cast<int64_t>(s) * kCells * 2,
+                                       P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3,
+                                       V3<double>{pp[0], pp[1], pp[2]}, cfg.col_d_max * cfg.col_d_max,
+                                       cfg.col_d_min * cfg.col_d_min, &hint);
+    pl.col_terms[i] = collision_term(sqrt(d2), cfg.col_scale, cfg.col_slope, cfg.col_d_min, cfg.col_d_max);
   }
 }
 
@@ -1189,9 +1161,9 @@ __global__ void __launch_bounds__(128) k_stage2_col_sum(BatchIn in, Plan pl, Dev
 void launch_col_queries(const Perception& P, const Plan& pl, const DevConfig& cfg, const ColJobs& J, int64_t jobs,
                         cudaStream_t st) {
   cudaMemsetAsync(pl.col_count, 0, sizeof(unsigned int), st);
-  if (jobs == 0) return;
-  k_col_classify<<<static_cast<unsigned>((jobs + 127) / 128), 128, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
-  const int64_t q = jobs * ((cfg.N + kColRun - 1) / kColRun + 1);  // work items (upper bound)
+  const int64_t q = jobs * cfg.N;
+  if (q == 0) return;
+  k_col_classify<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
   const int64_t b = std::min<int64_t>((q + 127) / 128, static_cast<int64_t>(device_sms()) * 16);
   k_col_query<<<static_cast<unsigned>(b), 128, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
 }

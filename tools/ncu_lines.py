@@ -1,12 +1,16 @@
 #!/usr/bin/env python
 """Per-source-line summary of an `ncu --import-source on` capture.
 
-  tools/ncu_lines.py <report.ncu-rep> [top]
+  tools/ncu_lines.py <report.ncu-rep> [top]        # per source line
+  tools/ncu_lines.py <report.ncu-rep> --ops         # per SASS opcode + executed FP32 flops
 
 Reads `ncu -i ... --page source --csv --print-source cuda,sass` and prints,
 per CUDA source line (file:line), the share of warp-stall samples, of warp
 instructions executed, the average active threads per executed instruction
-and the two largest stall reasons -- the per-line view behind profiles/."""
+and the two largest stall reasons -- the per-line view behind profiles/.
+--ops reads the SASS page instead: the opcode mix and the FP32 flops the
+kernel executed (FFMA 2, FADD/FMUL 1, packed FFMA2 4, FADD2/FMUL2 2 per
+predicated-on thread instruction)."""
 import collections
 import csv
 import io
@@ -53,5 +57,34 @@ def main(path, top=40):
               f"`{a['src'].replace('|', '/')}` |")
 
 
+def ops(path, top=30):
+    import re
+
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = next(r for r in rows if r and r[0] == "Address")
+    col = {h: i for i, h in enumerate(hdr)}
+    warp, thread = collections.Counter(), collections.Counter()
+    for r in rows:
+        if len(r) < len(hdr) or not r[0].startswith("0x"):
+            continue
+        m = re.match(r"\s*(@!?U?P\w+\s+)?([A-Z0-9_]+)", r[col["Source"]])
+        if not m:
+            continue
+        warp[m.group(2)] += float(r[col["Instructions Executed"]] or 0)
+        thread[m.group(2)] += float(r[col["Predicated-On Thread Instructions Executed"]] or 0)
+    tot = sum(warp.values()) or 1
+    print("| opcode | share of warp instructions | warp instructions | thread instructions |\n|---|---|---|---|")
+    for op, n in warp.most_common(top):
+        print(f"| {op} | {100 * n / tot:.1f}% | {n:.3g} | {thread[op]:.3g} |")
+    flops = {"FFMA": 2, "FADD": 1, "FMUL": 1, "FFMA2": 4, "FADD2": 2, "FMUL2": 2}
+    f = sum(thread[o] * k for o, k in flops.items())
+    print(f"\nexecuted FP32 flops per launch (FFMA 2, FADD/FMUL 1, FFMA2 4, FADD2/FMUL2 2): {f:.4g}")
+
+
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    if len(sys.argv) > 2 and sys.argv[2] == "--ops":
+        ops(sys.argv[1])
+    else:
+        main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
