@@ -53,9 +53,9 @@ FLOPS_PER_STEP = 440  # algorithmic FP32 flops per rollout-ste
 BYTES_PER_POINT = 12  # FP32 xyz read once by the keying pass
 # ncu --set full of the FP32 screening kernels (bound + main pass) on the C5
 # batch as one chunk: DRAM read+write per step and the main pass's issue-slot
-# use (profiles/r01_c5_full.md)
-TRAFFIC_BYTES_PER_LAUNCH = 193.6e6
-TRAFFIC_SOURCE = "profiles/r01_c5_full.md"
+# use (profiles/r02_c5_full.md)
+TRAFFIC_BYTES_PER_LAUNCH = 194.4e6
+TRAFFIC_SOURCE = "profiles/r02_c5_full.md"
 ISSUE_ACTIVE_FRAC = 0.722
 
 

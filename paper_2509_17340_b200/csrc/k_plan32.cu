@@ -512,6 +512,13 @@ constexpr int kScreenThreads = 128;
 #define AMPPI_MAIN_COMPACT 10
 #endif
 constexpr int kMainThreads = AMPPI_MAIN_THREADS, kMainMinBlocks = AMPPI_MAIN_MINBLOCKS;
+#ifndef AMPPI_REPACK_KEY
+#define AMPPI_REPACK_KEY 0  // 0: grid-cell hash of the position, 1: nearest point block of the last query
+#endif
+#ifndef AMPPI_MAIN_GROUPS
+#define AMPPI_MAIN_GROUPS 1
+#endif
+constexpr int kMainGroups = AMPPI_MAIN_GROUPS;
 #ifndef AMPPI_BOUND_SAMPLES
 #define AMPPI_BOUND_SAMPLES 32
 #endif
@@ -695,11 +702,17 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         int bkt = 0;
         uint32_t rank = 0;
         if (live) {
+#if AMPPI_REPACK_KEY == 1
+          // by the previous step's nearest point block: samples near the same
+          // obstacle patch share a warp and walk the same leaves
+          bkt = env.hint == kNoHint ? 0 : 1 + static_cast<int>((env.hint >> 2) % 63u);
+#else
           const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
           const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);
           const int cz = __float2int_rd((x.p.z - env.grid.origin_f[2]) * env.grid.inv_h_f);
           bkt = static_cast<int>((static_cast<uint32_t>(cx) * 73856093u ^ static_cast<uint32_t>(cy) * 19349663u ^
                                   static_cast<uint32_t>(cz) * 83492791u) >> 26);
+#endif
           rank = atomicAdd(&s_bcnt[bkt], 1u);
         }
         __syncthreads();
@@ -987,7 +1000,18 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
     // the better live samples pack: 224 threads (5 CTAs per SM; the whole
     // K = 256 main pass of an instance in one CTA) beat 128 (9 per SM) by 4%,
     // 64 threads lose 15% (C5, measured); 128 when that covers the samples.
-    if (kBoundSamples < 32 && kr - k1 > kMainThreads && kr - k1 <= 256) {  // (experiment builds) one 256-thread CTA
+    if (kMainGroups > 1 && kr - k1 > 128) {
+      // (experiment builds) the main pass in kMainGroups sequential launches
+      // of 128-sample CTAs; each group aborts against the minimum of every
+      // sample screened before it, a tighter bound than the 32 bound samples
+      const int per = (kr - k1 + kMainGroups - 1) / kMainGroups;
+      for (int g0 = k1; g0 < kr; g0 += per) {
+        const int g1 = min(kr, g0 + per);
+        const int tiles = (g1 - g0 + kScreenThreads - 1) / kScreenThreads;
+        k_stage1_f32c<9, kMainCompact, kScreenThreads>
+            <<<static_cast<unsigned>(SM * tiles), kScreenThreads, 0, st>>>(in, P, pl, cfg, sc, iter, g0, g1, g0);
+      }
+    } else if (kBoundSamples < 32 && kr - k1 > kMainThreads && kr - k1 <= 256) {  // (experiment builds) one 256-thread CTA
       k_stage1_f32c<4, kMainCompact, 256><<<static_cast<unsigned>(SM), 256, 0, st>>>(in, P, pl, cfg, sc, iter, k1,
                                                                                     kr, k1);
     } else if (kr - k1 > 128) {

@@ -759,6 +759,7 @@ __global__ void __launch_bounds__(128) k_merge(Plan pl, DevConfig cfg, const dou
 // values and sums as rollout_costs<double, Pert, true>.  sm: per-warp scratch
 // of kWarpRolloutDoubles(N) doubles.
 constexpr int kRolloutMaxN = 64;
+constexpr int kRolloutDone = 1 << 20;  // ready-word marker: trajectory finished (+ number of finite states)
 __host__ __device__ constexpr int warp_rollout_doubles(int N) { return 4 * N + 10 * (N + 1) + 7 * N; }
 
 // rk4_normalized<double> evaluated by a whole warp: every lane runs the
@@ -813,7 +814,7 @@ __device__ __forceinline__ St<double> rk4_normalized_warp(const St<double>& x, d
 
 template <typename Pert>
 __device__ TrajSums rollout_warp64(St<double> x0, const RolloutEnv<double>& env, const Pert& pert, double* pos_out,
-                                   double* sm) {
+                                   double* sm, volatile int* ready = nullptr) {
   const int lane = threadIdx.x & 31, N = env.N;
   double* su = sm;                  // [N*4] applied controls
   double* sx = su + 4 * N;          // [(N+1)*10] states p q v
@@ -846,6 +847,10 @@ __device__ TrajSums rollout_warp64(St<double> x0, const RolloutEnv<double>& env,
         o[0] = x.p.x; o[1] = x.p.y; o[2] = x.p.z;
         o[3] = x.q.w; o[4] = x.q.x; o[5] = x.q.y; o[6] = x.q.z;
         o[7] = x.v.x; o[8] = x.v.y; o[9] = x.v.z;
+        if (ready) {  // state j is visible to the consumer warp of the CTA
+          __threadfence_block();
+          *ready = j + 1;
+        }
       }
       const St<double> nx =
           rk4_normalized_warp(x, su[4 * j], V3<double>{su[4 * j + 1], su[4 * j + 2], su[4 * j + 3]}, dy);
@@ -857,6 +862,10 @@ __device__ TrajSums rollout_warp64(St<double> x0, const RolloutEnv<double>& env,
     }
   }
   const bool valid = n_ok == N;
+  if (ready && lane == 0) {
+    __threadfence_block();
+    *ready = kRolloutDone + n_ok;  // the chain is over: n_ok states exist
+  }
   __syncwarp();
   for (int j = lane; j < n_ok; j += 32) {
     const double* o = sx + 10 * j;
@@ -906,19 +915,115 @@ __global__ void __launch_bounds__(64) k_stage2_traj(BatchIn in, Perception P, Pl
   pl.tsum[smi] = t;
 }
 
-// Latency form: one warp per instance (rollout_warp64).
-__global__ void __launch_bounds__(64) k_stage2_traj_w(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
-  __shared__ double s_scr[2][warp_rollout_doubles(kRolloutMaxN)];
-  const int64_t smi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
-  TrajSums t{0, 0, 0, 0, 0, 0};
-  if (pl.alive[smi]) {
-    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
-    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
-    t = rollout_warp64(load_state(in.states + 10 * s), env, PertZero<double>{}, pl.pos64 + smi * cfg.N * 4,
-                       s_scr[threadIdx.x >> 5]);
+// Latency path, fused: one 64-thread CTA per trajectory.  Warp 0 runs the
+// FP64 trajectory (rollout_warp64) and publishes each state as soon as the
+// RK4 chain reaches it; warp 1 answers the exact collision query of step j
+// (lane j) as soon as state j is published, so the queries overlap the chain
+// instead of following it in a second kernel.  Same terms, summed in step
+// order: the results equal the two-kernel form.
+__device__ __forceinline__ void consume_collisions(const RolloutEnv<double>& env, const double* sx, int N,
+                                                   volatile int* ready, double* terms) {
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j < N; j += 32) {
+    int r;
+    while ((r = *ready) <= j) {
+    }
+    __threadfence_block();
+    const int n_ok = r >= kRolloutDone ? r - kRolloutDone : N;
+    terms[j] = j < n_ok ? env.collision(V3<double>{sx[10 * j], sx[10 * j + 1], sx[10 * j + 2]}) : 0.0;
   }
-  if ((threadIdx.x & 31) == 0) pl.tsum[smi] = t;
+}
+
+__global__ void __launch_bounds__(64) k_stage2_fused_w(BatchIn in, Perception P, Plan pl, DevConfig cfg) {
+  __shared__ double s_scr[warp_rollout_doubles(kRolloutMaxN)];
+  __shared__ double s_terms[kRolloutMaxN];
+  __shared__ int s_ready;
+  __shared__ TrajSums s_t;
+  const int64_t smi = blockIdx.x;
+  if (smi >= static_cast<int64_t>(in.S) * cfg.M) return;
+  if (threadIdx.x == 0) s_ready = 0;
+  __syncthreads();
+  const bool alive = pl.alive[smi];
+  const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+  if (alive) {
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    double* sx = s_scr + 4 * cfg.N;  // rollout_warp64's state table
+    if (threadIdx.x < 32) {
+      const TrajSums t = rollout_warp64(load_state(in.states + 10 * s), env, PertZero<double>{},
+                                        pl.pos64 + smi * cfg.N * 4, s_scr, &s_ready);
+      if (threadIdx.x == 0) s_t = t;
+    } else {
+      consume_collisions(env, sx, cfg.N, &s_ready, s_terms);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double st2 = __longlong_as_double(0x7ff0000000000000ll);
+    bool valid = false;
+    double bd[5] = {0, 0, 0, 0, 0};
+    if (alive && s_t.valid) {
+      double col = 0.0;
+      for (int j = 0; j < cfg.N; ++j) col = col + s_terms[j];
+      const TrajSums t = s_t;
+      st2 = t.goal + col;  // stage2_cost (costs.hpp:139-147)
+      valid = isfinite(st2);
+      bd[0] = cfg.q_track * t.trk;
+      bd[1] = cfg.q_vnorm * t.vn;
+      bd[2] = cfg.q_c * t.mag + cfg.q_c_delta * t.rate;
+      bd[3] = t.goal;
+      bd[4] = col;
+    }
+    pl.stage2[smi] = st2;
+    pl.valid[smi] = valid ? 1 : 0;
+    for (int i = 0; i < 5; ++i) pl.breakdown[smi * 5 + i] = bd[i];
+  }
+}
+
+__global__ void __launch_bounds__(64) k_refine_fused_w(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                       UpdateScratch us, int iter) {
+  __shared__ double s_scr[warp_rollout_doubles(kRolloutMaxN)];
+  __shared__ double s_terms[kRolloutMaxN];
+  __shared__ int s_ready;
+  __shared__ TrajSums s_t;
+  const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
+  for (unsigned long long w = blockIdx.x; w < n; w += gridDim.x) {
+    if (threadIdx.x == 0) s_ready = 0;
+    __syncthreads();
+    const uint2 pr = us.pairs[w];
+    const int64_t smi = pr.x;
+    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
+    const int k = static_cast<int>(us.cand_k[smi * cfg.K + pr.y]);
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
+    double* pos = pl.pos64 + static_cast<int64_t>(w) * cfg.N * 4;
+    if (threadIdx.x < 32) {
+      const St<double> x0 = load_state(in.states + 10 * s);
+      TrajSums t;
+      if (in.injected) {
+        t = rollout_warp64(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)}, pos, s_scr, &s_ready);
+      } else {
+        const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+        const PertRngD prng{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                            cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+        t = rollout_warp64(x0, env, prng, pos, s_scr, &s_ready);
+      }
+      if (threadIdx.x == 0) s_t = t;
+    } else {
+      consume_collisions(env, s_scr + 4 * cfg.N, cfg.N, &s_ready, s_terms);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const TrajSums t = s_t;
+      double val = __longlong_as_double(0x7ff0000000000000ll);
+      if (t.valid) {
+        double col = 0.0;
+        for (int j = 0; j < cfg.N; ++j) col = col + s_terms[j];
+        val = ((cfg.q_track * t.trk + cfg.q_vnorm * t.vn) + (cfg.q_c * t.mag + cfg.q_c_delta * t.rate)) + (t.goal + col);
+      }
+      pl.tsum[w] = t;
+      us.cand_s[smi * cfg.K + pr.y] = val;
+    }
+    __syncthreads();  // s_ready / s_terms are reused by the next trajectory
+  }
 }
 
 // Sum of the N collision terms of one deferred trajectory, in step order
@@ -989,35 +1094,6 @@ __global__ void __launch_bounds__(64) k_refine_traj(BatchIn in, Perception P, Pl
       cs = rollout_costs<double, PertRngD, true>(x0, env, prng, nullptr, nullptr, pos);
     }
     pl.tsum[w] = TrajSums{cs.trk, cs.vn, cs.mag, cs.rate, cs.goal, cs.valid ? 1 : 0};
-  }
-}
-
-// Latency form: one warp per support pair (rollout_warp64).
-__global__ void __launch_bounds__(64) k_refine_traj_w(BatchIn in, Perception P, Plan pl, DevConfig cfg,
-                                                      UpdateScratch us, int iter) {
-  __shared__ double s_scr[2][warp_rollout_doubles(kRolloutMaxN)];
-  const unsigned long long n = min(*us.pair_count, static_cast<unsigned long long>(pl.pos_cap));
-  for (unsigned long long w = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n;
-       w += (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5) {
-    const uint2 pr = us.pairs[w];
-    const int64_t smi = pr.x;
-    const int s = static_cast<int>(smi / cfg.M), m = static_cast<int>(smi % cfg.M);
-    const int k = static_cast<int>(us.cand_k[smi * cfg.K + pr.y]);
-    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * cfg.N * 4);
-    const St<double> x0 = load_state(in.states + 10 * s);
-    double* pos = pl.pos64 + static_cast<int64_t>(w) * cfg.N * 4;
-    double* scr = s_scr[threadIdx.x >> 5];
-    TrajSums t;
-    if (in.injected) {
-      t = rollout_warp64(x0, env, PertInjected<double>{injected_row(in, cfg, s, iter, m, k)}, pos, scr);
-    } else {
-      const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
-      const PertRngD prng{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
-                          cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
-      t = rollout_warp64(x0, env, prng, pos, scr);
-    }
-    if ((threadIdx.x & 31) == 0) pl.tsum[w] = t;
-    __syncwarp();
   }
 }
 
@@ -1267,14 +1343,14 @@ static void launch_support_refine(const BatchIn& in, const Perception& P, const 
   {
     TimedRegion t(timer, "k_refine_traj", st);
     if (jobs < static_cast<int64_t>(sms) * 64) {  // too few rollouts to fill the GPU: cut the latency instead
-      const int64_t b = (jobs * 32 + 63) / 64;
-      k_refine_traj_w<<<static_cast<int>(std::min<int64_t>(b, sms * 32)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
+      // trajectory and collision terms in one CTA per pair (queries overlap the RK4 chain)
+      k_refine_fused_w<<<static_cast<int>(std::min<int64_t>(jobs, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
     } else {
       const int64_t b = (jobs + 63) / 64;
       k_refine_traj<<<static_cast<int>(std::min<int64_t>(b, sms * 16)), 64, 0, st>>>(in, P, pl, cfg, us, iter);
     }
   }
-  {
+  if (jobs >= static_cast<int64_t>(sms) * 64) {  // (the latency path's fused kernel produced the costs)
     TimedRegion t(timer, "k_refine_col", st);
     if (kColPasses) {
       launch_col_queries(P, pl, cfg, ColJobs{us.pairs, us.pair_count, pl.pos_cap}, jobs, st);
@@ -1295,14 +1371,15 @@ static void launch_support_refine(const BatchIn& in, const Perception& P, const 
 cudaError_t launch_plan_finish(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg,
                                bool want_winner_rollout, cudaStream_t st, KernelTimer* timer) {
   const int SM = in.S * cfg.M;
-  {
+  const bool latency = SM < device_sms() * 64;
+  if (latency) {  // trajectory and collision terms in one CTA per instance
+    TimedRegion t(timer, "k_stage2_fused_w", st);
+    k_stage2_fused_w<<<SM, 64, 0, st>>>(in, P, pl, cfg);
+  } else {
     TimedRegion t(timer, "k_stage2_traj", st);
-    if (SM < device_sms() * 64)
-      k_stage2_traj_w<<<(SM * 32 + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
-    else
-      k_stage2_traj<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
+    k_stage2_traj<<<(SM + 63) / 64, 64, 0, st>>>(in, P, pl, cfg);
   }
-  {
+  if (!latency) {
     TimedRegion t(timer, "k_stage2_col", st);
     if (kColPasses) {
       launch_col_queries(P, pl, cfg, ColJobs{nullptr, nullptr, SM}, SM, st);
