@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_CELL_SORT
+#define AMPPI_CELL_SORT 0  // 1: counting sort by cell + per-cell insertion sort (measured 37x slower: dense cells); 0: block bitonic sort
+#endif
 
 struct FinalizeSmem {
   double rng[kCells];  // also the u64 range-bits table during fused keying, and
@@ -463,13 +466,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   SNAP_PHASE(4);  // grid meta
 
   // collision grid: sort the filtered points by (cell, Morton code of the
-  // 1/8-cell sub-position) with a block bitonic sort in shared memory (the
-  // per-cell tables are dead by now): each cell's points become contiguous and
-  // spatially ordered.
+  // 1/8-cell sub-position) in shared memory (the per-cell tables are dead by
+  // now): each cell's points become contiguous and spatially ordered.
   uint32_t* keys = reinterpret_cast<uint32_t*>(sm.rng);             // [<= 8192]
   uint16_t* vals = reinterpret_cast<uint16_t*>(keys + kCellsPow2);  // [<= 8192]
-  uint32_t n2 = 1;
-  while (n2 < n_pts) n2 <<= 1;
   auto cell_of = [&](const V3<double>& p, int* c3, int* sub3) {
     const double rel[3] = {p.x - meta.origin[0], p.y - meta.origin[1], p.z - meta.origin[2]};
 #pragma unroll
@@ -483,19 +483,79 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
     return (c3[0] * meta.dims[1] + c3[1]) * meta.dims[2] + c3[2];
   };
-  for (uint32_t k = tid; k < n2; k += blockDim.x) {
-    uint32_t key = 0xFFFFFFFFu;
-    if (k < n_pts) {
-      const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
-      int c3[3], s3[3];
-      const int c = cell_of(pw, c3, s3);
-      uint32_t mort = 0;
+  auto key_of = [&](uint32_t k) {
+    const V3<double> pw{filt[3 * k], filt[3 * k + 1], filt[3 * k + 2]};
+    int c3[3], s3[3];
+    const int c = cell_of(pw, c3, s3);
+    uint32_t mort = 0;
 #pragma unroll
-      for (int bit = 2; bit >= 0; --bit)
-        mort = (mort << 3) | (((s3[0] >> bit) & 1) << 2) | (((s3[1] >> bit) & 1) << 1) | ((s3[2] >> bit) & 1);
-      key = (static_cast<uint32_t>(c) << 9) | mort;
+    for (int bit = 2; bit >= 0; --bit)
+      mort = (mort << 3) | (((s3[0] >> bit) & 1) << 2) | (((s3[1] >> bit) & 1) << 1) | ((s3[2] >> bit) & 1);
+    return (static_cast<uint32_t>(c) << 9) | mort;
+  };
+#if AMPPI_CELL_SORT
+  // Counting sort by grid cell: 16-bit per-cell counters packed in pairs in
+  // the (dead) idx table, a block scan to segment offsets, a scatter, then
+  // every cell's segment ordered by (Morton code, point index) by one thread
+  // -- four barrier phases instead of a bitonic network's ~80.
+  {
+    const int ncells = meta.dims[0] * meta.dims[1] * meta.dims[2];  // <= kGridCells
+    uint32_t* cnt = sm.idx;                                        // [ceil(ncells / 2)] u16 pairs
+    const int nwords = (ncells + 1) / 2;
+    for (int w = tid; w < nwords; w += blockDim.x) cnt[w] = 0u;
+    __syncthreads();
+    for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
+      const uint32_t c = key_of(k) >> 9;
+      atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
     }
-    keys[k] = key;
+    __syncthreads();
+    // exclusive scan of the counts; each thread owns whole words
+    const int per = 2 * ((nwords + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x));
+    const int c0 = tid * per, c1 = min(c0 + per, ncells);
+    uint32_t local = 0;
+    for (int c = c0; c < c1; ++c) local += (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+    uint32_t run = block_exclusive_scan(local, sm.warp_sums, &sm.total);
+    for (int c = c0; c < c1; c += 2) {  // rewrite both halves of each owned word as offsets
+      const uint32_t w = cnt[c >> 1];
+      const uint32_t lo = run;
+      run += w & 0xFFFFu;
+      const uint32_t hi = run;
+      run += c + 1 < c1 ? (w >> 16) : 0u;
+      cnt[c >> 1] = lo | (hi << 16);
+    }
+    __syncthreads();
+    for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
+      const uint32_t key = key_of(k), c = key >> 9;
+      const uint32_t old = atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
+      const uint32_t pos = (old >> (16 * (c & 1))) & 0xFFFFu;
+      keys[pos] = key;
+      vals[pos] = static_cast<uint16_t>(k);
+    }
+    __syncthreads();
+    // cnt now holds every cell's segment end
+    for (int c = tid; c < ncells; c += blockDim.x) {
+      const uint32_t e = (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+      const uint32_t b = c > 0 ? (cnt[(c - 1) >> 1] >> (16 * ((c - 1) & 1))) & 0xFFFFu : 0u;
+      for (uint32_t i = b + 1; i < e; ++i) {  // insertion sort by (key, point index)
+        const uint32_t kk = keys[i];
+        const uint16_t vv = vals[i];
+        uint32_t j = i;
+        while (j > b && (keys[j - 1] > kk || (keys[j - 1] == kk && vals[j - 1] > vv))) {
+          keys[j] = keys[j - 1];
+          vals[j] = vals[j - 1];
+          --j;
+        }
+        keys[j] = kk;
+        vals[j] = vv;
+      }
+    }
+    __syncthreads();
+  }
+#else
+  uint32_t n2 = 1;
+  while (n2 < n_pts) n2 <<= 1;
+  for (uint32_t k = tid; k < n2; k += blockDim.x) {
+    keys[k] = k < n_pts ? key_of(k) : 0xFFFFFFFFu;
     vals[k] = static_cast<uint16_t>(k);
   }
   __syncthreads();
@@ -524,6 +584,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       else
         __syncwarp();
     }
+#endif
   SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
   // leaves of kLeafSize consecutive (Morton-ordered) points
