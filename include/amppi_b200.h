@@ -242,6 +242,16 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
 int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in_device,
                              amppi_batch_output* out_device);
 
+/* Streaming form of amppi_cycle_batch: submit queues one batch (uploads on the
+ * copy engine, planning on the compute streams) and returns a ticket; wait
+ * returns that batch's results.  Two batches may be in flight, so the next
+ * batch's upload overlaps the current batch's planning.  The caller's xyz
+ * buffer (pinned memory for an asynchronous copy) must stay valid until the
+ * batch is waited for; the per-scene arrays are copied at submit.  Tickets
+ * are waited for in submit order. */
+int amppi_cycle_batch_submit(amppi_ctx* ctx, const amppi_batch_input* in, int64_t* ticket);
+int amppi_cycle_batch_wait(amppi_ctx* ctx, int64_t ticket, amppi_batch_output* out);
+
 /* Sample-sharded plan_step (config C4): one context per GPU,
  * each owning samples [k_begin, k_end) of every instance (the global sample
  * index keys the perturbation stream, so the draws equal the unsharded plan).

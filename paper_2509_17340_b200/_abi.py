@@ -154,6 +154,8 @@ EXPORTS = {
                                   c_double_p, ctypes.POINTER(PlanResult)]),
     "amppi_cycle_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BatchInput), ctypes.POINTER(BatchOutput)]),
     "amppi_cycle_batch_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BatchInput), ctypes.POINTER(BatchOutput)]),
+    "amppi_cycle_batch_submit": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BatchInput), c_int64_p]),
+    "amppi_cycle_batch_wait": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(BatchOutput)]),
     "amppi_kernel_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p), c_double_p, c_int64_p,
                                           ctypes.c_int32, c_int32_p]),
     "amppi_kernel_times_reset": (ctypes.c_int, [ctypes.c_void_p]),

@@ -172,6 +172,22 @@ struct amppi_ctx {
   unsigned char* d_gather{nullptr};
   unsigned char* h_gather{nullptr};  // pinned mirror of d_gather (per-chunk result copies)
   std::vector<cudaEvent_t> chunk_done;
+  // streaming batches (amppi_cycle_batch_submit / _wait): two input slots, so
+  // batch t+1's upload overlaps batch t's planning
+  struct StreamSlot {
+    float* d_xyz{nullptr};
+    int64_t xyz_cap{0};
+    unsigned char* d_in{nullptr};
+    unsigned char* h_in{nullptr};
+    InputBlock din{}, hin{};
+    unsigned char* h_gather{nullptr};
+    cudaEvent_t uploaded{nullptr}, done{nullptr};
+    bool busy{false};
+    int S{0};
+    int64_t ticket{-1};
+  };
+  StreamSlot slots[2];
+  int64_t next_ticket{0};
   uint32_t* h_flags{nullptr};  // mapped device error word (Perception::flags)
   // single-scene plan captured as a CUDA graph (the plan kernels of one
   // amppi_plan call), replayed while its key matches
@@ -735,6 +751,14 @@ int amppi_destroy(amppi_ctx* ctx) {
   if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
   if (ctx->plan_graph) cudaGraphExecDestroy(ctx->plan_graph);
+  for (auto& sl : ctx->slots) {
+    if (sl.d_xyz) cudaFree(sl.d_xyz);
+    if (sl.d_in) cudaFree(sl.d_in);
+    if (sl.h_in) cudaFreeHost(sl.h_in);
+    if (sl.h_gather) cudaFreeHost(sl.h_gather);
+    if (sl.uploaded) cudaEventDestroy(sl.uploaded);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
@@ -1094,6 +1118,7 @@ int amppi_shard_finish(amppi_ctx* ctx, amppi_plan_result* out) {
 int32_t amppi_shard_partials_stride(const amppi_ctx* ctx) { return ctx ? 3 + 4 * ctx->dc.N : 0; }
 
 static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, bool device_out);
+static int plan_device_batch(amppi_ctx* ctx, const BatchIn& bin, int64_t max_scene);
 static int ensure_gather(amppi_ctx* ctx, bool pinned);
 static int gather_chunk(amppi_ctx* ctx, int s0, int s1, const amppi_batch_output* out, cudaStream_t st);
 static void collect_chunk(amppi_ctx* ctx, int s0, int s1, amppi_batch_output* out);
@@ -1285,6 +1310,14 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
   // context's capacity (blocks beyond a scene's end exit immediately)
   const int64_t max_scene = std::max<int64_t>(1, ctx->P_cap / S);
   if (ctx->P.cand_cap < ctx->P_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point capacity");
+  if (int rc = plan_device_batch(ctx, bin, max_scene); rc != AMPPI_OK) return rc;
+  return batch_outputs_gather(ctx, S, out, true);
+}
+
+// Snapshot + plan of a batch whose inputs are on the device (bin), on the
+// context's compute streams; results stay in the plan arrays.
+static int plan_device_batch(amppi_ctx* ctx, const BatchIn& bin, int64_t max_scene) {
+  const int S = bin.S;
   // Device-resident inputs need no upload pipeline, but a few chunks on the
   // compute streams still overlap one chunk's latency-bound tail kernels with
   // the others' work (C5: 3 chunks 18.9 ms, 2 chunks 19.0, 1 chunk 19.3,
@@ -1296,10 +1329,7 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
   // scenes past kFusedMaxPoints take the many-CTA snapshot (shared candidate
   // log): no concurrent chunks
   if (max_scene > kFusedMaxPoints) chunks = 1;
-  if (chunks == 1) {
-    if (int rc = run_cycle(ctx, bin, max_scene, true, true, false); rc != AMPPI_OK) return rc;
-    return batch_outputs_gather(ctx, S, out, true);
-  }
+  if (chunks == 1) return run_cycle(ctx, bin, max_scene, true, true, false);
   if (int rc = fork_streams(ctx); rc != AMPPI_OK) return rc;
   for (int c = 0; c < chunks; ++c) {
     const int s0 = static_cast<int>(static_cast<int64_t>(S) * c / chunks);
@@ -1317,8 +1347,7 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
     cb.seeds += s0;
     if (int rc = run_chunk(ctx, cb, max_scene, s0, c, compute_stream(ctx, c)); rc != AMPPI_OK) return rc;
   }
-  if (int rc = join_streams(ctx); rc != AMPPI_OK) return rc;
-  return batch_outputs_gather(ctx, S, out, true);
+  return join_streams(ctx);
 }
 
 int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches, int32_t cap,
@@ -1448,6 +1477,136 @@ static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, 
   if (out->stage2)
     CK(cudaMemcpyAsync(out->stage2, g.stage2, static_cast<size_t>(S) * M * sizeof(double), cudaMemcpyDeviceToHost, st));
   return sync_and_collect(ctx);
+}
+
+// ---------------------------------------------------------------------------
+// Streaming batches: submit returns once the batch is queued; wait returns its
+// results.  Inputs go through one of two device slots, so with two batches in
+// flight the next batch's point upload (copy engine) runs under the current
+// batch's planning (SMs) -- the steady state is max(upload, planning) instead
+// of their sum.  Planning arrays are shared: batches plan one after another on
+// the context's streams.
+// ---------------------------------------------------------------------------
+static size_t gather_bytes(const amppi_ctx* ctx) {
+  const size_t Sc = static_cast<size_t>(ctx->S_cap);
+  return Sc * (2 * sizeof(int32_t) + (4 + 5 + static_cast<size_t>(ctx->dc.N) * 4 + ctx->dc.M) * sizeof(double)) + 256;
+}
+
+extern "C" int amppi_cycle_batch_submit(amppi_ctx* ctx, const amppi_batch_input* in, int64_t* ticket) {
+  if (!ctx || !in || !ticket) return AMPPI_INVALID_ARGUMENT;
+  const int S = in->n_scenes;
+  if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
+  const int N = ctx->dc.N;
+  if (!in->point_offsets || !in->xyz || !in->poses || !in->states || !in->goals || !in->last_applied ||
+      !in->cycles || !in->seeds)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "null batch input array");
+  if (in->point_offsets[0] != 0) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point_offsets[0] must be 0");
+  int64_t max_scene = 0;
+  for (int s = 0; s < S; ++s) {
+    const int64_t n = in->point_offsets[s + 1] - in->point_offsets[s];
+    if (n < 0) return ctx->fail(AMPPI_INVALID_ARGUMENT, "point_offsets must be non-decreasing");
+    if (n > 0xFFFFFFFFll) return ctx->fail(AMPPI_INVALID_ARGUMENT, "at most 2^32-1 points per scene");
+    max_scene = std::max(max_scene, n);
+  }
+  const int64_t total = in->point_offsets[S];
+  amppi_ctx::StreamSlot& sl = ctx->slots[ctx->next_ticket & 1];
+  if (sl.busy) return ctx->fail(AMPPI_INVALID_ARGUMENT, "two batches already in flight: wait for one first");
+  if (total > ctx->P_cap) {  // the candidate log and point tables are sized by P_cap
+    CK(cudaDeviceSynchronize());
+    if (int rc = alloc_points(ctx, total); rc != AMPPI_OK) return rc;
+  }
+  if (int rc = ensure_gather(ctx, false); rc != AMPPI_OK) return rc;
+  void* p = nullptr;
+  if (!sl.uploaded) {
+    CK(cudaEventCreateWithFlags(&sl.uploaded, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    const InputBlock probe = layout_inputs(nullptr, ctx->S_cap, N);
+    CK(cudaMalloc(&p, probe.bytes));
+    sl.d_in = static_cast<unsigned char*>(p);
+    CK(cudaMallocHost(&p, probe.bytes));
+    sl.h_in = static_cast<unsigned char*>(p);
+    sl.din = layout_inputs(sl.d_in, ctx->S_cap, N);
+    sl.hin = layout_inputs(sl.h_in, ctx->S_cap, N);
+    CK(cudaMallocHost(&p, gather_bytes(ctx)));
+    sl.h_gather = static_cast<unsigned char*>(p);
+  }
+  if (sl.xyz_cap < total) {
+    CK(cudaStreamSynchronize(ctx->copy_stream));
+    if (sl.d_xyz) cudaFree(sl.d_xyz);
+    sl.d_xyz = nullptr;
+    sl.xyz_cap = std::max<int64_t>(total, 1024);
+    CK(cudaMalloc(&p, static_cast<size_t>(sl.xyz_cap) * 3 * sizeof(float)));
+    sl.d_xyz = static_cast<float*>(p);
+  }
+  // per-scene arrays -> the slot's pinned block (its previous upload is over:
+  // that batch was waited for)
+  InputBlock& h = sl.hin;
+  std::memcpy(h.poses, in->poses, static_cast<size_t>(S) * 10 * sizeof(double));
+  std::memcpy(h.states, in->states, static_cast<size_t>(S) * 10 * sizeof(double));
+  std::memcpy(h.goals, in->goals, static_cast<size_t>(S) * 10 * sizeof(double));
+  std::memcpy(h.last, in->last_applied, static_cast<size_t>(S) * 4 * sizeof(double));
+  if (in->previous) std::memcpy(h.prev, in->previous, static_cast<size_t>(S) * N * 4 * sizeof(double));
+  std::memcpy(h.offsets, in->point_offsets, static_cast<size_t>(S + 1) * sizeof(int64_t));
+  std::memcpy(h.cycles, in->cycles, static_cast<size_t>(S) * sizeof(uint64_t));
+  std::memcpy(h.seeds, in->seeds, static_cast<size_t>(S) * sizeof(uint64_t));
+  for (int s = 0; s < S; ++s) h.prev_len[s] = in->previous ? (in->previous_len ? in->previous_len[s] : N) : 0;
+  const size_t span = static_cast<size_t>(reinterpret_cast<unsigned char*>(h.prev_len + ctx->S_cap) -
+                                          reinterpret_cast<unsigned char*>(h.poses));
+  // upload on the copy stream (the slot's device buffers were last read by
+  // that earlier batch's planning, which it waited for)
+  CK(cudaStreamWaitEvent(ctx->copy_stream, sl.done, 0));
+  CK(cudaMemcpyAsync(sl.din.poses, h.poses, span, cudaMemcpyHostToDevice, ctx->copy_stream));
+  if (total > 0)
+    CK(cudaMemcpyAsync(sl.d_xyz, in->xyz, static_cast<size_t>(total) * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                       ctx->copy_stream));
+  CK(cudaEventRecord(sl.uploaded, ctx->copy_stream));
+  // plan on the compute streams once uploaded, then gather into the slot's pinned mirror
+  CK(cudaStreamWaitEvent(ctx->stream, sl.uploaded, 0));
+  BatchIn bin{};
+  bin.xyz = sl.d_xyz;
+  bin.offsets = sl.din.offsets;
+  bin.poses = sl.din.poses;
+  bin.states = sl.din.states;
+  bin.goals = sl.din.goals;
+  bin.prev = sl.din.prev;
+  bin.prev_len = sl.din.prev_len;
+  bin.last_applied = sl.din.last;
+  bin.cycles = sl.din.cycles;
+  bin.seeds = sl.din.seeds;
+  bin.S = S;
+  bin.r_max = in->r_max;
+  ctx->have_snapshot = false;  // the batch overwrites the single-scene perception slot
+  if (int rc = plan_device_batch(ctx, bin, max_scene); rc != AMPPI_OK) return rc;
+  const GatherOut g = gather_view(ctx, ctx->d_gather, 0);
+  cudaError_t e = launch_gather(ctx->pl, ctx->dc, S, g, ctx->stream);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_gather");
+  CK(cudaMemcpyAsync(sl.h_gather, ctx->d_gather, gather_bytes(ctx), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaEventRecord(sl.done, ctx->stream));
+  sl.busy = true;
+  sl.S = S;
+  sl.ticket = ctx->next_ticket;
+  *ticket = ctx->next_ticket++;
+  return AMPPI_OK;
+}
+
+extern "C" int amppi_cycle_batch_wait(amppi_ctx* ctx, int64_t ticket, amppi_batch_output* out) {
+  if (!ctx) return AMPPI_INVALID_ARGUMENT;
+  amppi_ctx::StreamSlot& sl = ctx->slots[ticket & 1];
+  if (!sl.busy || sl.ticket != ticket) return ctx->fail(AMPPI_INVALID_ARGUMENT, "unknown or already collected ticket");
+  CK(cudaEventSynchronize(sl.done));
+  sl.busy = false;
+  if (ctx->timer.enabled) ctx->timer.collect();
+  if (ctx->h_flags && *ctx->h_flags) {
+    *ctx->h_flags = 0u;
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "a batch exceeded the context's point capacity; its results are invalid");
+  }
+  if (out) {
+    unsigned char* saved = ctx->h_gather;
+    ctx->h_gather = sl.h_gather;  // collect_chunk reads the pinned mirror
+    collect_chunk(ctx, 0, sl.S, out);
+    ctx->h_gather = saved;
+  }
+  return AMPPI_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -516,6 +516,34 @@ class Planner:
 
         poses/states: [S,10]; goals: [S,10] (p, v, q); last_applied: [S,4];
         previous: [S,N,4] or None (hover warm start)."""
+        bi, arrs, out, bo = self._batch_structs(offsets, xyz, poses, states, goals, last_applied, cycles, seeds,
+                                                previous, r_max)
+        self._gen += 1  # the batch overwrites the single-scene snapshot slot
+        self._check(self.lib.amppi_cycle_batch(self._h, ctypes.byref(bi), ctypes.byref(bo)))
+        return out
+
+    def cycle_batch_submit(self, offsets: np.ndarray, xyz: np.ndarray, poses: np.ndarray, states: np.ndarray,
+                           goals: np.ndarray, last_applied: np.ndarray, cycles: np.ndarray, seeds: np.ndarray,
+                           previous: np.ndarray | None = None, r_max: float = 10.0) -> int:
+        """Streaming form (amppi_cycle_batch_submit): queue the batch and return
+        a ticket; up to two batches in flight, so the next batch's upload
+        overlaps this one's planning.  xyz should be pinned memory (e.g. a
+        torch pin_memory() tensor's numpy view) for the copy to be asynchronous."""
+        bi, arrs, out, bo = self._batch_structs(offsets, xyz, poses, states, goals, last_applied, cycles, seeds,
+                                                previous, r_max)
+        t = ctypes.c_int64()
+        self._gen += 1
+        self._check(self.lib.amppi_cycle_batch_submit(self._h, ctypes.byref(bi), ctypes.byref(t)))
+        self._inflight = getattr(self, "_inflight", {})
+        self._inflight[int(t.value)] = (arrs, out, bo)  # the host arrays must outlive the upload
+        return int(t.value)
+
+    def cycle_batch_wait(self, ticket: int) -> dict:
+        arrs, out, bo = self._inflight.pop(ticket)
+        self._check(self.lib.amppi_cycle_batch_wait(self._h, ticket, ctypes.byref(bo)))
+        return out
+
+    def _batch_structs(self, offsets, xyz, poses, states, goals, last_applied, cycles, seeds, previous, r_max):
         S = int(len(offsets) - 1)
         N, M = self.cfg.mppi.horizon, self.cfg.grid.count()
         off = np.asarray(offsets)
@@ -562,9 +590,7 @@ class Planner:
         bo.winner_nominal = _ptr(out["winner_nominal"], ctypes.c_double)
         bo.stage2 = _ptr(out["stage2"], ctypes.c_double)
         bo.breakdown = _ptr(out["breakdown"], ctypes.c_double)
-        self._gen += 1  # the batch overwrites the single-scene snapshot slot
-        self._check(self.lib.amppi_cycle_batch(self._h, ctypes.byref(bi), ctypes.byref(bo)))
-        return out
+        return bi, arrs, out, bo
 
     def cycle_batch_device(self, dev: dict, out: dict, n_scenes: int, r_max: float = 10.0) -> None:
         """Same cycle on device-resident inputs (dict of raw device pointers,
