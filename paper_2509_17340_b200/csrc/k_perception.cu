@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_KEY_PREFILTER
+#define AMPPI_KEY_PREFILTER 0  // FP32 prefilter of the fused snapshot's keying pass
+#endif
 #ifndef AMPPI_CELL_SORT
 #define AMPPI_CELL_SORT 0  // 1: counting sort by cell + per-cell insertion sort (measured 37x slower: dense cells); 0: block bitonic sort
 #endif
@@ -803,8 +806,30 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
     }
   };
   if (!in.xyz64) fetch(b);
+#if AMPPI_KEY_PREFILTER
+  // FP32 pose for the prefilter (float input only): a point whose FP32 range
+  // (error < 1e-4 m for coordinates below 1e3 m) is clearly past r_max, below
+  // the minimum range, or clearly above its cell's running minimum cannot be
+  // a cell minimum and skips the exact FP64 keying and the 64-bit atomic; its
+  // cell comes from the FP32 fast key, taken only where that key is exact
+  // (horizontal and total range >= 1 m, outside the guard band)
+  float fr[9], fp[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    fp[i] = static_cast<float>(i == 0 ? pose.p.x : (i == 1 ? pose.p.y : pose.p.z));
+#pragma unroll
+    for (int j = 0; j < 3; ++j) fr[3 * i + j] = static_cast<float>(pose.r.m[i][j]);
+  }
+  const bool prefilter = !in.xyz64 && fabsf(fp[0]) < 1e3f && fabsf(fp[1]) < 1e3f && fabsf(fp[2]) < 1e3f;
+  const float rmax_f = static_cast<float>(r_max);
+#endif
   for (int64_t g0 = b; g0 < e; g0 += kUnroll * blockDim.x) {
     V3<double> w[kUnroll];
+#if AMPPI_KEY_PREFILTER
+    V3<float> wf[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) wf[u] = nxt[u];
+#endif
     if (in.xyz64) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -822,7 +847,34 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
       int f = 0;
       uint64_t bits = 0;
       bool cand = false;
-      if (g < e && key_point(pose, w[u], r_max, f, bits)) cand = atomicMin(cell_bits + f, bits) >= bits;
+      bool skip = g >= e;
+#if AMPPI_KEY_PREFILTER
+      if (!skip && prefilter) {
+        const float dx = wf[u].x - fp[0], dy = wf[u].y - fp[1], dz = wf[u].z - fp[2];
+        if (fabsf(wf[u].x) < 1e3f && fabsf(wf[u].y) < 1e3f && fabsf(wf[u].z) < 1e3f) {
+          // R^T (w - p), the body frame (perception.cpp:58-61)
+          const float bx = (fr[0] * dx + fr[3] * dy) + fr[6] * dz;
+          const float by = (fr[1] * dx + fr[4] * dy) + fr[7] * dz;
+          const float bz = (fr[2] * dx + fr[5] * dy) + fr[8] * dz;
+          const float rho = sqrtf(bx * bx + by * by);
+          const float rf = sqrtf(rho * rho + bz * bz);
+          if (rf > rmax_f + 1e-3f || rf < static_cast<float>(kMinPointRange) - 1e-3f) {
+            skip = true;
+          } else if (rho >= 1.0f) {
+            constexpr float kInvStepF = static_cast<float>(1.0 / 0x1.acee9f37bebd5p-5);
+            int i = fast_cell(by, bx, 3.14159265358979f, kInvStepF);
+            const int j = fast_cell(bz, rho, 1.57079632679490f, kInvStepF);
+            if (i >= 0 && j >= 0) {
+              if (i >= kAz) i -= kAz;
+              const int fc = min(max(i, 0), kAz - 1) * kEl + min(max(j, 0), kEl - 1);
+              const double cur = __longlong_as_double(static_cast<long long>(cell_bits[fc]));  // may be stale: larger
+              skip = static_cast<double>(rf) - 1e-3 > cur;
+            }
+          }
+        }
+      }
+#endif
+      if (!skip && key_point(pose, w[u], r_max, f, bits)) cand = atomicMin(cell_bits + f, bits) >= bits;
       const unsigned want = __ballot_sync(0xffffffffu, cand);
       if (want) {
         uint32_t base = 0;
