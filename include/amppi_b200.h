@@ -348,6 +348,20 @@ int amppi_anchors_csv(const char* path, int32_t step, int32_t n_anchors, const d
 int amppi_kernel_times(amppi_ctx* ctx, const char** names, double* ms, int64_t* launches,
                        int32_t cap, int32_t* count);
 int amppi_kernel_times_reset(amppi_ctx* ctx);
+
+/* Screening-drift diagnostic (verification only; DESIGN.md §2 "The d_max
+ * jump"): after amppi_cycle_batch_device over in_device, integrates every
+ * sample_stride-th sample of every instance twice -- as the FP32 screening
+ * does (no abort bound) and as the FP64 refine does -- with the current
+ * nominal and the perturbation stream of `iteration`, and compares them step
+ * by step.  stats[8]: rollouts compared, max |p32 - p64| (m), max |d32 - d64|
+ * where the clearance is below the grid cell size (1.001 d_max; both queries
+ * exact there) minus 1e-4 (m), steps compared there, steps
+ * on opposite sides of d_max outside the screening band (must be 0), steps the
+ * screening flags, max relative stage-I cost difference of unflagged
+ * rollouts, rollouts valid in one precision only. */
+int amppi_screen_drift(amppi_ctx* ctx, const amppi_batch_input* in_device, int32_t iteration,
+                       int32_t sample_stride, double* stats);
 int amppi_set_stream(amppi_ctx* ctx, void* stream);
 void* amppi_get_stream(const amppi_ctx* ctx);  /* the cudaStream_t the context launches on */
 

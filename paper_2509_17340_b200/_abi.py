@@ -159,6 +159,8 @@ EXPORTS = {
     "amppi_kernel_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p), c_double_p, c_int64_p,
                                           ctypes.c_int32, c_int32_p]),
     "amppi_kernel_times_reset": (ctypes.c_int, [ctypes.c_void_p]),
+    "amppi_screen_drift": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BatchInput), ctypes.c_int32, ctypes.c_int32,
+                                          c_double_p]),
     "amppi_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "amppi_get_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
     "amppi_nccl_version": (ctypes.c_int, [c_int32_p]),
@@ -211,7 +213,10 @@ def load(path: str | None = None) -> ctypes.CDLL:
     if not os.path.exists(p):
         raise RuntimeError(f"{p} not found: run __graft_entry__.build() (no CPU fallback exists)")
     lib = ctypes.CDLL(p)
+    lenient = os.environ.get("AMPPI_ABI_LENIENT") == "1"  # tools/ab.py timing older builds
     for name, (res, args) in EXPORTS.items():
+        if lenient and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

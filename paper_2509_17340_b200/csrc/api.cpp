@@ -1373,6 +1373,61 @@ int amppi_kernel_times_reset(amppi_ctx* ctx) {
   return AMPPI_OK;
 }
 
+int amppi_screen_drift(amppi_ctx* ctx, const amppi_batch_input* in, int32_t iteration, int32_t sample_stride,
+                       double* stats) {
+  if (!ctx || !in || !stats) return AMPPI_INVALID_ARGUMENT;
+  const DevConfig& dc = ctx->dc;
+  const int S = in->n_scenes;
+  if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
+  if (sample_stride < 1 || iteration < 0 || iteration >= dc.iterations)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "sample_stride < 1 or iteration out of range");
+  if (dc.N > 64) return ctx->fail(AMPPI_INVALID_ARGUMENT, "horizon > 64");
+  if (!in->states || !in->goals || !in->cycles || !in->seeds)
+    return ctx->fail(AMPPI_INVALID_ARGUMENT, "null batch input array");
+  BatchIn bin{};
+  bin.states = reinterpret_cast<const double*>(in->states);
+  bin.goals = reinterpret_cast<const double*>(in->goals);
+  bin.cycles = in->cycles;
+  bin.seeds = in->seeds;
+  bin.S = S;
+  const int kn = (dc.k_hi - dc.k_lo + sample_stride - 1) / sample_stride;
+  const int64_t per_scene = static_cast<int64_t>(dc.M) * kn;
+  // scenes per launch pair: at most 512 MB of per-step records
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(S, (int64_t{1} << 29) / (per_scene * dc.N * 16)));
+  float4* steps = nullptr;
+  float* cost = nullptr;
+  unsigned long long* acc = nullptr;
+  auto release = [&] {
+    cudaFree(steps);
+    cudaFree(cost);
+    cudaFree(acc);
+  };
+  cudaError_t e = cudaMalloc(&steps, static_cast<size_t>(chunk * per_scene * dc.N) * sizeof(float4));
+  if (e == cudaSuccess) e = cudaMalloc(&cost, static_cast<size_t>(chunk * per_scene) * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&acc, (kDriftSlots + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemsetAsync(acc, 0, (kDriftSlots + 1) * sizeof(unsigned long long), ctx->stream);
+  for (int64_t s0 = 0; e == cudaSuccess && s0 < S; s0 += chunk) {
+    const int n = static_cast<int>(std::min<int64_t>(chunk, S - s0));
+    e = launch_drift32(bin, ctx->P, ctx->pl, dc, iteration, static_cast<int>(s0), n, sample_stride, steps, cost,
+                       ctx->stream);
+    if (e == cudaSuccess)
+      e = launch_drift64(bin, ctx->P, ctx->pl, dc, iteration, static_cast<int>(s0), n, sample_stride, steps, cost, acc,
+                         ctx->stream);
+  }
+  unsigned long long h[kDriftSlots] = {};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  release();
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "amppi_screen_drift");
+  for (int i = 0; i < kDriftSlots; ++i) {
+    const bool is_max = i == 1 || i == 2 || i == 6;
+    double v;
+    std::memcpy(&v, &h[i], sizeof(v));
+    stats[i] = is_max ? v : static_cast<double>(h[i]);
+  }
+  return AMPPI_OK;
+}
+
 }  // extern "C"
 
 // Gathered results: one field-major block of S_cap scenes (device, and a

@@ -214,16 +214,34 @@ __device__ __forceinline__ void normal_pair(uint64_t key, uint32_t p, double& n0
   n1 = r * s;
 }
 
-// FP32 screening draw: same integers, float arithmetic.  1 - U comes from
-// the integer complement (so U near 1 keeps its tail) rounded once to float,
-// and one hardware log2 serves every U -- no data-dependent branch, so the
-// lanes of a warp stay converged (absolute error of log(1-U) < 1e-6, far
-// inside the screening window).
+// FP32 screening draw: same integers, float arithmetic.  log(1 - U): for
+// U >= 1/16 the hardware log of 1 - U (from the integer complement, so U near
+// 1 keeps its tail; relative error < 6e-6 there); for U < 1/16 the series
+// -U (1 + U/2 + ... + U^5/6) on U itself (relative error < 1e-7) -- the float
+// 1 - U would lose U below 2^-24, and the hardware log's absolute error
+// (~4e-7) would dominate log(1 - U) ~ -U, turning a rare draw with U ~ 1e-6
+// into a normal off by ~1e-3 (an FP32 rollout 1e-4 m from its FP64 twin;
+// tools/screen_drift.py).  Both forms are evaluated and one selected, so the
+// lanes of a warp stay converged.
+#ifndef AMPPI_F32_BOX
+#define AMPPI_F32_BOX 1  // nearest_sq_exact prunes boxes in FP32 with a rounding margin (0: FP64 box test)
+#endif
+#ifndef AMPPI_LOG_SERIES
+#define AMPPI_LOG_SERIES 1
+#endif
 __device__ __forceinline__ void normal_pair_f(uint64_t key, uint32_t p, float& n0, float& n1) {
   const uint64_t a = mix64(key + (2ull * p + 1ull) * kGamma);
   const uint64_t b = mix64(key + (2ull * p + 2ull) * kGamma);
   const uint64_t ma = a >> 11;
-  const float lg = __logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
+  const float lhw = __logf(static_cast<float>((1ull << 53) - ma) * 0x1.0p-53f);
+#if AMPPI_LOG_SERIES
+  const float u = static_cast<float>(ma) * 0x1.0p-53f;
+  const float ser =
+      -u * (1.0f + u * (0.5f + u * (0.333333343f + u * (0.25f + u * (0.200000003f + u * 0.166666672f)))));
+  const float lg = u < 0.0625f ? ser : lhw;
+#else
+  const float lg = lhw;
+#endif
   const float r = sqrt_approx(fmaxf(-2.0f * lg, 0.0f));  // (the approximate log may round above 0 next to 1)
   // angle 2*pi*u2 in [0, 2pi): hardware sin/cos after reduction to [-pi, pi)
   // (abs error ~1e-6, far inside the screening window)
@@ -421,6 +439,16 @@ __device__ __forceinline__ float screen_collision_b(float d2, float cs, float ca
 // Stored screening cost: a flagged (lower-bound) cost carries the sign bit.
 __device__ __forceinline__ float screen_store(float cost, bool amb) { return amb ? -cost : cost; }
 
+// The FP32 data and the FP32 screening live in the scene's local frame:
+// x_f = float(x - g.org), the difference taken in FP64 before the one
+// rounding, with org the snapshot pose.  Positions then stay within metres of
+// 0 whatever the world coordinates, so the FP32 rollout drift does not grow
+// with them (DESIGN.md §2 "The d_max jump"; tools/screen_drift.py).
+__device__ __forceinline__ V3<float> to_local_f(const GridMeta& g, const double* v) {
+  return {static_cast<float>(v[0] - g.org[0]), static_cast<float>(v[1] - g.org[1]),
+          static_cast<float>(v[2] - g.org[2])};
+}
+
 // Collision-grid queries (replacing ClearanceIndex::nearest,
 // perception.cpp:191-235).  The squared distance to the nearest filtered point
 // is exact whenever the true nearest distance is below d_max: every such point
@@ -455,65 +483,6 @@ __device__ __forceinline__ uint32_t nbr_phase(uint32_t m, int phase) {
   return m & (phase == 0 ? kNbrCenter : (phase == 1 ? kNbrFaces : ~(kNbrCenter | kNbrFaces)));
 }
 
-__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ rec,
-                                                   const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
-                                                   const double* __restrict__ pts, V3<double> p, double lim2,
-                                                   double stop2, uint32_t* hint) {
-  double best = __longlong_as_double(0x7ff0000000000000ll);
-  if (g.dims[0] == 0) return best;
-  uint32_t bi = *hint;
-  if (bi != kNoHint) {
-    best = sqnorm(p - V3<double>{pts[3 * bi], pts[3 * bi + 1], pts[3 * bi + 2]});
-    if (best < stop2) return best;
-  }
-  const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
-  const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
-  const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
-  const uint32_t m = nbr_mask(g, nbr, cx, cy, cz);
-  if (!m) return best;
-  const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
-  const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
-  // box lower bounds in the same arithmetic as the point distances (sqnorm of
-  // a difference), so box distance <= point distance; the 1e-12 slack only
-  // guards the lim2 comparison
-  auto box_d2 = [&](uint32_t lx, uint32_t ly, uint32_t lz, uint32_t hx, uint32_t hy, uint32_t hz) {
-    const V3<double> lo{__uint_as_float(lx), __uint_as_float(ly), __uint_as_float(lz)};
-    const V3<double> hi{__uint_as_float(hx), __uint_as_float(hy), __uint_as_float(hz)};
-    return sqnorm(V3<double>{fmax(fmax(lo.x - p.x, p.x - hi.x), 0.0), fmax(fmax(lo.y - p.y, p.y - hi.y), 0.0),
-                             fmax(fmax(lo.z - p.z, p.z - hi.z), 0.0)});
-  };
-  for (int phase = 0; phase < 3; ++phase) {
-    uint32_t mm = nbr_phase(m, phase);
-    while (mm) {
-      const int b = __ffs(mm) - 1;
-      mm &= mm - 1;
-      const int c = cbase + nbr_offset(b, d12, d2);
-      const uint4 ra = rec[2 * c], rb = rec[2 * c + 1];
-      if (box_d2(ra.z, rb.x, rb.z, ra.w, rb.y, rb.w) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
-      const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
-      const uint4* lf = leaves + 2 * ra.y;
-      for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
-        const uint4 la = lf[0], lb = lf[1];
-        if (box_d2(la.x, la.z, lb.x, la.y, la.w, lb.y) > fmin(best, lim2) * (1.0 + 1e-12)) continue;
-        const uint32_t te = min(t + kLeafSize, k1);
-        for (uint32_t k = t; k < te; ++k) {
-          const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
-          if (dd < best) {
-            best = dd;
-            bi = k;
-          }
-        }
-        if (best < stop2) {
-          *hint = bi;
-          return best;
-        }
-      }
-    }
-  }
-  *hint = bi;
-  return best;
-}
-
 // Squared norm with a pinned evaluation shape, fma(z, z, fma(y, y, x * x)):
 // the FP32 box bounds and the packed point distances below both use it, and
 // it is monotone in each |component|, so a box distance never exceeds the
@@ -532,6 +501,98 @@ __device__ __forceinline__ float box_gap_sq(uint32_t lx, uint32_t hx, uint32_t l
   const float2 dy = __fadd2_rn(make_float2(__uint_as_float(ly), __uint_as_float(hy)), make_float2(-p.y, -p.y));
   const float2 dz = __fadd2_rn(make_float2(__uint_as_float(lz), __uint_as_float(hz)), make_float2(-p.z, -p.z));
   return sq3f(fmaxf(fmaxf(dx.x, -dx.y), 0.f), fmaxf(fmaxf(dy.x, -dy.y), 0.f), fmaxf(fmaxf(dz.x, -dz.y), 0.f));
+}
+
+__device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ rec,
+                                                   const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
+                                                   const double* __restrict__ pts, V3<double> p, double lim2,
+                                                   double stop2, uint32_t* hint) {
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  if (g.dims[0] == 0) return best;
+  uint32_t bi = *hint;
+  if (bi != kNoHint) {
+    best = sqnorm(p - V3<double>{pts[3 * bi], pts[3 * bi + 1], pts[3 * bi + 2]});
+    if (best < stop2) return best;
+  }
+  const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
+  const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
+  const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
+  const uint32_t m = nbr_mask(g, nbr, cx, cy, cz);
+  if (!m) return best;
+  const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
+  const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
+#if AMPPI_F32_BOX
+  // Box pruning in FP32, in the local frame of the float boxes (the
+  // screening's box_gap_sq on pf = float(p - org)), with a margin that covers
+  // its rounding: per axis the FP32 gap is off by at most
+  // E = 2^-23 (|p - org|max + 2h + 1) (the rounding of pf plus the FADD's,
+  // for boxes within the 27 cells around p), so the float box distance exceeds the true one
+  // by at most 3.5 E sqrt(lim2) + 4 E^2 for any threshold <= lim2 -- plus the
+  // relative rounding of the three squares and of the threshold.  A box is
+  // skipped only when that slack still leaves it farther than the best point
+  // so far (or than sqrt(lim2)): the same boxes as an exact test can keep,
+  // never fewer, so the FP64 minimum is unchanged.
+  const V3<float> pf{static_cast<float>(p.x - g.org[0]), static_cast<float>(p.y - g.org[1]),
+                     static_cast<float>(p.z - g.org[2])};  // to_local_f
+  const float e_ax = 0x1.0p-23f * (fmaxf(fmaxf(fabsf(pf.x), fabsf(pf.y)), fabsf(pf.z)) + 2.0f * g.h_f + 1.0f);
+  const float slack = 3.5f * e_ax * __double2float_ru(sqrt(lim2)) + 4.0f * e_ax * e_ax;
+  auto far = [&](float gap2, double thr) { return gap2 > __double2float_ru(thr) * (1.0f + 1e-6f) + slack; };
+  auto rec_far = [&](const uint4& ra, const uint4& rb) {
+    return far(box_gap_sq(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w, pf), fmin(best, lim2));
+  };
+  auto leaf_far = [&](const uint4& la, const uint4& lb) {
+    return far(box_gap_sq(la.x, la.y, la.z, la.w, lb.x, lb.y, pf), fmin(best, lim2));
+  };
+#else
+  // box lower bounds in the same arithmetic as the point distances (sqnorm of
+  // a difference), so box distance <= point distance; the 1e-12 slack only
+  // guards the lim2 comparison
+  // (the float boxes are in the local frame of the FP32 data: pl = p - org,
+  // off by at most an FP64 rounding, far inside the slack for any d > 1e-3)
+  const V3<double> pl{p.x - g.org[0], p.y - g.org[1], p.z - g.org[2]};
+  auto box_d2 = [&](uint32_t lx, uint32_t ly, uint32_t lz, uint32_t hx, uint32_t hy, uint32_t hz) {
+    const V3<double> lo{__uint_as_float(lx), __uint_as_float(ly), __uint_as_float(lz)};
+    const V3<double> hi{__uint_as_float(hx), __uint_as_float(hy), __uint_as_float(hz)};
+    return sqnorm(V3<double>{fmax(fmax(lo.x - pl.x, pl.x - hi.x), 0.0), fmax(fmax(lo.y - pl.y, pl.y - hi.y), 0.0),
+                             fmax(fmax(lo.z - pl.z, pl.z - hi.z), 0.0)});
+  };
+  auto rec_far = [&](const uint4& ra, const uint4& rb) {
+    return box_d2(ra.z, rb.x, rb.z, ra.w, rb.y, rb.w) > fmin(best, lim2) * (1.0 + 1e-12);
+  };
+  auto leaf_far = [&](const uint4& la, const uint4& lb) {
+    return box_d2(la.x, la.z, lb.x, la.y, la.w, lb.y) > fmin(best, lim2) * (1.0 + 1e-12);
+  };
+#endif
+  for (int phase = 0; phase < 3; ++phase) {
+    uint32_t mm = nbr_phase(m, phase);
+    while (mm) {
+      const int b = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int c = cbase + nbr_offset(b, d12, d2);
+      const uint4 ra = rec[2 * c], rb = rec[2 * c + 1];
+      if (rec_far(ra, rb)) continue;
+      const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
+      const uint4* lf = leaves + 2 * ra.y;
+      for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
+        const uint4 la = lf[0], lb = lf[1];
+        if (leaf_far(la, lb)) continue;
+        const uint32_t te = min(t + kLeafSize, k1);
+        for (uint32_t k = t; k < te; ++k) {
+          const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
+          if (dd < best) {
+            best = dd;
+            bi = k;
+          }
+        }
+        if (best < stop2) {
+          *hint = bi;
+          return best;
+        }
+      }
+    }
+  }
+  *hint = bi;
+  return best;
 }
 
 // Squared distances from p to the 4 points of one FP32 point block

@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_LOCAL_FRAME
+#define AMPPI_LOCAL_FRAME 1  // FP32 grid data and screening relative to the snapshot pose (0: world frame)
+#endif
 #ifndef AMPPI_KEY_PREFILTER
 #define AMPPI_KEY_PREFILTER 0  // FP32 prefilter of the fused snapshot's keying pass
 #endif
@@ -435,6 +438,11 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   if (tid == 0) {
     GridMeta m{};
     m.n_points = static_cast<int>(n_pts);
+#if AMPPI_LOCAL_FRAME
+    m.org[0] = sm.pose.p.x;  // the FP32 local frame (to_local_f)
+    m.org[1] = sm.pose.p.y;
+    m.org[2] = sm.pose.p.z;
+#endif
     if (n_pts > 0) {
       double L[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, H[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
@@ -452,7 +460,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       m.inv_h = 1.0 / h;
       for (int a = 0; a < 3; ++a) {
         m.origin[a] = L[a];
-        m.origin_f[a] = static_cast<float>(L[a]);
+        m.origin_f[a] = static_cast<float>(L[a] - m.org[a]);
         int d = static_cast<int>(floor((H[a] - L[a]) * m.inv_h)) + 1;
         m.dims[a] = d < 1 ? 1 : (d > kGridAxis ? kGridAxis : d);
       }
@@ -611,9 +619,9 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     gp64[3 * i + 1] = y;
     gp64[3 * i + 2] = z;
     float* blk = reinterpret_cast<float*>(gp32 + 3 * (i / kPointBlock)) + i % kPointBlock;
-    blk[0] = static_cast<float>(x);
-    blk[kPointBlock] = static_cast<float>(y);
-    blk[2 * kPointBlock] = static_cast<float>(z);
+    blk[0] = static_cast<float>(x - meta.org[0]);
+    blk[kPointBlock] = static_cast<float>(y - meta.org[1]);
+    blk[2 * kPointBlock] = static_cast<float>(z - meta.org[2]);
     const uint32_t c = keys[i] >> 9;
     if (i == 0 || (keys[i - 1] >> 9) != c) {  // first point of cell c
       uint32_t e = i + 1;
@@ -655,7 +663,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       const uint32_t t = (lstart[l] & 0x7FFFFFFFu) + sub;
       if (t < (lstart[l + 1] & 0x7FFFFFFFu))
 #pragma unroll
-        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = gp64[3 * t + a];
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = gp64[3 * t + a] - meta.org[a];  // local frame, as gp32
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1)

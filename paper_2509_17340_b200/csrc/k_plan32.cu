@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
   env.N = N;
   env.dyn = sc.dyn;
   const double* gl = in.goals + 10 * s;
-  env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  env.pg = to_local_f(P.grid[s], gl);
   env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
   env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
   env.q_p = sc.q_p;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_stage1_f32(BatchIn in, Perc
 
   const double* xs = in.states + 10 * s;
   St<float> x0;
-  x0.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x0.p = to_local_f(P.grid[s], xs);
   x0.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
   x0.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
 
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(32) k_stage1_bound(BatchIn in, Perception P, P
   env.N = N;
   env.dyn = sc.dyn;
   const double* gl = in.goals + 10 * s;
-  env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  env.pg = to_local_f(P.grid[s], gl);
   env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
   env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
   env.q_p = sc.q_p;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(32) k_stage1_bound(BatchIn in, Perception P, P
   env.band = sc.band;
   const double* xs = in.states + 10 * s;
   St<float> x0;
-  x0.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x0.p = to_local_f(P.grid[s], xs);
   x0.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
   x0.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
   const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   env.N = N;
   env.dyn = sc.dyn;
   const double* gl = in.goals + 10 * s;
-  env.pg = {static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  env.pg = to_local_f(P.grid[s], gl);
   env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
   env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
   env.q_p = sc.q_p;
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   pr.key = stream_key(seed, static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k));
   const double* xs = in.states + 10 * s;
   St<float> x;
-  x.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x.p = to_local_f(P.grid[s], xs);
   x.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
   x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
   CostSums<float> cs{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, true, false, false};
@@ -876,7 +876,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn i
   }
   const double* xs = in.states + 10 * s;
   St<float> x;
-  x.p = {static_cast<float>(xs[0]), static_cast<float>(xs[1]), static_cast<float>(xs[2])};
+  x.p = to_local_f(P.grid[s], xs);
   x.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
   x.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
   int n_ok = N;
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn i
   __syncwarp();
   // per-state terms + collision, lane = step
   const double* gl = in.goals + 10 * s;
-  const V3<float> pg{static_cast<float>(gl[0]), static_cast<float>(gl[1]), static_cast<float>(gl[2])};
+  const V3<float> pg = to_local_f(P.grid[s], gl);
   const V3<float> vg{static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
   const Q4<float> qg{static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]),
                      static_cast<float>(gl[9])};
@@ -948,7 +948,99 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta32) k_stage1_warp32(BatchIn i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Screening-drift diagnostic, FP32 half (amppi_screen_drift; DESIGN.md §2
+// "The d_max jump"): sampled rollouts of scenes [s0, s0 + S) integrated as
+// the screening integrates them (FP32 draws, clamp, RK4; rollout_costs<float>
+// has the screening's sums and order for every sample it does not abort),
+// with no abort bound.  Per step it stores the FP32 position and the exact
+// FP32 squared clearance (reach: the grid cell h, no early stop); per rollout the
+// screening cost (sign bit = flagged, +inf = invalid).  k_drift64 (k_plan64.cu)
+// integrates the same rollouts in FP64 and compares.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_drift32(BatchIn in, Perception P, Plan pl, DevConfig cfg,
+                                                 const ScreenConsts sc, int iter, int s0, int S, int kstride,
+                                                 float4* steps, float* cost) {
+  const int kn = (cfg.k_hi - cfg.k_lo + kstride - 1) / kstride;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= static_cast<int64_t>(S) * cfg.M * kn) return;
+  const int kk = static_cast<int>(r % kn);
+  const int m = static_cast<int>((r / kn) % cfg.M);
+  const int s = s0 + static_cast<int>(r / (static_cast<int64_t>(kn) * cfg.M));
+  const int k = cfg.k_lo + kk * kstride;
+  const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
+  const int N = cfg.N;
+  float4* st = steps + r * N;
+  if (!pl.alive[smi]) {
+    cost[r] = __int_as_float(0x7fc00000);  // NaN: instance not planned
+    return;
+  }
+  float unom[4 * kMaxN];
+  for (int i = 0; i < 4 * N; ++i) unom[i] = static_cast<float>(pl.nominal[smi * N * 4 + i]);  // as k_unom32
+  RolloutEnv<float> env;
+  env.unom = unom;
+  env.guide = pl.guide32 + smi * N;
+  env.N = N;
+  env.dyn = sc.dyn;
+  const double* gl = in.goals + 10 * s;
+  env.pg = to_local_f(P.grid[s], gl);
+  env.vg = {static_cast<float>(gl[3]), static_cast<float>(gl[4]), static_cast<float>(gl[5])};
+  env.qg = {static_cast<float>(gl[6]), static_cast<float>(gl[7]), static_cast<float>(gl[8]), static_cast<float>(gl[9])};
+  env.q_p = sc.q_p;
+  env.q_v = sc.q_v;
+  env.q_q = sc.q_q;
+  env.cs = sc.cs;
+  env.ca = sc.ca;
+  env.cdmin = sc.cdmin;
+  env.cdmax = sc.cdmax;
+  env.grid = P.grid[s];
+  env.grec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+  env.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
+  env.gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
+  env.gpts = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
+  env.has_guide = true;
+  env.abort_above = __int_as_float(0x7f800000);
+  env.wq_track = sc.wq_track;
+  env.wq_vnorm = sc.wq_vnorm;
+  env.wq_c = sc.wq_c;
+  env.wq_cd = sc.wq_cd;
+  env.reach2 = sc.reach2;
+  env.band = sc.band;
+  const double* xs = in.states + 10 * s;
+  St<float> x0;
+  x0.p = to_local_f(P.grid[s], xs);
+  x0.q = {static_cast<float>(xs[3]), static_cast<float>(xs[4]), static_cast<float>(xs[5]), static_cast<float>(xs[6])};
+  x0.v = {static_cast<float>(xs[7]), static_cast<float>(xs[8]), static_cast<float>(xs[9])};
+  const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+  const PertRngF pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                    sc.sigma[0], sc.sigma[1], sc.sigma[2], sc.sigma[3]};
+  const CostSums<float> cs = rollout_costs(x0, env, pr);
+  cost[r] = cs.valid ? screen_store(stage1_total(cs, env.wq_track, env.wq_vnorm, env.wq_c, env.wq_cd), cs.amb)
+                     : __int_as_float(0x7f800000);
+  float pos[4 * kMaxN];
+  for (int j = 0; j < N; ++j) pos[4 * j] = pos[4 * j + 1] = pos[4 * j + 2] = __int_as_float(0x7fc00000);
+  rollout_costs<float, PertRngF, true>(x0, env, pr, nullptr, nullptr, pos);
+  const float lim = env.grid.h_f;  // exact below the cell size (k_drift64)
+  uint32_t hint = kNoHint;
+  for (int j = 0; j < N; ++j) {
+    const V3<float> p{pos[4 * j], pos[4 * j + 1], pos[4 * j + 2]};
+    const float d2 = isfinite(p.x) ? nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, p, lim * lim,
+                                                     0.f, &hint)
+                                   : __int_as_float(0x7fc00000);
+    st[j] = make_float4(p.x, p.y, p.z, d2);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_drift32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
+                           int s0, int S, int kstride, float4* steps, float* cost, cudaStream_t st) {
+  const int kn = (cfg.k_hi - cfg.k_lo + kstride - 1) / kstride;
+  const int64_t rows = static_cast<int64_t>(S) * cfg.M * kn;
+  k_drift32<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(in, P, pl, cfg, screen_consts(cfg), iter, s0, S,
+                                                                      kstride, steps, cost);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
                               cudaStream_t st, KernelTimer* timer) {

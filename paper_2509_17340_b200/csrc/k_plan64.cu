@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(64) k_anchors(BatchIn in, Perception P, Plan p
     pl.guide64[3 * gi] = o.x;
     pl.guide64[3 * gi + 1] = o.y;
     pl.guide64[3 * gi + 2] = o.z;
-    pl.guide32[gi] = make_float4(static_cast<float>(o.x), static_cast<float>(o.y), static_cast<float>(o.z), 0.f);
+    const V3<float> of = to_local_f(P.grid[s], &pl.guide64[3 * gi]);  // the screening's local frame
+    pl.guide32[gi] = make_float4(of.x, of.y, of.z, 0.f);
   }
   // warm start: shifted previous winner, or hover (ensemble.cpp:68-77)
   const int plen = in.prev ? (in.prev_len ? in.prev_len[s] : N) : 0;
@@ -1295,7 +1296,129 @@ __global__ void k_gather(Plan pl, DevConfig cfg, int S, GatherOut g) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Screening-drift diagnostic, FP64 half (amppi_screen_drift): the rollouts
+// k_drift32 integrated in FP32, integrated again as the refine does (FP64
+// draws, oracle op order), with the exact FP64 clearance per step.  Reduced
+// into acc[kDriftSlots] (non-negative doubles as ordered bits for the maxima):
+//   0 rollouts compared (valid in both)      1 max |p32 - p64| (m)
+//   2 max |d32 - d64| where min(d) < h - 1e-4 (m; h = grid cell > d_max + band)   3 steps in slot 2
+//   4 steps on opposite sides of d_max outside the band (soundness: 0)
+//   5 steps the screening flags (|d32 - d_max| < band)
+//   6 max |S32 - S64| / |S64| over unflagged rollouts
+//   7 rollouts valid in one precision only
+// d32 is the screening's own distance: sqrt.approx of the FP32 squared
+// clearance; band = 1e-4 d_max + 1e-4 as amb_band.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_max_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u(unsigned long long v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(128) k_drift64(BatchIn in, Perception P, Plan pl, DevConfig cfg, int iter, int s0,
+                                                 int S, int kstride, const float4* steps, const float* cost,
+                                                 unsigned long long* acc) {
+  const int kn = (cfg.k_hi - cfg.k_lo + kstride - 1) / kstride;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t rows = static_cast<int64_t>(S) * cfg.M * kn;
+  double dp_max = 0.0, dd_max = 0.0, rel_max = 0.0;
+  unsigned long long n_roll = 0, n_cmp = 0, n_viol = 0, n_amb = 0, n_mis = 0;
+  const float c32 = r < rows ? cost[r] : __int_as_float(0x7fc00000);
+  if (r < rows && !isnan(c32)) {
+    const int kk = static_cast<int>(r % kn);
+    const int m = static_cast<int>((r / kn) % cfg.M);
+    const int s = s0 + static_cast<int>(r / (static_cast<int64_t>(kn) * cfg.M));
+    const int k = cfg.k_lo + kk * kstride;
+    const int64_t smi = static_cast<int64_t>(s) * cfg.M + m;
+    const int N = cfg.N;
+    const RolloutEnv<double> env = make_env64(in, P, pl, cfg, s, m, pl.nominal + smi * N * 4);
+    const St<double> x0 = load_state(in.states + 10 * s);
+    const uint64_t iter_cycle = in.cycles[s] * static_cast<uint64_t>(cfg.iterations) + static_cast<uint64_t>(iter);
+    const PertRngD pr{stream_key(in.seeds[s], static_cast<uint64_t>(m), iter_cycle, static_cast<uint64_t>(k)),
+                      cfg.sigma[0], cfg.sigma[1], cfg.sigma[2], cfg.sigma[3]};
+    const CostSums<double> cs = rollout_costs(x0, env, pr);
+    const bool v32 = isfinite(c32);
+    if (cs.valid != v32) {
+      n_mis = 1;
+    } else if (cs.valid) {
+      n_roll = 1;
+      const double c64 = stage1_total(cs, cfg.q_track, cfg.q_vnorm, cfg.q_c, cfg.q_c_delta);
+      if (!signbit(c32)) rel_max = fabs(static_cast<double>(c32) - c64) / fmax(fabs(c64), 1e-300);
+      double pos[4 * 64];
+      rollout_costs<double, PertRngD, true>(x0, env, pr, nullptr, nullptr, pos);
+      const float dmaxf = static_cast<float>(cfg.col_d_max);
+      const float band = 1e-4f * dmaxf + 1e-4f;
+      // both queries are exact below the grid cell h (>= d_max + band): the
+      // 27 cells around a position hold every point that close
+      const double lim = env.grid.h;
+      uint32_t hint = kNoHint;
+      const float4* st = steps + r * N;
+      for (int j = 0; j < N; ++j) {
+        const float4 q = st[j];
+        const V3<double> p{pos[4 * j], pos[4 * j + 1], pos[4 * j + 2]};
+        // q is in the screening's local frame (to_local_f)
+        const V3<double> e{static_cast<double>(q.x) - (p.x - env.grid.org[0]),
+                           static_cast<double>(q.y) - (p.y - env.grid.org[1]),
+                           static_cast<double>(q.z) - (p.z - env.grid.org[2])};
+        dp_max = fmax(dp_max, sqrt(sqnorm(e)));
+        const double d64 = sqrt(nearest_sq_exact(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, p, lim * lim, 0.0,
+                                                 &hint));
+        const float d32f = sqrt_approx(q.w);
+        const double d32 = d32f;  // +inf past the reach in both
+        if (fmin(d32, d64) < lim - 1e-4) {
+          dd_max = fmax(dd_max, fabs(d32 - d64));
+          ++n_cmp;
+#ifdef AMPPI_DRIFT_DEBUG
+          if (fabs(d32 - d64) > 1e-3 && atomicAdd(acc + 8, 1ull) < 12)
+            printf("drift s=%d m=%d k=%d j=%d d32=%.9g d64=%.9g p64=(%.9g %.9g %.9g) p32=(%.9g %.9g %.9g) "
+                   "grid origin=(%.9g %.9g %.9g) h=%.9g dims=(%d %d %d)\n",
+                   s, m, k, j, d32, d64, p.x, p.y, p.z, q.x, q.y, q.z, env.grid.origin[0], env.grid.origin[1],
+                   env.grid.origin[2], env.grid.h, env.grid.dims[0], env.grid.dims[1], env.grid.dims[2]);
+#endif
+        }
+        if (fabsf(d32f - dmaxf) < band) {
+          ++n_amb;
+        } else if ((d32f < dmaxf) != (d64 < cfg.col_d_max)) {
+          ++n_viol;
+        }
+      }
+    }
+  }
+  dp_max = warp_max_d(dp_max);
+  dd_max = warp_max_d(dd_max);
+  rel_max = warp_max_d(rel_max);
+  n_roll = warp_sum_u(n_roll);
+  n_cmp = warp_sum_u(n_cmp);
+  n_viol = warp_sum_u(n_viol);
+  n_amb = warp_sum_u(n_amb);
+  n_mis = warp_sum_u(n_mis);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc + 0, n_roll);
+    atomicMax(acc + 1, static_cast<unsigned long long>(__double_as_longlong(dp_max)));
+    atomicMax(acc + 2, static_cast<unsigned long long>(__double_as_longlong(dd_max)));
+    atomicAdd(acc + 3, n_cmp);
+    atomicAdd(acc + 4, n_viol);
+    atomicAdd(acc + 5, n_amb);
+    atomicMax(acc + 6, static_cast<unsigned long long>(__double_as_longlong(rel_max)));
+    atomicAdd(acc + 7, n_mis);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_drift64(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
+                           int s0, int S, int kstride, const float4* steps, const float* cost,
+                           unsigned long long* acc, cudaStream_t st) {
+  const int kn = (cfg.k_hi - cfg.k_lo + kstride - 1) / kstride;
+  const int64_t rows = static_cast<int64_t>(S) * cfg.M * kn;
+  k_drift64<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(in, P, pl, cfg, iter, s0, S, kstride, steps,
+                                                                      cost, acc);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gather(const Plan& pl, const DevConfig& cfg, int S, const GatherOut& g, cudaStream_t st) {
   k_gather<<<S, 128, 0, st>>>(pl, cfg, S, g);

@@ -123,4 +123,15 @@ int device_sms();  // SM count of the current device (cached)
 cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
                               cudaStream_t st, KernelTimer* timer);
 
+// Screening-drift diagnostic (amppi_screen_drift): sampled rollouts of scenes
+// [s0, s0 + S) in FP32 as the screening runs them (k_plan32.cu), then in FP64
+// as the refine runs them, compared per step (k_plan64.cu).  steps: [rows*N],
+// cost: [rows], rows = S * M * ceil((k_hi - k_lo) / kstride); acc: [8].
+constexpr int kDriftSlots = 8;
+cudaError_t launch_drift32(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
+                           int s0, int S, int kstride, float4* steps, float* cost, cudaStream_t st);
+cudaError_t launch_drift64(const BatchIn& in, const Perception& P, const Plan& pl, const DevConfig& cfg, int iter,
+                           int s0, int S, int kstride, const float4* steps, const float* cost,
+                           unsigned long long* acc, cudaStream_t st);
+
 }  // namespace amppi_dev

@@ -69,6 +69,7 @@ struct DevConfig {
 };
 
 struct GridMeta {
+  double org[3];  // the FP32 local frame: FP32 grid data and screening positions are float(x - org) (the snapshot pose)
   double origin[3];
   double h, inv_h;
   float origin_f[3];

@@ -595,6 +595,30 @@ class Planner:
     def cycle_batch_device(self, dev: dict, out: dict, n_scenes: int, r_max: float = 10.0) -> None:
         """Same cycle on device-resident inputs (dict of raw device pointers,
         e.g. torch tensors' data_ptr()); enqueued on the planner's stream."""
+        bi = self._device_batch_input(dev, n_scenes, r_max)
+        bo = _abi.BatchOutput()
+        for k, ct in (("status", ctypes.c_int32), ("winner", ctypes.c_int32), ("control", ctypes.c_double),
+                      ("winner_nominal", ctypes.c_double), ("stage2", ctypes.c_double),
+                      ("breakdown", ctypes.c_double)):
+            if out.get(k):
+                setattr(bo, k, ctypes.cast(ctypes.c_void_p(out[k]), ctypes.POINTER(ct)))
+        self._gen += 1  # the batch overwrites the single-scene snapshot slot
+        self._check(self.lib.amppi_cycle_batch_device(self._h, ctypes.byref(bi), ctypes.byref(bo)))
+
+    DRIFT_KEYS = ("rollouts", "max_pos_diff", "max_clearance_diff", "steps_compared", "dmax_side_violations",
+                  "flagged_steps", "max_rel_cost_diff", "validity_mismatches")
+
+    def screen_drift(self, dev: dict, n_scenes: int, iteration: int = 0, sample_stride: int = 1) -> dict:
+        """FP32-screening vs FP64 drift of the batch cycle_batch_device just
+        planned on `dev` (amppi_screen_drift; verification only)."""
+        bi = self._device_batch_input(dev, n_scenes, 10.0)
+        st = np.zeros(8)
+        self._check(self.lib.amppi_screen_drift(self._h, ctypes.byref(bi), int(iteration), int(sample_stride),
+                                                _ptr(st, ctypes.c_double)))
+        return {k: (float(v) if k.startswith("max") else int(v)) for k, v in zip(self.DRIFT_KEYS, st)}
+
+    @staticmethod
+    def _device_batch_input(dev: dict, n_scenes: int, r_max: float):
         bi = _abi.BatchInput()
         bi.n_scenes = n_scenes
         bi.point_offsets = ctypes.cast(ctypes.c_void_p(dev["offsets"]), _abi.c_int64_p)
@@ -608,14 +632,7 @@ class Planner:
         if dev.get("prev"):
             bi.previous = ctypes.cast(ctypes.c_void_p(dev["prev"]), _abi.c_double_p)
         bi.r_max = float(r_max)
-        bo = _abi.BatchOutput()
-        for k, ct in (("status", ctypes.c_int32), ("winner", ctypes.c_int32), ("control", ctypes.c_double),
-                      ("winner_nominal", ctypes.c_double), ("stage2", ctypes.c_double),
-                      ("breakdown", ctypes.c_double)):
-            if out.get(k):
-                setattr(bo, k, ctypes.cast(ctypes.c_void_p(out[k]), ctypes.POINTER(ct)))
-        self._gen += 1  # the batch overwrites the single-scene snapshot slot
-        self._check(self.lib.amppi_cycle_batch_device(self._h, ctypes.byref(bi), ctypes.byref(bo)))
+        return bi
 
     def synchronize(self) -> None:
         self._check(self.lib.amppi_synchronize(self._h))

@@ -228,6 +228,23 @@ def test_c1_forest_cycle(oracle, precision):
              last_applied=np.array([10.2, 0.0, 0.1, 0.0]), cycle=100, seed=1, precision=precision, f64=False)
 
 
+@pytest.mark.parametrize("path", ["latency", "throughput"])
+def test_far_from_world_origin(oracle, path):
+    """The same forest cycle translated 8 km / 4 km from the world origin,
+    where an FP32 world coordinate's ulp (1e-3 m) is five times the d_max band:
+    the FP32 screening runs in the snapshot pose's local frame (to_local_f),
+    so its costs keep their accuracy and the plan still matches the oracle."""
+    off = np.array([8192.0, -4096.0, 0.0])
+    cloud, pose = forest_cycle_inputs(oracle)
+    cloud = np.asarray(cloud, dtype=np.float32).astype(np.float64) + off  # exact in FP64
+    pose = pose.copy()
+    pose[:3] += off
+    prev = np.tile(np.array([9.81, 0.1, -0.05, 0.02]), (30, 1))
+    cfg = make_cfg(4, 2, K=256, N=30) if path == "latency" else make_cfg(8, 8, K=2048, N=30)
+    run_case(oracle, cfg, cloud, pose, pose, goal_target=tuple(np.array([45.0, 0.0, 2.0]) + off), previous=prev,
+             last_applied=np.array([10.2, 0.0, 0.1, 0.0]), cycle=100, seed=1, f64=True)
+
+
 def test_large_ensemble_shape(oracle):
     """C4 shape (8x8 anchors, N=50) at a reduced K the oracle finishes quickly."""
     cfg = make_cfg(8, 8, K=512, N=50)

@@ -49,7 +49,7 @@ def main():
     res = {name: [] for name, _ in variants}
     for r in range(reps):
         for name, lib in variants:
-            env = dict(os.environ, AB_ROOT=ROOT, AMPPI_LIB_PATH=os.path.join(ROOT, lib))
+            env = dict(os.environ, AB_ROOT=ROOT, AMPPI_LIB_PATH=os.path.join(ROOT, lib), AMPPI_ABI_LENIENT="1")
             out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
             line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
             if not line:
