@@ -226,6 +226,9 @@ __device__ __forceinline__ void normal_pair(uint64_t key, uint32_t p, double& n0
 #ifndef AMPPI_F32_BOX
 #define AMPPI_F32_BOX 1  // nearest_sq_exact prunes boxes in FP32 with a rounding margin (0: FP64 box test)
 #endif
+#ifndef AMPPI_F32_PRESCREEN
+#define AMPPI_F32_PRESCREEN 1  // nearest_sq_exact prescreens points in FP32 (needs AMPPI_F32_BOX)
+#endif
 #ifndef AMPPI_LOG_SERIES
 #define AMPPI_LOG_SERIES 1
 #endif
@@ -503,10 +506,31 @@ __device__ __forceinline__ float box_gap_sq(uint32_t lx, uint32_t hx, uint32_t l
   return sq3f(fmaxf(fmaxf(dx.x, -dx.y), 0.f), fmaxf(fmaxf(dy.x, -dy.y), 0.f), fmaxf(fmaxf(dz.x, -dz.y), 0.f));
 }
 
+// Squared distances from p to the 4 points of one FP32 point block
+// ({x0..x3}, {y0..y3}, {z0..z3}), as two packed FP32x2 pairs: per pair one
+// FADD2 per axis, FMUL2, two FFMA2 (sm_100 packed FP32) -- the sq3f shape.
+__device__ __forceinline__ void block_d2(const float4* __restrict__ blk, V3<float> p, float2& d01, float2& d23) {
+  const float4 X = __ldg(blk), Y = __ldg(blk + 1), Z = __ldg(blk + 2);
+  const float2 npx = make_float2(-p.x, -p.x), npy = make_float2(-p.y, -p.y), npz = make_float2(-p.z, -p.z);
+  float2 dx = __fadd2_rn(make_float2(X.x, X.y), npx), dy = __fadd2_rn(make_float2(Y.x, Y.y), npy),
+         dz = __fadd2_rn(make_float2(Z.x, Z.y), npz);
+  d01 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+  dx = __fadd2_rn(make_float2(X.z, X.w), npx);
+  dy = __fadd2_rn(make_float2(Y.z, Y.w), npy);
+  dz = __fadd2_rn(make_float2(Z.z, Z.w), npz);
+  d23 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+}
+
+__device__ __forceinline__ float block_min_d2(const float4* __restrict__ pts, uint32_t blk, V3<float> p) {
+  float2 a, b;
+  block_d2(pts + 3 * blk, p, a, b);
+  return fminf(fminf(a.x, a.y), fminf(b.x, b.y));
+}
+
 __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ rec,
                                                    const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
-                                                   const double* __restrict__ pts, V3<double> p, double lim2,
-                                                   double stop2, uint32_t* hint) {
+                                                   const double* __restrict__ pts, const float4* __restrict__ pts32,
+                                                   V3<double> p, double lim2, double stop2, uint32_t* hint) {
   double best = __longlong_as_double(0x7ff0000000000000ll);
   if (g.dims[0] == 0) return best;
   uint32_t bi = *hint;
@@ -536,12 +560,14 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
                      static_cast<float>(p.z - g.org[2])};  // to_local_f
   const float e_ax = 0x1.0p-23f * (fmaxf(fmaxf(fabsf(pf.x), fabsf(pf.y)), fabsf(pf.z)) + 2.0f * g.h_f + 1.0f);
   const float slack = 3.5f * e_ax * __double2float_ru(sqrt(lim2)) + 4.0f * e_ax * e_ax;
-  auto far = [&](float gap2, double thr) { return gap2 > __double2float_ru(thr) * (1.0f + 1e-6f) + slack; };
+  // (a float squared distance above cut cannot be within fmin(best, lim2))
+  auto cut_of = [&](double b) { return __double2float_ru(fmin(b, lim2)) * (1.0f + 1e-6f) + slack; };
+  float cut = cut_of(best);
   auto rec_far = [&](const uint4& ra, const uint4& rb) {
-    return far(box_gap_sq(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w, pf), fmin(best, lim2));
+    return box_gap_sq(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w, pf) > cut;
   };
   auto leaf_far = [&](const uint4& la, const uint4& lb) {
-    return far(box_gap_sq(la.x, la.y, la.z, la.w, lb.x, lb.y, pf), fmin(best, lim2));
+    return box_gap_sq(la.x, la.y, la.z, la.w, lb.x, lb.y, pf) > cut;
   };
 #else
   // box lower bounds in the same arithmetic as the point distances (sqnorm of
@@ -577,13 +603,41 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
         const uint4 la = lf[0], lb = lf[1];
         if (leaf_far(la, lb)) continue;
         const uint32_t te = min(t + kLeafSize, k1);
+#if AMPPI_F32_BOX && AMPPI_F32_PRESCREEN
+        // FP32 prescreen: the leaf's 4-point float blocks (the screening's,
+        // same local frame) in packed FP32x2; a point's FP32 squared distance
+        // is off from the true one by no more than a box's, so FP64 is
+        // evaluated only for points that can still beat best (or reach
+        // lim2).  The blocks may hold a few real points of the neighbouring
+        // leaves (harmless: real points) and +inf padding (never evaluated).
+        for (uint32_t u = t / kPointBlock; u <= (te - 1) / kPointBlock; ++u) {
+          float2 a01, a23;
+          block_d2(pts32 + 3 * u, pf, a01, a23);
+          const float dq[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (!(dq[i] <= cut)) continue;
+            const uint32_t k = u * kPointBlock + i;
+            const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
+            if (dd < best) {
+              best = dd;
+              bi = k;
+              cut = cut_of(best);
+            }
+          }
+        }
+#else
         for (uint32_t k = t; k < te; ++k) {
           const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
           if (dd < best) {
             best = dd;
             bi = k;
+#if AMPPI_F32_BOX
+            cut = cut_of(best);
+#endif
           }
         }
+#endif
         if (best < stop2) {
           *hint = bi;
           return best;
@@ -593,27 +647,6 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
   }
   *hint = bi;
   return best;
-}
-
-// Squared distances from p to the 4 points of one FP32 point block
-// ({x0..x3}, {y0..y3}, {z0..z3}), as two packed FP32x2 pairs: per pair one
-// FADD2 per axis, FMUL2, two FFMA2 (sm_100 packed FP32) -- the sq3f shape.
-__device__ __forceinline__ void block_d2(const float4* __restrict__ blk, V3<float> p, float2& d01, float2& d23) {
-  const float4 X = __ldg(blk), Y = __ldg(blk + 1), Z = __ldg(blk + 2);
-  const float2 npx = make_float2(-p.x, -p.x), npy = make_float2(-p.y, -p.y), npz = make_float2(-p.z, -p.z);
-  float2 dx = __fadd2_rn(make_float2(X.x, X.y), npx), dy = __fadd2_rn(make_float2(Y.x, Y.y), npy),
-         dz = __fadd2_rn(make_float2(Z.x, Z.y), npz);
-  d01 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-  dx = __fadd2_rn(make_float2(X.z, X.w), npx);
-  dy = __fadd2_rn(make_float2(Y.z, Y.w), npy);
-  dz = __fadd2_rn(make_float2(Z.z, Z.w), npz);
-  d23 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-}
-
-__device__ __forceinline__ float block_min_d2(const float4* __restrict__ pts, uint32_t blk, V3<float> p) {
-  float2 a, b;
-  block_d2(pts + 3 * blk, p, a, b);
-  return fminf(fminf(a.x, a.y), fminf(b.x, b.y));
 }
 
 // FP32 screening query: as nearest_sq_exact, plus a second branch-and-bound

@@ -324,6 +324,7 @@ __device__ __forceinline__ RolloutEnv<double> make_env64(const BatchIn& in, cons
   e.gnbr = P.grid_nbr + static_cast<int64_t>(s) * kPadCells;
   e.gleaf = P.grid_leaf + static_cast<int64_t>(s) * kCells * 2;
   e.gpts = P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3;
+  e.gpts32 = P.grid_pts32 + static_cast<int64_t>(s) * kCells;
   e.has_guide = true;
   e.abort_above = __longlong_as_double(0x7ff0000000000000ll);
   return e;
@@ -1187,6 +1188,7 @@ __global__ void __launch_bounds__(128) k_col_query(Perception P, Plan pl, DevCon
                                        P.grid_nbr + static_cast<int64_t>(s) * kPadCells,
                                        P.grid_leaf + static_cast<int64_t>(s) * kCells * 2,
                                        P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3,
+                                       P.grid_pts32 + static_cast<int64_t>(s) * kCells,
                                        V3<double>{pp[0], pp[1], pp[2]}, cfg.col_d_max * cfg.col_d_max,
                                        cfg.col_d_min * cfg.col_d_min, &hint);
     pl.col_terms[i] = collision_term(sqrt(d2), cfg.col_scale, cfg.col_slope, cfg.col_d_min, cfg.col_d_max);
@@ -1365,7 +1367,7 @@ __global__ void __launch_bounds__(128) k_drift64(BatchIn in, Perception P, Plan 
                            static_cast<double>(q.y) - (p.y - env.grid.org[1]),
                            static_cast<double>(q.z) - (p.z - env.grid.org[2])};
         dp_max = fmax(dp_max, sqrt(sqnorm(e)));
-        const double d64 = sqrt(nearest_sq_exact(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, p, lim * lim, 0.0,
+        const double d64 = sqrt(nearest_sq_exact(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, env.gpts32, p, lim * lim, 0.0,
                                                  &hint));
         const float d32f = sqrt_approx(q.w);
         const double d32 = d32f;  // +inf past the reach in both

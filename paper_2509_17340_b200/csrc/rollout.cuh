@@ -40,6 +40,7 @@ struct RolloutEnv<double> {
   const uint32_t* gnbr;
   const uint4* gleaf;
   const double* gpts;
+  const float4* gpts32;  // the FP32 point blocks (local frame): the exact query's prescreen
   bool has_guide;
   double abort_above;
   mutable uint32_t hint = kNoHint;  // nearest point of the previous query (per rollout)
@@ -50,7 +51,7 @@ struct RolloutEnv<double> {
   __device__ __forceinline__ double unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ double attitude(Q4<double> q) const { return attitude_err_exact(q, gt); }
   __device__ __forceinline__ double collision(V3<double> p) const {
-    const double d2 = nearest_sq_exact(grid, grec, gnbr, gleaf, gpts, p, cdmax * cdmax, cdmin * cdmin, &hint);
+    const double d2 = nearest_sq_exact(grid, grec, gnbr, gleaf, gpts, gpts32, p, cdmax * cdmax, cdmin * cdmin, &hint);
     return collision_term(sqrt(d2), cs, ca, cdmin, cdmax);
   }
 };
