@@ -525,6 +525,15 @@ constexpr int kMainGroups = AMPPI_MAIN_GROUPS;
 constexpr int kBoundSamples = AMPPI_BOUND_SAMPLES;  // 32, 16, 8 or 4
 static_assert(32 % kBoundSamples == 0, "bound samples divide a warp");
 constexpr int kMainCompact = AMPPI_MAIN_COMPACT;
+// Bound pass as a cascade: samples [0, 8) in full (4 instances per warp),
+// then samples [8, 32) aborted against those 8 (one warp per instance).  The
+// 32-sample minimum U the main pass aborts against is unchanged: a cascade
+// sample stops only once its partial cost passes U8 + window >= U8, so its
+// final cost could not have lowered the minimum.
+#ifndef AMPPI_BOUND_CASCADE
+#define AMPPI_BOUND_CASCADE 0
+#endif
+constexpr int kCascadeFirst = 8;
 constexpr int kStateWords = 22;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint amb
 
 // Samples [k_lo + kb0, k_lo + kend) of every instance, aborted against the
@@ -1076,7 +1085,12 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   const int k1 = in.injected ? 32 : kBoundSamples;
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
-    if (in.injected || kBoundSamples == 32) {
+    if (AMPPI_BOUND_CASCADE && !in.injected && kBoundSamples == 32) {
+      constexpr int G = 32 / kCascadeFirst;
+      k_stage1_bound<G><<<static_cast<unsigned>((SM + G - 1) / G), 32, 0, st>>>(in, P, pl, cfg, sc, iter);
+      k_stage1_f32c<32, kMainCompact, 32><<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter,
+                                                                                   kCascadeFirst, 32, kCascadeFirst);
+    } else if (in.injected || kBoundSamples == 32) {
       kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
     } else {
       constexpr int G = 32 / kBoundSamples;
