@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; the ranges cost nothing unless a profiler injects a tool
+
 #include "../../include/amppi_b200.h"
 #include "kernels.h"
 #include "layout.h"
@@ -228,6 +230,14 @@ struct amppi_ctx {
     cudaError_t _e = (expr);                                  \
     if (_e != cudaSuccess) return ctx->cuda_fail(_e, #expr);  \
   } while (0)
+
+// NVTX range over a host entry point (nsys / ncu --nvtx see the API phases).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 
@@ -601,6 +611,7 @@ Perception shift_perception(const Perception& p, int64_t s0) {
 // the chunk's own offset, so chunks can run concurrently on different
 // streams.  Needs the fused snapshot (>= 148 scenes per chunk).
 int run_chunk(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, int64_t s0, int chunk, cudaStream_t st) {
+  NvtxRange nvtx_range("amppi chunk (snapshot + plan)");
   const DevConfig& dc = ctx->dc;
   const Perception P = shift_perception(ctx->P, s0);
   Plan pl = shift_plan(ctx->pl, s0, dc);
@@ -822,6 +833,7 @@ int amppi_set_stream(amppi_ctx* ctx, void* stream) {
 
 static int snapshot_common(amppi_ctx* ctx, const void* pts, bool f64, int64_t n, const amppi_state* pose,
                            double r_max, bool on_device = false) {
+  NvtxRange nvtx_range("amppi_snapshot");
   if (!ctx || (!pts && n > 0) || !pose || n < 0) return ctx ? ctx->fail(AMPPI_INVALID_ARGUMENT, "bad arguments")
                                                             : AMPPI_INVALID_ARGUMENT;
   if (!(r_max > 0.0)) return ctx->fail(AMPPI_INVALID_ARGUMENT, "r_max must be positive");
@@ -1013,6 +1025,7 @@ extern "C" {
 int amppi_plan(amppi_ctx* ctx, const amppi_state* x, const amppi_goal* goal, const double* previous,
                int32_t previous_len, const amppi_control* last_applied, uint64_t cycle, uint64_t seed,
                const double* injected, amppi_plan_result* out) {
+  NvtxRange nvtx_range("amppi_plan");
   if (!ctx) return AMPPI_INVALID_ARGUMENT;
   BatchIn in{};
   if (int rc = stage_plan_inputs(ctx, x, goal, previous, previous_len, last_applied, cycle, seed, injected, &in);
@@ -1124,6 +1137,7 @@ static int gather_chunk(amppi_ctx* ctx, int s0, int s1, const amppi_batch_output
 static void collect_chunk(amppi_ctx* ctx, int s0, int s1, amppi_batch_output* out);
 
 int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_output* out) {
+  NvtxRange nvtx_range("amppi_cycle_batch");
   if (!ctx || !in) return AMPPI_INVALID_ARGUMENT;
   const int S = in->n_scenes;
   if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
@@ -1284,6 +1298,7 @@ int amppi_cycle_batch(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_o
 }
 
 int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_batch_output* out) {
+  NvtxRange nvtx_range("amppi_cycle_batch_device");
   if (!ctx || !in) return AMPPI_INVALID_ARGUMENT;
   const int S = in->n_scenes;
   if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
@@ -1375,6 +1390,7 @@ int amppi_kernel_times_reset(amppi_ctx* ctx) {
 
 int amppi_screen_drift(amppi_ctx* ctx, const amppi_batch_input* in, int32_t iteration, int32_t sample_stride,
                        double* stats) {
+  NvtxRange nvtx_range("amppi_screen_drift");
   if (!ctx || !in || !stats) return AMPPI_INVALID_ARGUMENT;
   const DevConfig& dc = ctx->dc;
   const int S = in->n_scenes;
@@ -1548,6 +1564,7 @@ static size_t gather_bytes(const amppi_ctx* ctx) {
 }
 
 extern "C" int amppi_cycle_batch_submit(amppi_ctx* ctx, const amppi_batch_input* in, int64_t* ticket) {
+  NvtxRange nvtx_range("amppi_cycle_batch_submit");
   if (!ctx || !in || !ticket) return AMPPI_INVALID_ARGUMENT;
   const int S = in->n_scenes;
   if (S < 1 || S > ctx->S_cap) return ctx->fail(AMPPI_INVALID_ARGUMENT, "n_scenes out of range");
@@ -1645,6 +1662,7 @@ extern "C" int amppi_cycle_batch_submit(amppi_ctx* ctx, const amppi_batch_input*
 }
 
 extern "C" int amppi_cycle_batch_wait(amppi_ctx* ctx, int64_t ticket, amppi_batch_output* out) {
+  NvtxRange nvtx_range("amppi_cycle_batch_wait");
   if (!ctx) return AMPPI_INVALID_ARGUMENT;
   amppi_ctx::StreamSlot& sl = ctx->slots[ticket & 1];
   if (!sl.busy || sl.ticket != ticket) return ctx->fail(AMPPI_INVALID_ARGUMENT, "unknown or already collected ticket");
@@ -1772,6 +1790,7 @@ int amppi_loop_create(amppi_ctx* ctx, int32_t scene_kind, uint64_t scene_seed, u
 }
 
 int amppi_loop_run(amppi_loop* lp, int64_t cycles, int64_t* ran) {
+  NvtxRange nvtx_range("amppi_loop_run");
   using namespace amppi_dev;
   if (!lp) return AMPPI_INVALID_ARGUMENT;
   amppi_ctx* ctx = lp->ctx;
