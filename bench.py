@@ -54,9 +54,14 @@ BYTES_PER_POINT = 12  # FP32 xyz read once by the keying pass
 # ncu --set full of the FP32 screening kernels (bound + main pass) on the C5
 # batch as one chunk: DRAM read+write per step and the main pass's issue-slot
 # use (profiles/r02_c5_full.md)
-TRAFFIC_BYTES_PER_LAUNCH = 194.4e6
+TRAFFIC_BYTES_PER_LAUNCH = 197.4e6
 TRAFFIC_SOURCE = "profiles/r02_c5_full.md"
-ISSUE_ACTIVE_FRAC = 0.722
+ISSUE_ACTIVE_FRAC = 0.7225
+# FP32 flops the two screening kernels executed in one C5 launch, counted by ncu on the SASS page
+# (FFMA 2, FADD/FMUL 1, FFMA2 4, FADD2/FMUL2 2 per predicated-on thread instruction; the collision
+# queries' distance arithmetic included): main pass 2.109e11 + bound pass 5.552e10
+# (tools/ncu_lines.py <rep> --ops <kernel>, profiles/r02_c5_full.md)
+EXECUTED_FLOPS_PER_LAUNCH = 2.109e11 + 5.552e10
 
 
 def parse():
@@ -354,6 +359,11 @@ def screening_roofline(ktimes, rollout_steps_per_launch: float, peak: float, tot
             "algorithmic_flops_per_launch": per_launch_flops,
             "achieved_note": "effective rate: 440 flop x every rollout-step of the launch, including the steps the "
                              "abort bound proves outside the softmin support and never integrates",
+            "executed_flops_per_launch": EXECUTED_FLOPS_PER_LAUNCH,
+            "executed_tflops": EXECUTED_FLOPS_PER_LAUNCH / (screen_ms / 1e3) / 1e12,
+            "executed_frac": EXECUTED_FLOPS_PER_LAUNCH / (screen_ms / 1e3) / 1e12 / peak,
+            "executed_note": "FP32 flops the screening kernels executed (ncu SASS counts, collision-query distance "
+                             "arithmetic included, " + TRAFFIC_SOURCE + ") over this run's kernel time",
             "kernel_ms_per_launch": screen_ms, "kernel_share_of_step": (k_ms + b_ms) / total_ms,
             "issue_active_frac": ISSUE_ACTIVE_FRAC,
             "issue_source": "smsp__issue_active.avg.pct_of_peak_sustained_active of the main pass, ncu --set full, "

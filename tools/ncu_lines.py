@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Per-source-line summary of an `ncu --import-source on` capture.
 
-  tools/ncu_lines.py <report.ncu-rep> [top]        # per source line
-  tools/ncu_lines.py <report.ncu-rep> --ops         # per SASS opcode + executed FP32 flops
+  tools/ncu_lines.py <report.ncu-rep> [top [kernel-regex]]  # per source line
+  tools/ncu_lines.py <report.ncu-rep> --ops [kernel-regex]  # per SASS opcode + executed FP32 flops
 
 Reads `ncu -i ... --page source --csv --print-source cuda,sass` and prints,
 per CUDA source line (file:line), the share of warp-stall samples, of warp
@@ -18,8 +18,9 @@ import subprocess
 import sys
 
 
-def main(path, top=40):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+def main(path, top=40, kernel=None):
+    flt = ["-k", f"regex:{kernel}"] if kernel else []
+    out = subprocess.run(["ncu", "-i", path] + flt + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     cur_file, hdr = None, None
@@ -57,10 +58,11 @@ def main(path, top=40):
               f"`{a['src'].replace('|', '/')}` |")
 
 
-def ops(path, top=30):
+def ops(path, top=30, kernel=None):
     import re
 
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+    flt = ["-k", f"regex:{kernel}"] if kernel else []
+    out = subprocess.run(["ncu", "-i", path] + flt + ["--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = next(r for r in rows if r and r[0] == "Address")
@@ -84,7 +86,7 @@ def ops(path, top=30):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 2 and sys.argv[2] == "--ops":
-        ops(sys.argv[1])
+    if len(sys.argv) > 2 and sys.argv[2] == "--ops":  # [kernel regex]
+        ops(sys.argv[1], kernel=sys.argv[3] if len(sys.argv) > 3 else None)
     else:
-        main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+        main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40, sys.argv[3] if len(sys.argv) > 3 else None)
