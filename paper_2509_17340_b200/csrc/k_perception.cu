@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_LEAF_SCAN
+#define AMPPI_LEAF_SCAN 0  // 1: each cell's first thread walks the cell to flag its leaf starts (r01)
+#endif
 #ifndef AMPPI_LOCAL_FRAME
 #define AMPPI_LOCAL_FRAME 1  // FP32 grid data and screening relative to the snapshot pose (0: world frame)
 #endif
@@ -605,6 +608,10 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   uint4* __restrict__ gleaf = P.grid_leaf + cell_base * 2;
   uint8_t* lflag = reinterpret_cast<uint8_t*>(vals + kCellsPow2);  // [8192] (inside rng, past keys/vals)
   for (uint32_t i = tid; i < kCellsPow2; i += blockDim.x) lflag[i] = 0;
+#if !AMPPI_LEAF_SCAN
+  uint32_t* cstart = reinterpret_cast<uint32_t*>(lflag + kCellsPow2);  // [256] bitmap of cell starts (inside rng)
+  for (uint32_t i = tid; i < kCellsPow2 / 32; i += blockDim.x) cstart[i] = 0u;
+#endif
   // +inf padding of the last FP32 point block
   if (n_pts + tid < (n_pts + kPointBlock - 1) / kPointBlock * kPointBlock) {
     const uint32_t i = n_pts + tid;
@@ -624,13 +631,31 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     blk[2 * kPointBlock] = static_cast<float>(z - meta.org[2]);
     const uint32_t c = keys[i] >> 9;
     if (i == 0 || (keys[i - 1] >> 9) != c) {  // first point of cell c
+#if AMPPI_LEAF_SCAN
       uint32_t e = i + 1;
       while (e < n_pts && (keys[e] >> 9) == c) ++e;
       for (uint32_t t = i; t < e; t += kLeafSize) lflag[t] = 1;
+#else
+      atomicOr(&cstart[i >> 5], 1u << (i & 31));
+#endif
       atomicOr(&sm.rows[c / meta.dims[2]], 1u << (c % meta.dims[2]));  // row x*dims[1]+y, bit z
     }
   }
   __syncthreads();
+#if !AMPPI_LEAF_SCAN
+  // leaf starts: every point finds its cell's first point (the highest cell
+  // start at or below it, a few bitmap words back) and starts a leaf at
+  // offsets 0, kLeafSize, ... -- all threads in parallel, where a serial walk
+  // by each cell's first thread held its warp for the length of a dense cell
+  for (uint32_t i = tid; i < n_pts; i += blockDim.x) {
+    int w = static_cast<int>(i >> 5);
+    uint32_t bits = cstart[w] & (0xFFFFFFFFu >> (31u - (i & 31u)));
+    while (bits == 0u) bits = cstart[--w];
+    const uint32_t first = (static_cast<uint32_t>(w) << 5) + 31u - __clz(bits);
+    lflag[i] = ((i - first) % kLeafSize) == 0u;
+  }
+  __syncthreads();
+#endif
   SNAP_PHASE(6);  // scatter + leaf flags
   // leaf ids = prefix count of leaf starts (contiguous 16-point chunks per thread)
   const uint32_t kPerThread = kCellsPow2 / blockDim.x;  // blockDim.x divides 8192
