@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_LOG_BITS
+#define AMPPI_LOG_BITS 1  // fused pass A logs (cell, index, range bits); 0: (cell, index), pass B re-keys
+#endif
 #ifndef AMPPI_LEAF_SCAN
 #define AMPPI_LEAF_SCAN 0  // 1: each cell's first thread walks the cell to flag its leaf starts (r01)
 #endif
@@ -820,12 +823,19 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
   // pass A: minimum range bits per cell; a point that was <= the running
   // minimum when it arrived may be the final minimum and is logged (cell,
   // index) for the tie-break -- typically a third of the points
+#if AMPPI_LOG_BITS
+  // log entries carry the candidate's range bits, so pass B compares instead
+  // of re-keying (no second point load, FP64 transform and sqrt)
+  Candidate* __restrict__ log = P.cand + b;  // [points of this scene]
+  const bool rekey = e - b > 0x10000 || e > P.cand_cap;
+#else
   uint32_t* __restrict__ log = reinterpret_cast<uint32_t*>(P.cand) + b;  // [points of this scene]
+  const bool rekey = e - b > 0x10000 || e > 4 * P.cand_cap;
+#endif
   if (tid == 0) sm.n_cand = 0u;
   __syncthreads();
   // the log holds the scene's candidates at [b, e) of the context's candidate
   // buffer; a scene past 2^16 points or past that buffer re-keys in pass B
-  const bool rekey = e - b > 0x10000 || e > 4 * P.cand_cap;
   const int lane = tid & 31;
   constexpr int kUnroll = 4;  // points per thread per iteration
   // software pipeline: the next iteration's points are loaded before this
@@ -913,8 +923,14 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
         uint32_t base = 0;
         if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
         base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
-        if (cand && !rekey)
+        if (cand && !rekey) {
+#if AMPPI_LOG_BITS
+          log[base + __popc(want & ((1u << lane) - 1u))] =
+              Candidate{static_cast<uint32_t>(f), static_cast<uint32_t>(g - b), bits};
+#else
           log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
+#endif
+        }
       }
     }
   }
@@ -935,12 +951,17 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
   }
   const uint32_t n_cand = rekey ? 0u : sm.n_cand;
   for (uint32_t c = tid; c < n_cand; c += blockDim.x) {
+#if AMPPI_LOG_BITS
+    const Candidate cd = log[c];
+    if (cell_bits[cd.cell] == cd.bits) atomicMin(sm.idx + cd.cell, cd.idx);
+#else
     const uint32_t en = log[c];
     const int f = static_cast<int>(en >> 16);
     const uint32_t idx = en & 0xFFFFu;
     const V3<double> p = to_body(pose, load_point(in, b + idx));
     const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(sqrt(sqnorm(p))));
     if (cell_bits[f] == bits) atomicMin(sm.idx + f, idx);
+#endif
   }
   __syncthreads();
   for (int f = tid; f < kCells; f += blockDim.x) {

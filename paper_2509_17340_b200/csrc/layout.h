@@ -108,7 +108,7 @@ struct Perception {
   uint32_t* cell_idx;          // [S*7200] argmin point index
   Candidate* cand;             // [cap]
   unsigned long long* cand_count;
-  int64_t cand_cap;            // Candidate slots; the fused kernel's uint32 log holds 4 * cand_cap entries
+  int64_t cand_cap;            // Candidate slots (the fused kernel logs one Candidate per logged point)
   uint32_t* flags;             // device error word (kFlag*), mapped host memory
   const double* cell_dir;      // [7200*3] cell-centre directions (host libm)
   // outputs
