@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_POOL_STRIDED
+#define AMPPI_POOL_STRIDED 1  // filtered compaction: one thread per filtered slot (0: per-thread cell chunks)
+#endif
 #ifndef AMPPI_LOG_BITS
 #define AMPPI_LOG_BITS 1  // fused pass A logs (cell, index, range bits); 0: (cell, index), pass B re-keys
 #endif
@@ -401,6 +404,50 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   const uint32_t n_pts = sm.total;
   double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
   double* __restrict__ filt = P.filtered + cell_base * 3;
+#if AMPPI_POOL_STRIDED
+  // Compaction map first (filtered slot -> point index and cell, in the dead
+  // range table once pool_coarse has read it), then one thread per filtered
+  // slot: the point gathers are independent across a warp and the filtered
+  // records are written coalesced.
+  {
+    uint32_t* comp_k = reinterpret_cast<uint32_t*>(sm.rng);           // [<= 7200]
+    uint16_t* comp_f = reinterpret_cast<uint16_t*>(comp_k + kCells);  // [<= 7200]
+    __syncthreads();  // pool_coarse has read sm.rng
+    uint32_t pos = pos0;
+    for (int f = f0; f < f1; ++f) {
+      const uint32_t k = sm.idx[f];
+      if (k == 0xFFFFFFFFu) continue;
+      comp_k[pos] = k;
+      comp_f[pos] = static_cast<uint16_t>(f);
+      ++pos;
+    }
+    __syncthreads();
+    if (P.nearest)
+      for (int f = tid; f < kCells; f += blockDim.x)
+        if (sm.idx[f] == 0xFFFFFFFFu) {
+          P.nearest[(cell_base + f) * 3] = 0.0;
+          P.nearest[(cell_base + f) * 3 + 1] = 0.0;
+          P.nearest[(cell_base + f) * 3 + 2] = 0.0;
+        }
+#pragma unroll 4
+    for (uint32_t q = tid; q < n_pts; q += blockDim.x) {
+      const uint32_t k = comp_k[q];
+      const V3<double> pb = to_body(sm.pose, load_point(in, pt_base + k));
+      const V3<double> pw = sm.pose.p + mat_vec(sm.pose.r, pb);
+      if (P.nearest) {
+        const int f = comp_f[q];
+        P.nearest[(cell_base + f) * 3] = pb.x;
+        P.nearest[(cell_base + f) * 3 + 1] = pb.y;
+        P.nearest[(cell_base + f) * 3 + 2] = pb.z;
+      }
+      filt[3 * q] = pw.x;
+      filt[3 * q + 1] = pw.y;
+      filt[3 * q + 2] = pw.z;
+      lo[0] = fmin(lo[0], pw.x); lo[1] = fmin(lo[1], pw.y); lo[2] = fmin(lo[2], pw.z);
+      hi[0] = fmax(hi[0], pw.x); hi[1] = fmax(hi[1], pw.y); hi[2] = fmax(hi[2], pw.z);
+    }
+  }
+#else
   uint32_t pos = pos0;
 #pragma unroll 5
   for (int f = f0; f < f1; ++f) {
@@ -427,6 +474,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     hi[0] = fmax(hi[0], pw.x); hi[1] = fmax(hi[1], pw.y); hi[2] = fmax(hi[2], pw.z);
     ++pos;
   }
+#endif
   const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
