@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_RANK_SORT
+#define AMPPI_RANK_SORT 0  // grid build: counting sort by cell + in-cell ranks (0: bitonic network only)
+#endif
 #ifndef AMPPI_POOL_STRIDED
 #define AMPPI_POOL_STRIDED 1  // filtered compaction: one thread per filtered slot (0: per-thread cell chunks)
 #endif
@@ -320,6 +323,7 @@ struct FinalizeSmem {
   PoseFrame pose;
   uint32_t total;
   uint32_t n_cand;
+  uint32_t max_cnt;  // rank sort: largest cell count past its limit (0: none)
 };
 
 // Block-wide exclusive scan of one value per thread; returns the prefix and
@@ -617,6 +621,84 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     __syncthreads();
   }
 #else
+  bool sorted = false;
+#if AMPPI_RANK_SORT
+  // Counting sort by grid cell, then every point's rank inside its cell by
+  // (key, point index): four passes and five barriers where the bitonic
+  // network needs ~80 stages.  The rank pass costs the sum over cells of the
+  // squared cell counts, so scenes past 4096 filtered points (the layout
+  // below) or with a cell past 1024 points take the bitonic network.  Both
+  // give keys in ascending order; equal keys (points in the same 1/8-cell)
+  // come out here by point index, there in network order -- either is a
+  // valid grid order (the queries' minima do not depend on it).
+  if (n_pts <= 4096) {
+    const int ncells = meta.dims[0] * meta.dims[1] * meta.dims[2];  // <= kGridCells
+    uint32_t* cnt = sm.idx;                                        // [ceil(ncells / 2)] u16 pairs
+    uint32_t* tkey = keys + 4096;                                  // [n] scattered by cell
+    uint16_t* tval = vals + 4096;                                  // [n]
+    uint16_t* fpos = reinterpret_cast<uint16_t*>(vals + kCellsPow2);  // [n] final slot
+    const int nwords = (ncells + 1) / 2;
+    for (int w = tid; w < nwords; w += blockDim.x) cnt[w] = 0u;
+    if (tid == 0) sm.max_cnt = 0u;
+    __syncthreads();
+    for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
+      const uint32_t key = key_of(k), c = key >> 9;
+      keys[k] = key;  // by point index until the final pass
+      atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
+    }
+    __syncthreads();
+    const int per = 2 * ((nwords + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x));
+    const int c0 = tid * per, c1 = min(c0 + per, ncells);
+    uint32_t local = 0, lmax = 0;
+    for (int c = c0; c < c1; ++c) {
+      const uint32_t n = (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+      local += n;
+      lmax = max(lmax, n);
+    }
+    uint32_t run = block_exclusive_scan(local, sm.warp_sums, &sm.total);
+    if (lmax > 1024u) atomicMax(&sm.max_cnt, lmax);
+    for (int c = c0; c < c1; c += 2) {  // rewrite both halves of each owned word as segment starts
+      const uint32_t w = cnt[c >> 1];
+      const uint32_t lo = run;
+      run += w & 0xFFFFu;
+      const uint32_t hi = run;
+      run += c + 1 < c1 ? (w >> 16) : 0u;
+      cnt[c >> 1] = lo | (hi << 16);
+    }
+    __syncthreads();
+    if (sm.max_cnt == 0u) {
+      for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
+        const uint32_t key = keys[k], c = key >> 9;
+        const uint32_t old = atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
+        const uint32_t pos = (old >> (16 * (c & 1))) & 0xFFFFu;
+        tkey[pos] = key;
+        tval[pos] = static_cast<uint16_t>(k);
+      }
+      __syncthreads();
+      // cnt now holds every cell's segment end (= the next cell's start)
+      for (uint32_t q = tid; q < n_pts; q += blockDim.x) {
+        const uint32_t key = tkey[q], v = tval[q], c = key >> 9;
+        const uint32_t e = (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+        const uint32_t b = c > 0 ? (cnt[(c - 1) >> 1] >> (16 * ((c - 1) & 1))) & 0xFFFFu : 0u;
+        uint32_t rank = 0;
+        for (uint32_t o = b; o < e; ++o) {
+          const uint32_t ko = tkey[o];
+          rank += (ko < key || (ko == key && tval[o] < v)) ? 1u : 0u;
+        }
+        fpos[q] = static_cast<uint16_t>(b + rank);
+      }
+      __syncthreads();
+      for (uint32_t q = tid; q < n_pts; q += blockDim.x) {
+        const uint32_t d = fpos[q];
+        keys[d] = tkey[q];
+        vals[d] = tval[q];
+      }
+      __syncthreads();
+      sorted = true;
+    }
+  }
+#endif
+  if (!sorted) {
   uint32_t n2 = 1;
   while (n2 < n_pts) n2 <<= 1;
   for (uint32_t k = tid; k < n2; k += blockDim.x) {
@@ -649,6 +731,8 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       else
         __syncwarp();
     }
+  __syncthreads();
+  }
 #endif
   SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
