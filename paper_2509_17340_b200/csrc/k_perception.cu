@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_SORT_ASCENDING
+#define AMPPI_SORT_ASCENDING 1  // all-ascending bitonic network that skips the padding (0: classic network over n2)
+#endif
 #ifndef AMPPI_RANK_SORT
 #define AMPPI_RANK_SORT 0  // grid build: counting sort by cell + in-cell ranks (0: bitonic network only)
 #endif
@@ -701,6 +704,53 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   if (!sorted) {
   uint32_t n2 = 1;
   while (n2 < n_pts) n2 <<= 1;
+#if AMPPI_SORT_ASCENDING
+  // Bitonic network in its all-ascending form (each merge starts with a
+  // flip stage, i against the mirror of i in its block, then half-cleaners;
+  // every compare-exchange puts the smaller key at the lower index).  The
+  // +inf padding past n_pts is larger than every key, so it only ever moves
+  // up and never leaves [n_pts, n2): every pair reaching past n_pts is a
+  // no-op and is skipped -- the work follows n_pts, not the padded n2
+  // (C5 scenes hold 700-2800 filtered points, padded to 1024-4096).
+  for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
+    keys[k] = key_of(k);
+    vals[k] = static_cast<uint16_t>(k);
+  }
+  __syncthreads();
+  auto cx = [&](uint32_t i, uint32_t j) {
+    if (j < n_pts) {
+      const uint32_t ki = keys[i], kj = keys[j];
+      if (ki > kj) {
+        keys[i] = kj;
+        keys[j] = ki;
+        const uint16_t v = vals[i];
+        vals[i] = vals[j];
+        vals[j] = v;
+      }
+    }
+  };
+  for (uint32_t size = 2; size <= n2; size <<= 1) {
+    const uint32_t half = size >> 1;
+    const uint32_t tf = min(n2 >> 1, (n_pts + size) >> 1);
+    for (uint32_t t = tid; t < tf; t += blockDim.x) {  // flip: i <-> mirror in its block
+      const uint32_t o = t & (half - 1);
+      const uint32_t i = 2 * t - o;
+      cx(i, i + size - 1 - 2 * o);
+    }
+    if (size > 64) __syncthreads(); else __syncwarp();
+    for (uint32_t stride = half >> 1; stride > 0; stride >>= 1) {
+      const uint32_t th = min(n2 >> 1, (n_pts + stride) >> 1);
+      for (uint32_t t = tid; t < th; t += blockDim.x) {
+        const uint32_t i = 2 * t - (t & (stride - 1));
+        cx(i, i + stride);
+      }
+      const uint32_t next = stride > 1 ? stride >> 1 : size;  // the next stage's reach (stride, or flip of 2*size)
+      if (stride > 32 || next > 32) __syncthreads(); else __syncwarp();
+    }
+  }
+  __syncthreads();
+  }
+#else
   for (uint32_t k = tid; k < n2; k += blockDim.x) {
     keys[k] = k < n_pts ? key_of(k) : 0xFFFFFFFFu;
     vals[k] = static_cast<uint16_t>(k);
@@ -733,6 +783,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
   __syncthreads();
   }
+#endif
 #endif
   SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
