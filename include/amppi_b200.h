@@ -96,7 +96,7 @@ typedef struct {
   int32_t pipeline_chunks;   /* amppi_cycle_batch: host-upload pipeline chunks (auto: up to 6) */
   double pipeline_ratio;     /* growth ratio of successive pipeline chunks (auto: 1.2; >= 1) */
   int32_t pipeline_streams;  /* compute streams chunks rotate over, 2..4 (auto: 3) */
-  int32_t device_chunks;     /* amppi_cycle_batch_device: concurrent chunks (auto: up to 3) */
+  int32_t device_chunks;     /* amppi_cycle_batch_device: concurrent chunks (auto: up to 2) */
   int32_t chunk_gather;      /* host pipeline: gather each chunk's results as it finishes (auto/1) or once (-1) */
   int32_t loop_graph;        /* closed loop: replay one captured cycle as a CUDA graph (auto/1) or launch (-1) */
   int32_t plan_graph;        /* amppi_plan: replay the plan kernels as a cached CUDA graph (auto/1) or launch (-1) */

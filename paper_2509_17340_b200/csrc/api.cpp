@@ -1333,12 +1333,12 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in, amppi_
 // context's compute streams; results stay in the plan arrays.
 static int plan_device_batch(amppi_ctx* ctx, const BatchIn& bin, int64_t max_scene) {
   const int S = bin.S;
-  // Device-resident inputs need no upload pipeline, but a few chunks on the
+  // Device-resident inputs need no upload pipeline, but two chunks on the
   // compute streams still overlap one chunk's latency-bound tail kernels with
-  // the others' work (C5: 3 chunks 18.9 ms, 2 chunks 19.0, 1 chunk 19.3,
-  // 4 chunks 20.9).
+  // the other's work (C5, r02 kernels: 1 chunk 17.03 ms, 2 chunks 16.54,
+  // 3 chunks 16.71, 4 chunks 19.37, 6 chunks 19.0; gpurun_out/r44_*.log).
   int chunks = std::min(pipeline_streams(ctx), S / (2 * 148));
-  chunks = std::max(1, std::min(chunks, 3));
+  chunks = std::max(1, std::min(chunks, 2));
   if (ctx->opt.schedule.device_chunks > 0) chunks = std::max(1, std::min(kMaxChunks, ctx->opt.schedule.device_chunks));
   if (chunks > 1 && S / chunks < 148) chunks = 1;
   // scenes past kFusedMaxPoints take the many-CTA snapshot (shared candidate
