@@ -27,7 +27,7 @@ using namespace amppi_dev;
 namespace {
 
 constexpr double kPi = std::numbers::pi;
-constexpr int kMaxChunks = 8;  // chunks of a pipelined batch (one work-list counter each)
+constexpr int kMaxChunks = 8;  // chunks of a pipelined batch (one work-list counter block each)
 constexpr int kExtraStreams = 2;  // compute streams beyond stream / stream2
 
 struct Arena {
@@ -481,7 +481,7 @@ int create_impl(amppi_ctx* ctx) {
     pl.col_terms = static_cast<double*>(p);
     CK(A.alloc(&p, jobs * N * sizeof(uint32_t)));
     pl.col_work = static_cast<uint32_t*>(p);
-    CK(A.alloc(&p, kMaxChunks * sizeof(unsigned int)));
+    CK(A.alloc(&p, kMaxChunks * kColCountStride * sizeof(unsigned int)));
     pl.col_count = static_cast<unsigned int*>(p);
   }
   CK(A.alloc(&p, static_cast<size_t>(S) * sizeof(int32_t)));
@@ -620,7 +620,7 @@ int run_chunk(amppi_ctx* ctx, const BatchIn& in, int64_t max_pts_scene, int64_t 
   pl.tsum += 4 * sm0;
   pl.col_terms += 4 * sm0 * dc.N;
   pl.col_work += 4 * sm0 * dc.N;
-  pl.col_count += chunk;
+  pl.col_count += chunk * kColCountStride;
   pl.pos_cap = std::min<int64_t>(4 * smc, ctx->pl.pos_cap);
   cudaError_t e = launch_snapshot(in, P, dc, max_pts_scene, st, &ctx->timer);
   if (e != cudaSuccess) return ctx->cuda_fail(e, "launch_snapshot");

@@ -1178,6 +1178,80 @@ __global__ void __launch_bounds__(256) k_col_classify(Perception P, Plan pl, Dev
 #endif
 constexpr int kColGroup = AMPPI_COL_GROUP;
 
+// Bucketed work list (AMPPI_COL_BUCKETS): a query's cost grows with the
+// number of non-empty cells around it, and a warp of the query pass runs as
+// long as its slowest lane, so the list is ordered by that count (most cells
+// first): lanes of a warp get queries of similar cost.  Two passes over the
+// queries: k_col_count histograms the counts (term 0 for empty
+// neighbourhoods, as k_col_classify), k_col_place writes each listed query
+// into its bucket's range.  counters: [0] list length, [1 + b] bucket count,
+// [32 + b] bucket fill, for b = 27 - popcount(mask) in 0..26.
+#ifndef AMPPI_COL_BUCKETS
+#define AMPPI_COL_BUCKETS 1
+#endif
+constexpr int kColBucketSlots = 64;
+
+__device__ __forceinline__ int col_bucket(const Perception& P, const Plan& pl, const ColJobs& J, const DevConfig& cfg,
+                                          int64_t i, bool* valid) {
+  const int64_t w = i / cfg.N;
+  int64_t smi;
+  *valid = col_traj(J, pl, w, &smi);
+  if (!*valid) return -1;
+  const int s = static_cast<int>(smi / cfg.M);
+  const GridMeta g = P.grid[s];
+  if (g.dims[0] == 0) return -1;
+  const double* q = pl.pos64 + 4 * i;
+  const int cx = static_cast<int>(floor((q[0] - g.origin[0]) * g.inv_h));
+  const int cy = static_cast<int>(floor((q[1] - g.origin[1]) * g.inv_h));
+  const int cz = static_cast<int>(floor((q[2] - g.origin[2]) * g.inv_h));
+  const uint32_t m = nbr_mask(g, P.grid_nbr + static_cast<int64_t>(s) * kPadCells, cx, cy, cz);
+  return m ? 27 - __popc(m) : -1;
+}
+
+__global__ void __launch_bounds__(256) k_col_count(Perception P, Plan pl, DevConfig cfg, ColJobs J, int64_t q,
+                                                   unsigned int* __restrict__ counters) {
+  __shared__ unsigned int h[27];
+  if (threadIdx.x < 27) h[threadIdx.x] = 0u;
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < q) {
+    bool valid;
+    const int b = col_bucket(P, pl, J, cfg, i, &valid);
+    if (b >= 0) atomicAdd(&h[b], 1u);
+    else if (valid) pl.col_terms[i] = 0.0;  // no point within d_max: collision_term(+inf) = 0
+  }
+  __syncthreads();
+  if (threadIdx.x < 27 && h[threadIdx.x]) atomicAdd(&counters[1 + threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_col_place(Perception P, Plan pl, DevConfig cfg, ColJobs J, int64_t q,
+                                                   uint32_t* __restrict__ work, unsigned int* __restrict__ counters) {
+  __shared__ unsigned int h[27], base[27], start[27];
+  if (threadIdx.x < 27) h[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) {  // bucket starts: exclusive prefix of the counts
+    unsigned int run = 0;
+    for (int b = 0; b < 27; ++b) {
+      start[b] = run;
+      run += counters[1 + b];
+    }
+    if (blockIdx.x == 0) counters[0] = run;
+  }
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int b = -1;
+  unsigned int r = 0;
+  if (i < q) {
+    bool valid;
+    b = col_bucket(P, pl, J, cfg, i, &valid);
+    if (b >= 0) r = atomicAdd(&h[b], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 27 && h[threadIdx.x])
+    base[threadIdx.x] = start[threadIdx.x] + atomicAdd(&counters[32 + threadIdx.x], h[threadIdx.x]);
+  __syncthreads();
+  if (b >= 0) work[base[b] + r] = static_cast<uint32_t>(i);
+}
+
 __global__ void __launch_bounds__(128) k_col_query(Perception P, Plan pl, DevConfig cfg, ColJobs J,
                                                    const uint32_t* __restrict__ work,
                                                    const unsigned int* __restrict__ count) {
@@ -1266,10 +1340,15 @@ __global__ void __launch_bounds__(128) k_stage2_col_sum(BatchIn in, Plan pl, Dev
 // classify + query passes for `jobs` (an upper bound of the) trajectories
 void launch_col_queries(const Perception& P, const Plan& pl, const DevConfig& cfg, const ColJobs& J, int64_t jobs,
                         cudaStream_t st) {
-  cudaMemsetAsync(pl.col_count, 0, sizeof(unsigned int), st);
+  cudaMemsetAsync(pl.col_count, 0, (AMPPI_COL_BUCKETS ? kColBucketSlots : 1) * sizeof(unsigned int), st);
   const int64_t q = jobs * cfg.N;
   if (q == 0) return;
+#if AMPPI_COL_BUCKETS
+  k_col_count<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st>>>(P, pl, cfg, J, q, pl.col_count);
+  k_col_place<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st>>>(P, pl, cfg, J, q, pl.col_work, pl.col_count);
+#else
   k_col_classify<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
+#endif
   const int64_t b = std::min<int64_t>((q * kColGroup + 127) / 128, static_cast<int64_t>(device_sms()) * 16);
   k_col_query<<<static_cast<unsigned>(b), 128, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
 }

@@ -138,6 +138,8 @@ struct TrajSums {
 // rollout (k_stage1_warp32).
 constexpr int kLatencyRollouts = 148 * 128;
 
+constexpr int kColCountStride = 64;  // unsigned ints per chunk in Plan::col_count
+
 struct Plan {
   // anchors / guides (FP64)
   double* anchor_init;         // [S*M*3]
@@ -167,7 +169,7 @@ struct Plan {
   int64_t pos_cap;             // support pairs the split refine handles (pos64/tsum hold max(4*S*M, kLatencyRollouts))
   double* col_terms;           // [pos_cap*N] per-step collision terms of the deferred trajectories
   uint32_t* col_work;          // [pos_cap*N] (trajectory*N + step) queries with a point within d_max
-  unsigned int* col_count;     // work-list length (one counter per concurrent chunk)
+  unsigned int* col_count;     // work-list counters ([kColCountStride] per concurrent chunk: length, bucket counts)
   // per scene
   int32_t* done;               // [S] arrival counter (self-resetting)
   int32_t* winner;             // [S]
