@@ -715,6 +715,13 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
           // by the previous step's nearest point block: samples near the same
           // obstacle patch share a warp and walk the same leaves
           bkt = env.hint == kNoHint ? 0 : 1 + static_cast<int>((env.hint >> 2) % 63u);
+#elif AMPPI_REPACK_KEY == 2
+          // by the number of non-empty cells around the sample (most first):
+          // lanes of a warp then run collision queries of similar cost
+          const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
+          const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);
+          const int cz = __float2int_rd((x.p.z - env.grid.origin_f[2]) * env.grid.inv_h_f);
+          bkt = 27 - __popc(nbr_mask(env.grid, env.gnbr, cx, cy, cz));
 #else
           const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
           const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);

@@ -1185,11 +1185,14 @@ constexpr int kColGroup = AMPPI_COL_GROUP;
 // queries: k_col_count histograms the counts (term 0 for empty
 // neighbourhoods, as k_col_classify), k_col_place writes each listed query
 // into its bucket's range.  counters: [0] list length, [1 + b] bucket count,
-// [32 + b] bucket fill, for b = 27 - popcount(mask) in 0..26.
+// [65 + b] bucket fill, for b = 27 - popcount(mask) in 0..26 (or, with
+// AMPPI_COL_BUCKETS=2, 63 - (points in those cells) / 16 in 0..63).
 #ifndef AMPPI_COL_BUCKETS
 #define AMPPI_COL_BUCKETS 1
 #endif
-constexpr int kColBucketSlots = 64;
+constexpr int kColBuckets = AMPPI_COL_BUCKETS == 2 ? 64 : 27;
+constexpr int kColBucketSlots = 2 * 64 + 1;  // [0] length, [1 + b] counts, [65 + b] fills
+static_assert(kColBucketSlots <= kColCountStride, "Plan::col_count stride");
 
 __device__ __forceinline__ int col_bucket(const Perception& P, const Plan& pl, const ColJobs& J, const DevConfig& cfg,
                                           int64_t i, bool* valid) {
@@ -1205,13 +1208,28 @@ __device__ __forceinline__ int col_bucket(const Perception& P, const Plan& pl, c
   const int cy = static_cast<int>(floor((q[1] - g.origin[1]) * g.inv_h));
   const int cz = static_cast<int>(floor((q[2] - g.origin[2]) * g.inv_h));
   const uint32_t m = nbr_mask(g, P.grid_nbr + static_cast<int64_t>(s) * kPadCells, cx, cy, cz);
+#if AMPPI_COL_BUCKETS == 2
+  // finer: the points in the non-empty cells around the query, 16 per bucket
+  if (!m) return -1;
+  const uint4* rec = P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2;
+  const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
+  const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
+  uint32_t pts = 0, mm = m;
+  while (mm) {
+    const int b = __ffs(mm) - 1;
+    mm &= mm - 1;
+    pts += rec[2 * (cbase + nbr_offset(b, d12, d2))].x >> 16;
+  }
+  return kColBuckets - 1 - static_cast<int>(min(pts >> 4, static_cast<uint32_t>(kColBuckets - 1)));
+#else
   return m ? 27 - __popc(m) : -1;
+#endif
 }
 
 __global__ void __launch_bounds__(256) k_col_count(Perception P, Plan pl, DevConfig cfg, ColJobs J, int64_t q,
                                                    unsigned int* __restrict__ counters) {
-  __shared__ unsigned int h[27];
-  if (threadIdx.x < 27) h[threadIdx.x] = 0u;
+  __shared__ unsigned int h[kColBuckets];
+  if (threadIdx.x < kColBuckets) h[threadIdx.x] = 0u;
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < q) {
@@ -1221,16 +1239,16 @@ __global__ void __launch_bounds__(256) k_col_count(Perception P, Plan pl, DevCon
     else if (valid) pl.col_terms[i] = 0.0;  // no point within d_max: collision_term(+inf) = 0
   }
   __syncthreads();
-  if (threadIdx.x < 27 && h[threadIdx.x]) atomicAdd(&counters[1 + threadIdx.x], h[threadIdx.x]);
+  if (threadIdx.x < kColBuckets && h[threadIdx.x]) atomicAdd(&counters[1 + threadIdx.x], h[threadIdx.x]);
 }
 
 __global__ void __launch_bounds__(256) k_col_place(Perception P, Plan pl, DevConfig cfg, ColJobs J, int64_t q,
                                                    uint32_t* __restrict__ work, unsigned int* __restrict__ counters) {
-  __shared__ unsigned int h[27], base[27], start[27];
-  if (threadIdx.x < 27) h[threadIdx.x] = 0u;
+  __shared__ unsigned int h[kColBuckets], base[kColBuckets], start[kColBuckets];
+  if (threadIdx.x < kColBuckets) h[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {  // bucket starts: exclusive prefix of the counts
     unsigned int run = 0;
-    for (int b = 0; b < 27; ++b) {
+    for (int b = 0; b < kColBuckets; ++b) {
       start[b] = run;
       run += counters[1 + b];
     }
@@ -1246,8 +1264,8 @@ __global__ void __launch_bounds__(256) k_col_place(Perception P, Plan pl, DevCon
     if (b >= 0) r = atomicAdd(&h[b], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 27 && h[threadIdx.x])
-    base[threadIdx.x] = start[threadIdx.x] + atomicAdd(&counters[32 + threadIdx.x], h[threadIdx.x]);
+  if (threadIdx.x < kColBuckets && h[threadIdx.x])
+    base[threadIdx.x] = start[threadIdx.x] + atomicAdd(&counters[65 + threadIdx.x], h[threadIdx.x]);
   __syncthreads();
   if (b >= 0) work[base[b] + r] = static_cast<uint32_t>(i);
 }

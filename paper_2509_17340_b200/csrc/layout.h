@@ -138,7 +138,7 @@ struct TrajSums {
 // rollout (k_stage1_warp32).
 constexpr int kLatencyRollouts = 148 * 128;
 
-constexpr int kColCountStride = 64;  // unsigned ints per chunk in Plan::col_count
+constexpr int kColCountStride = 160;  // unsigned ints per chunk in Plan::col_count
 
 struct Plan {
   // anchors / guides (FP64)
