@@ -54,7 +54,7 @@ BYTES_PER_POINT = 12  # FP32 xyz read once by the keying pass
 # ncu --set full of the FP32 screening kernels (bound + main pass) on the C5
 # batch as one chunk: DRAM read+write per step and the main pass's issue-slot
 # use (profiles/r02_c5_full.md)
-TRAFFIC_BYTES_PER_LAUNCH = 197.4e6
+TRAFFIC_BYTES_PER_LAUNCH = 193.7e6
 TRAFFIC_SOURCE = "profiles/r02_c5_full.md"
 ISSUE_ACTIVE_FRAC = 0.7225
 # FP32 flops the two screening kernels executed in one C5 launch, counted by ncu on the SASS page
@@ -178,6 +178,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # sampling is live before the timed region starts
+            while not self.lines and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
@@ -188,7 +191,11 @@ class ClockSampler:
     def stop(self) -> dict:
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        # one more sample after the timed region, so a region shorter than the
+        # 200 ms sampling period is still bracketed by samples
+        n0, t0 = len(self.lines), time.time()
+        while len(self.lines) <= n0 and time.time() - t0 < 1.0:
+            time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -343,7 +350,8 @@ def fp32_peak(device: int) -> float:
     return peak.value
 
 
-def screening_roofline(ktimes, rollout_steps_per_launch: float, peak: float, total_ms: float) -> dict:
+def screening_roofline(ktimes, rollout_steps_per_launch: float, peak: float, total_ms: float,
+                       executed_flops: float | None = None) -> dict:
     k_ms, k_n = ktimes.get("k_stage1_f32", (float("nan"), 1))
     b_ms = ktimes.get("k_stage1_f32_bound", (0.0, 1))[0]
     per_launch_flops = FLOPS_PER_STEP * rollout_steps_per_launch
@@ -359,11 +367,13 @@ def screening_roofline(ktimes, rollout_steps_per_launch: float, peak: float, tot
             "algorithmic_flops_per_launch": per_launch_flops,
             "achieved_note": "effective rate: 440 flop x every rollout-step of the launch, including the steps the "
                              "abort bound proves outside the softmin support and never integrates",
-            "executed_flops_per_launch": EXECUTED_FLOPS_PER_LAUNCH,
-            "executed_tflops": EXECUTED_FLOPS_PER_LAUNCH / (screen_ms / 1e3) / 1e12,
-            "executed_frac": EXECUTED_FLOPS_PER_LAUNCH / (screen_ms / 1e3) / 1e12 / peak,
-            "executed_note": "FP32 flops the screening kernels executed (ncu SASS counts, collision-query distance "
-                             "arithmetic included, " + TRAFFIC_SOURCE + ") over this run's kernel time",
+            **({} if executed_flops is None else {
+                "executed_flops_per_launch": executed_flops,
+                "executed_tflops": executed_flops / (screen_ms / 1e3) / 1e12,
+                "executed_frac": executed_flops / (screen_ms / 1e3) / 1e12 / peak,
+                "executed_note": "FP32 flops the screening kernels executed in one C5 launch (ncu SASS counts, "
+                                 "collision-query distance arithmetic included, " + TRAFFIC_SOURCE
+                                 + ") over this run's kernel time"}),
             "kernel_ms_per_launch": screen_ms, "kernel_share_of_step": (k_ms + b_ms) / total_ms,
             "issue_active_frac": ISSUE_ACTIVE_FRAC,
             "issue_source": "smsp__issue_active.avg.pct_of_peak_sustained_active of the main pass, ncu --set full, "
@@ -446,7 +456,8 @@ def run_c5(args, D: Dist):
     ktimes = planner.kernel_times()
     planner.set_schedule(device_chunks=args.device_chunks)
     roof = screening_roofline(ktimes, rollout_steps(cfg, S) / cfg.mppi.iterations, fp32_peak(device),
-                              sum(v[0] for v in ktimes.values()))
+                              sum(v[0] for v in ktimes.values()),
+                              executed_flops=EXECUTED_FLOPS_PER_LAUNCH * S / 4096)  # profiled on 4096 scenes
 
     e2e = None
     if not args.no_e2e:
