@@ -345,13 +345,14 @@ __device__ __forceinline__ int screen_post(St<float>& x, CostSums<float>& s, con
 
 template <typename Pert>
 __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, float (&up)[4], int j,
-                                           const RolloutEnv<float>& env, const Pert& pert) {
+                                           const RolloutEnv<float>& env, const Pert& pert, float* last_d2 = nullptr) {
   StepCtl c;
   if (screen_pre(x, s, up, j, env, pert, c)) return 1;
   // step 0 is x0 for every sample: its query was answered once per CTA
   const float d2 = j == 0 ? env.d2_x0
                           : nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2,
                                             c.stop2, &env.hint);
+  if (last_d2) *last_d2 = d2;
   return screen_post(x, s, c, d2, env);
 }
 
@@ -647,6 +648,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     env.d2_x0 = s_d2;
     env.hint = s_hint;
   }
+#if AMPPI_REPACK_KEY == 3
+  float last_d2 = env.d2_x0;
+#endif
   int round = 0;
   for (int j0 = 0; j0 < N; j0 += kCompact, ++round) {
     const int j1 = min(j0 + kCompact, N);
@@ -676,7 +680,11 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
 #else
     if (live) {
       for (int j = j0; j < j1; ++j) {
+#if AMPPI_REPACK_KEY == 3
+        const int st = screen_step(x, cs, up, j, env, pr, &last_d2);
+#else
         const int st = screen_step(x, cs, up, j, env, pr);
+#endif
         if (st) {
           out[k] = st == 1 ? 3.4028234663852886e38f : __int_as_float(0x7f800000);
           live = false;
@@ -715,6 +723,16 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
           // by the previous step's nearest point block: samples near the same
           // obstacle patch share a warp and walk the same leaves
           bkt = env.hint == kNoHint ? 0 : 1 + static_cast<int>((env.hint >> 2) % 63u);
+#elif AMPPI_REPACK_KEY == 3
+          // samples whose last query found a point within reach first (their
+          // next queries are likely hits, the expensive kind), each half by
+          // grid cell
+          const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
+          const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);
+          const int cz = __float2int_rd((x.p.z - env.grid.origin_f[2]) * env.grid.inv_h_f);
+          bkt = (last_d2 < env.reach2 ? 0 : 32) +
+                static_cast<int>((static_cast<uint32_t>(cx) * 73856093u ^ static_cast<uint32_t>(cy) * 19349663u ^
+                                  static_cast<uint32_t>(cz) * 83492791u) >> 27);
 #elif AMPPI_REPACK_KEY == 2
           // by the number of non-empty cells around the sample (most first):
           // lanes of a warp then run collision queries of similar cost
