@@ -11,6 +11,7 @@
 // "Precision").
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -524,6 +525,11 @@ constexpr int kMainGroups = AMPPI_MAIN_GROUPS;
 #define AMPPI_BOUND_SAMPLES 32
 #endif
 constexpr int kBoundSamples = AMPPI_BOUND_SAMPLES;  // 32, 16, 8 or 4
+#ifndef AMPPI_BOUND_LARGE
+#define AMPPI_BOUND_LARGE 1024
+#endif
+constexpr int kBoundLarge = AMPPI_BOUND_LARGE;  // bound-sample cap when K >= 2048 (K / 8 below it)
+static_assert(kBoundLarge % 32 == 0, "whole warps of bound samples");
 static_assert(32 % kBoundSamples == 0, "bound samples divide a warp");
 constexpr int kMainCompact = AMPPI_MAIN_COMPACT;
 // Bound pass as a cascade: samples [0, 8) in full (4 instances per warp),
@@ -1107,7 +1113,14 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
   unom32();
   // bound samples per instance: AMPPI_BOUND_SAMPLES of every instance, 32 / that
   // instances per warp (injected perturbations: 32, one instance per warp)
-  const int k1 = in.injected ? 32 : kBoundSamples;
+  // Large ensembles (K >= 2048 samples on this context) take an eighth of
+  // their samples, up to AMPPI_BOUND_LARGE, as bound samples: with 8192
+  // samples per instance a 32-sample minimum is a weak bound, and the bound
+  // pass is a small share of the screening (C4 64 x 8192 x 50: 32 bound
+  // samples 1.95 ms per cycle, 256: 1.84, 1024: 1.80; gpurun_out/r49, r50)
+  const int k1 = in.injected ? 32
+                             : (kr >= 2048 && kBoundSamples == 32 ? std::min(kBoundLarge, (kr / 8) & ~31)
+                                                                   : kBoundSamples);
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
     if (AMPPI_BOUND_CASCADE && !in.injected && kBoundSamples == 32) {
@@ -1116,7 +1129,7 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
       k_stage1_f32c<32, kMainCompact, 32><<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter,
                                                                                    kCascadeFirst, 32, kCascadeFirst);
     } else if (in.injected || kBoundSamples == 32) {
-      kern<<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
+      kern<<<static_cast<unsigned>(SM * (k1 / 32)), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
     } else {
       constexpr int G = 32 / kBoundSamples;
       k_stage1_bound<G><<<static_cast<unsigned>((SM + G - 1) / G), 32, 0, st>>>(in, P, pl, cfg, sc, iter);
