@@ -527,6 +527,7 @@ __device__ __forceinline__ float block_min_d2(const float4* __restrict__ pts, ui
   return fminf(fminf(a.x, a.y), fminf(b.x, b.y));
 }
 
+template <bool kPrescreen = (AMPPI_F32_BOX && AMPPI_F32_PRESCREEN)>
 __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint4* __restrict__ rec,
                                                    const uint32_t* __restrict__ nbr, const uint4* __restrict__ leaves,
                                                    const double* __restrict__ pts, const float4* __restrict__ pts32,
@@ -603,7 +604,8 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
         const uint4 la = lf[0], lb = lf[1];
         if (leaf_far(la, lb)) continue;
         const uint32_t te = min(t + kLeafSize, k1);
-#if AMPPI_F32_BOX && AMPPI_F32_PRESCREEN
+#if AMPPI_F32_BOX
+        if constexpr (kPrescreen) {
         // FP32 prescreen: the leaf's 4-point float blocks (the screening's,
         // same local frame) in packed FP32x2; a point's FP32 squared distance
         // is off from the true one by no more than a box's, so FP64 is
@@ -625,6 +627,16 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
               cut = cut_of(best);
             }
           }
+        }
+        } else {
+        for (uint32_t k = t; k < te; ++k) {
+          const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
+          if (dd < best) {
+            best = dd;
+            bi = k;
+            cut = cut_of(best);
+          }
+        }
         }
 #else
         for (uint32_t k = t; k < te; ++k) {

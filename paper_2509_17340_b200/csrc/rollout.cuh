@@ -13,6 +13,10 @@
 
 namespace amppi_dev {
 
+#ifndef AMPPI_ENV_PRESCREEN
+#define AMPPI_ENV_PRESCREEN (AMPPI_F32_BOX && AMPPI_F32_PRESCREEN)
+#endif
+
 template <typename R>
 struct CostSums {
   R trk, vn, mag, rate, goal, col;
@@ -51,7 +55,9 @@ struct RolloutEnv<double> {
   __device__ __forceinline__ double unom_at(int j, int c) const { return unom[4 * j + c]; }
   __device__ __forceinline__ double attitude(Q4<double> q) const { return attitude_err_exact(q, gt); }
   __device__ __forceinline__ double collision(V3<double> p) const {
-    const double d2 = nearest_sq_exact(grid, grec, gnbr, gleaf, gpts, gpts32, p, cdmax * cdmax, cdmin * cdmin, &hint);
+    // (the latency kernels' lane-per-step queries: AMPPI_ENV_PRESCREEN)
+    const double d2 =
+        nearest_sq_exact<AMPPI_ENV_PRESCREEN>(grid, grec, gnbr, gleaf, gpts, gpts32, p, cdmax * cdmax, cdmin * cdmin, &hint);
     return collision_term(sqrt(d2), cs, ca, cdmin, cdmax);
   }
 };
