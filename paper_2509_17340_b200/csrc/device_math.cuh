@@ -661,77 +661,6 @@ __device__ __forceinline__ double nearest_sq_exact(const GridMeta& g, const uint
   return best;
 }
 
-// nearest_sq_exact for a group of L consecutive lanes answering one query
-// together (the deferred FP64 collision queries, k_col_query): every lane of
-// the group walks the same cells and leaves (group-uniform box tests, so the
-// group never diverges), lane r of the group takes blocks r, r + L, ... of
-// each leaf (a leaf spans up to 5 four-point blocks), prescreens its points
-// in FP32 against the group's cut as nearest_sq_exact does and evaluates FP64
-// for the candidates; after each leaf the group min-reduces best.  Same
-// minimum as nearest_sq_exact (the group evaluates the same candidate set or
-// a superset of it).  Needs the FP32 blocks and AMPPI_F32_BOX.
-template <int L>
-__device__ __forceinline__ double nearest_sq_exact_group(const GridMeta& g, const uint4* __restrict__ rec,
-                                                         const uint32_t* __restrict__ nbr,
-                                                         const uint4* __restrict__ leaves,
-                                                         const double* __restrict__ pts,
-                                                         const float4* __restrict__ pts32, V3<double> p, double lim2,
-                                                         double stop2, unsigned gmask, int r) {
-  double best = __longlong_as_double(0x7ff0000000000000ll);
-  if (g.dims[0] == 0) return best;
-  const int cx = static_cast<int>(floor((p.x - g.origin[0]) * g.inv_h));
-  const int cy = static_cast<int>(floor((p.y - g.origin[1]) * g.inv_h));
-  const int cz = static_cast<int>(floor((p.z - g.origin[2]) * g.inv_h));
-  const uint32_t m = nbr_mask(g, nbr, cx, cy, cz);
-  if (!m) return best;
-  const int d2 = g.dims[2], d12 = g.dims[1] * g.dims[2];
-  const int cbase = ((cx - 1) * g.dims[1] + (cy - 1)) * d2 + (cz - 1);
-  const V3<float> pf{static_cast<float>(p.x - g.org[0]), static_cast<float>(p.y - g.org[1]),
-                     static_cast<float>(p.z - g.org[2])};  // to_local_f
-  const float e_ax = 0x1.0p-23f * (fmaxf(fmaxf(fabsf(pf.x), fabsf(pf.y)), fabsf(pf.z)) + 2.0f * g.h_f + 1.0f);
-  const float slack = 3.5f * e_ax * __double2float_ru(sqrt(lim2)) + 4.0f * e_ax * e_ax;
-  auto cut_of = [&](double b) { return __double2float_ru(fmin(b, lim2)) * (1.0f + 1e-6f) + slack; };
-  float cut = cut_of(best);
-  for (int phase = 0; phase < 3; ++phase) {
-    uint32_t mm = nbr_phase(m, phase);
-    while (mm) {
-      const int b = __ffs(mm) - 1;
-      mm &= mm - 1;
-      const int c = cbase + nbr_offset(b, d12, d2);
-      const uint4 ra = rec[2 * c], rb = rec[2 * c + 1];
-      if (box_gap_sq(ra.z, ra.w, rb.x, rb.y, rb.z, rb.w, pf) > cut) continue;
-      const uint32_t k0 = ra.x & 0xFFFFu, k1 = k0 + (ra.x >> 16);
-      const uint4* lf = leaves + 2 * ra.y;
-      for (uint32_t t = k0; t < k1; t += kLeafSize, lf += 2) {
-        const uint4 la = lf[0], lb = lf[1];
-        if (box_gap_sq(la.x, la.y, la.z, la.w, lb.x, lb.y, pf) > cut) continue;
-        const uint32_t te = min(t + kLeafSize, k1);
-        double mine = best;
-        for (uint32_t u = t / kPointBlock + r; u <= (te - 1) / kPointBlock; u += L) {
-          float2 a01, a23;
-          block_d2(pts32 + 3 * u, pf, a01, a23);
-          const float dq[4] = {a01.x, a01.y, a23.x, a23.y};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (!(dq[i] <= cut)) continue;
-            const uint32_t k = u * kPointBlock + i;
-            const double dd = sqnorm(p - V3<double>{pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]});
-            mine = fmin(mine, dd);
-          }
-        }
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) mine = fmin(mine, __shfl_xor_sync(gmask, mine, o, L));
-        if (mine < best) {
-          best = mine;
-          cut = cut_of(best);
-        }
-        if (best < stop2) return best;
-      }
-    }
-  }
-  return best;
-}
-
 // FP32 screening query: as nearest_sq_exact, plus a second branch-and-bound
 // level over each scanned cell's 16-point leaves (float leaf boxes).  Points
 // are stored in blocks of 4 (kPointBlock, struct-of-arrays x4 / y4 / z4,

@@ -290,12 +290,6 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
-#ifndef AMPPI_SORT_ASCENDING
-#define AMPPI_SORT_ASCENDING 1  // all-ascending bitonic network that skips the padding (0: classic network over n2)
-#endif
-#ifndef AMPPI_RANK_SORT
-#define AMPPI_RANK_SORT 0  // grid build: counting sort by cell + in-cell ranks (0: bitonic network only)
-#endif
 #ifndef AMPPI_POOL_STRIDED
 #define AMPPI_POOL_STRIDED 1  // filtered compaction: one thread per filtered slot (0: per-thread cell chunks)
 #endif
@@ -307,12 +301,6 @@ constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 #endif
 #ifndef AMPPI_LOCAL_FRAME
 #define AMPPI_LOCAL_FRAME 1  // FP32 grid data and screening relative to the snapshot pose (0: world frame)
-#endif
-#ifndef AMPPI_KEY_PREFILTER
-#define AMPPI_KEY_PREFILTER 0  // FP32 prefilter of the fused snapshot's keying pass
-#endif
-#ifndef AMPPI_CELL_SORT
-#define AMPPI_CELL_SORT 0  // 1: counting sort by cell + per-cell insertion sort (measured 37x slower: dense cells); 0: block bitonic sort
 #endif
 
 struct FinalizeSmem {
@@ -326,7 +314,6 @@ struct FinalizeSmem {
   PoseFrame pose;
   uint32_t total;
   uint32_t n_cand;
-  uint32_t max_cnt;  // rank sort: largest cell count past its limit (0: none)
 };
 
 // Block-wide exclusive scan of one value per thread; returns the prefix and
@@ -565,146 +552,8 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       mort = (mort << 3) | (((s3[0] >> bit) & 1) << 2) | (((s3[1] >> bit) & 1) << 1) | ((s3[2] >> bit) & 1);
     return (static_cast<uint32_t>(c) << 9) | mort;
   };
-#if AMPPI_CELL_SORT
-  // Counting sort by grid cell: 16-bit per-cell counters packed in pairs in
-  // the (dead) idx table, a block scan to segment offsets, a scatter, then
-  // every cell's segment ordered by (Morton code, point index) by one thread
-  // -- four barrier phases instead of a bitonic network's ~80.
-  {
-    const int ncells = meta.dims[0] * meta.dims[1] * meta.dims[2];  // <= kGridCells
-    uint32_t* cnt = sm.idx;                                        // [ceil(ncells / 2)] u16 pairs
-    const int nwords = (ncells + 1) / 2;
-    for (int w = tid; w < nwords; w += blockDim.x) cnt[w] = 0u;
-    __syncthreads();
-    for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
-      const uint32_t c = key_of(k) >> 9;
-      atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
-    }
-    __syncthreads();
-    // exclusive scan of the counts; each thread owns whole words
-    const int per = 2 * ((nwords + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x));
-    const int c0 = tid * per, c1 = min(c0 + per, ncells);
-    uint32_t local = 0;
-    for (int c = c0; c < c1; ++c) local += (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-    uint32_t run = block_exclusive_scan(local, sm.warp_sums, &sm.total);
-    for (int c = c0; c < c1; c += 2) {  // rewrite both halves of each owned word as offsets
-      const uint32_t w = cnt[c >> 1];
-      const uint32_t lo = run;
-      run += w & 0xFFFFu;
-      const uint32_t hi = run;
-      run += c + 1 < c1 ? (w >> 16) : 0u;
-      cnt[c >> 1] = lo | (hi << 16);
-    }
-    __syncthreads();
-    for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
-      const uint32_t key = key_of(k), c = key >> 9;
-      const uint32_t old = atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
-      const uint32_t pos = (old >> (16 * (c & 1))) & 0xFFFFu;
-      keys[pos] = key;
-      vals[pos] = static_cast<uint16_t>(k);
-    }
-    __syncthreads();
-    // cnt now holds every cell's segment end
-    for (int c = tid; c < ncells; c += blockDim.x) {
-      const uint32_t e = (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-      const uint32_t b = c > 0 ? (cnt[(c - 1) >> 1] >> (16 * ((c - 1) & 1))) & 0xFFFFu : 0u;
-      for (uint32_t i = b + 1; i < e; ++i) {  // insertion sort by (key, point index)
-        const uint32_t kk = keys[i];
-        const uint16_t vv = vals[i];
-        uint32_t j = i;
-        while (j > b && (keys[j - 1] > kk || (keys[j - 1] == kk && vals[j - 1] > vv))) {
-          keys[j] = keys[j - 1];
-          vals[j] = vals[j - 1];
-          --j;
-        }
-        keys[j] = kk;
-        vals[j] = vv;
-      }
-    }
-    __syncthreads();
-  }
-#else
-  bool sorted = false;
-#if AMPPI_RANK_SORT
-  // Counting sort by grid cell, then every point's rank inside its cell by
-  // (key, point index): four passes and five barriers where the bitonic
-  // network needs ~80 stages.  The rank pass costs the sum over cells of the
-  // squared cell counts, so scenes past 4096 filtered points (the layout
-  // below) or with a cell past 1024 points take the bitonic network.  Both
-  // give keys in ascending order; equal keys (points in the same 1/8-cell)
-  // come out here by point index, there in network order -- either is a
-  // valid grid order (the queries' minima do not depend on it).
-  if (n_pts <= 4096) {
-    const int ncells = meta.dims[0] * meta.dims[1] * meta.dims[2];  // <= kGridCells
-    uint32_t* cnt = sm.idx;                                        // [ceil(ncells / 2)] u16 pairs
-    uint32_t* tkey = keys + 4096;                                  // [n] scattered by cell
-    uint16_t* tval = vals + 4096;                                  // [n]
-    uint16_t* fpos = reinterpret_cast<uint16_t*>(vals + kCellsPow2);  // [n] final slot
-    const int nwords = (ncells + 1) / 2;
-    for (int w = tid; w < nwords; w += blockDim.x) cnt[w] = 0u;
-    if (tid == 0) sm.max_cnt = 0u;
-    __syncthreads();
-    for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
-      const uint32_t key = key_of(k), c = key >> 9;
-      keys[k] = key;  // by point index until the final pass
-      atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
-    }
-    __syncthreads();
-    const int per = 2 * ((nwords + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x));
-    const int c0 = tid * per, c1 = min(c0 + per, ncells);
-    uint32_t local = 0, lmax = 0;
-    for (int c = c0; c < c1; ++c) {
-      const uint32_t n = (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-      local += n;
-      lmax = max(lmax, n);
-    }
-    uint32_t run = block_exclusive_scan(local, sm.warp_sums, &sm.total);
-    if (lmax > 1024u) atomicMax(&sm.max_cnt, lmax);
-    for (int c = c0; c < c1; c += 2) {  // rewrite both halves of each owned word as segment starts
-      const uint32_t w = cnt[c >> 1];
-      const uint32_t lo = run;
-      run += w & 0xFFFFu;
-      const uint32_t hi = run;
-      run += c + 1 < c1 ? (w >> 16) : 0u;
-      cnt[c >> 1] = lo | (hi << 16);
-    }
-    __syncthreads();
-    if (sm.max_cnt == 0u) {
-      for (uint32_t k = tid; k < n_pts; k += blockDim.x) {
-        const uint32_t key = keys[k], c = key >> 9;
-        const uint32_t old = atomicAdd(&cnt[c >> 1], 1u << (16 * (c & 1)));
-        const uint32_t pos = (old >> (16 * (c & 1))) & 0xFFFFu;
-        tkey[pos] = key;
-        tval[pos] = static_cast<uint16_t>(k);
-      }
-      __syncthreads();
-      // cnt now holds every cell's segment end (= the next cell's start)
-      for (uint32_t q = tid; q < n_pts; q += blockDim.x) {
-        const uint32_t key = tkey[q], v = tval[q], c = key >> 9;
-        const uint32_t e = (cnt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-        const uint32_t b = c > 0 ? (cnt[(c - 1) >> 1] >> (16 * ((c - 1) & 1))) & 0xFFFFu : 0u;
-        uint32_t rank = 0;
-        for (uint32_t o = b; o < e; ++o) {
-          const uint32_t ko = tkey[o];
-          rank += (ko < key || (ko == key && tval[o] < v)) ? 1u : 0u;
-        }
-        fpos[q] = static_cast<uint16_t>(b + rank);
-      }
-      __syncthreads();
-      for (uint32_t q = tid; q < n_pts; q += blockDim.x) {
-        const uint32_t d = fpos[q];
-        keys[d] = tkey[q];
-        vals[d] = tval[q];
-      }
-      __syncthreads();
-      sorted = true;
-    }
-  }
-#endif
-  if (!sorted) {
   uint32_t n2 = 1;
   while (n2 < n_pts) n2 <<= 1;
-#if AMPPI_SORT_ASCENDING
   // Bitonic network in its all-ascending form (each merge starts with a
   // flip stage, i against the mirror of i in its block, then half-cleaners;
   // every compare-exchange puts the smaller key at the lower index).  The
@@ -749,42 +598,6 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
   }
   __syncthreads();
-  }
-#else
-  for (uint32_t k = tid; k < n2; k += blockDim.x) {
-    keys[k] = k < n_pts ? key_of(k) : 0xFFFFFFFFu;
-    vals[k] = static_cast<uint16_t>(k);
-  }
-  __syncthreads();
-  // Stages with stride <= 32 keep every warp inside its own 64-key windows
-  // (pair t -> keys 2t - t % stride, + stride; warp w owns keys [64w, 64w+64)
-  // of each 32-pair block), so consecutive such stages need only a warp
-  // barrier; a block barrier is needed when a stage reaches across windows.
-  for (uint32_t size = 2; size <= n2; size <<= 1)
-    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t t = tid; t < (n2 >> 1); t += blockDim.x) {
-        const uint32_t i = 2 * t - (t & (stride - 1));
-        const uint32_t j = i + stride;
-        const bool up = (i & size) == 0;
-        const uint32_t ki = keys[i], kj = keys[j];
-        if ((ki > kj) == up) {
-          keys[i] = kj;
-          keys[j] = ki;
-          const uint16_t v = vals[i];
-          vals[i] = vals[j];
-          vals[j] = v;
-        }
-      }
-      const uint32_t next = stride > 1 ? stride >> 1 : size;  // the next stage's stride
-      if (stride > 32 || next > 32)
-        __syncthreads();
-      else
-        __syncwarp();
-    }
-  __syncthreads();
-  }
-#endif
-#endif
   SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
   // leaves of kLeafSize consecutive (Morton-ordered) points
@@ -1032,30 +845,8 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
     }
   };
   if (!in.xyz64) fetch(b);
-#if AMPPI_KEY_PREFILTER
-  // FP32 pose for the prefilter (float input only): a point whose FP32 range
-  // (error < 1e-4 m for coordinates below 1e3 m) is clearly past r_max, below
-  // the minimum range, or clearly above its cell's running minimum cannot be
-  // a cell minimum and skips the exact FP64 keying and the 64-bit atomic; its
-  // cell comes from the FP32 fast key, taken only where that key is exact
-  // (horizontal and total range >= 1 m, outside the guard band)
-  float fr[9], fp[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    fp[i] = static_cast<float>(i == 0 ? pose.p.x : (i == 1 ? pose.p.y : pose.p.z));
-#pragma unroll
-    for (int j = 0; j < 3; ++j) fr[3 * i + j] = static_cast<float>(pose.r.m[i][j]);
-  }
-  const bool prefilter = !in.xyz64 && fabsf(fp[0]) < 1e3f && fabsf(fp[1]) < 1e3f && fabsf(fp[2]) < 1e3f;
-  const float rmax_f = static_cast<float>(r_max);
-#endif
   for (int64_t g0 = b; g0 < e; g0 += kUnroll * blockDim.x) {
     V3<double> w[kUnroll];
-#if AMPPI_KEY_PREFILTER
-    V3<float> wf[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) wf[u] = nxt[u];
-#endif
     if (in.xyz64) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -1074,32 +865,6 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
       uint64_t bits = 0;
       bool cand = false;
       bool skip = g >= e;
-#if AMPPI_KEY_PREFILTER
-      if (!skip && prefilter) {
-        const float dx = wf[u].x - fp[0], dy = wf[u].y - fp[1], dz = wf[u].z - fp[2];
-        if (fabsf(wf[u].x) < 1e3f && fabsf(wf[u].y) < 1e3f && fabsf(wf[u].z) < 1e3f) {
-          // R^T (w - p), the body frame (perception.cpp:58-61)
-          const float bx = (fr[0] * dx + fr[3] * dy) + fr[6] * dz;
-          const float by = (fr[1] * dx + fr[4] * dy) + fr[7] * dz;
-          const float bz = (fr[2] * dx + fr[5] * dy) + fr[8] * dz;
-          const float rho = sqrtf(bx * bx + by * by);
-          const float rf = sqrtf(rho * rho + bz * bz);
-          if (rf > rmax_f + 1e-3f || rf < static_cast<float>(kMinPointRange) - 1e-3f) {
-            skip = true;
-          } else if (rho >= 1.0f) {
-            constexpr float kInvStepF = static_cast<float>(1.0 / 0x1.acee9f37bebd5p-5);
-            int i = fast_cell(by, bx, 3.14159265358979f, kInvStepF);
-            const int j = fast_cell(bz, rho, 1.57079632679490f, kInvStepF);
-            if (i >= 0 && j >= 0) {
-              if (i >= kAz) i -= kAz;
-              const int fc = min(max(i, 0), kAz - 1) * kEl + min(max(j, 0), kEl - 1);
-              const double cur = __longlong_as_double(static_cast<long long>(cell_bits[fc]));  // may be stale: larger
-              skip = static_cast<double>(rf) - 1e-3 > cur;
-            }
-          }
-        }
-      }
-#endif
       if (!skip && key_point(pose, w[u], r_max, f, bits)) cand = atomicMin(cell_bits + f, bits) >= bits;
       const unsigned want = __ballot_sync(0xffffffffu, cand);
       if (want) {

@@ -357,146 +357,6 @@ __device__ __forceinline__ int screen_step(St<float>& x, CostSums<float>& s, flo
   return screen_post(x, s, c, d2, env);
 }
 
-// ---------------------------------------------------------------------------
-// Warp-shared neighbourhood (main pass): the lanes of a warp step in lockstep
-// and, after the cell-ordered repack, sit close together.  Per step the warp
-// gathers, once, every filtered point within query reach of the bounding box
-// of its live lanes' positions into a shared-memory list (the grid cells
-// overlapping the box, their point blocks read with coalesced 16-byte loads
-// by all 32 lanes), and every live lane scans that list with packed FP32x2
-// arithmetic -- the same distances, in the same sq3f shape, as the per-lane
-// branch-and-bound query, so the result is the same exact minimum (with the
-// same early stop below stop2) and every screening cost is unchanged.  No
-// data-dependent per-lane tree walk: the scan is warp-uniform.  A list past
-// kListCap points falls back to the per-lane query for that step.
-#ifndef AMPPI_WARP_LIST
-#define AMPPI_WARP_LIST 0
-#endif
-#ifndef AMPPI_LIST_CAP
-#define AMPPI_LIST_CAP 256
-#endif
-constexpr int kListCap = AMPPI_LIST_CAP;
-constexpr int kListStride = kListCap + 2;  // (+ one +inf pad for an odd count)
-
-// float -> int with the same order (for the integer warp reductions)
-__device__ __forceinline__ int ford(float f) {
-  const int b = __float_as_int(f);
-  return b >= 0 ? b : b ^ 0x7FFFFFFF;
-}
-__device__ __forceinline__ float iford(int b) { return __int_as_float(b >= 0 ? b : b ^ 0x7FFFFFFF); }
-
-// Returns false when the neighbourhood overflows the list (every lane then
-// answers its own query); else d2 holds each live lane's squared clearance.
-__device__ __forceinline__ bool warp_list_query(const RolloutEnv<float>& env, bool live, V3<float> p, float stop2,
-                                                float* __restrict__ lx, float* __restrict__ ly,
-                                                float* __restrict__ lz, float& d2) {
-  constexpr unsigned kFull = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const float kInf = __int_as_float(0x7f800000);
-  d2 = kInf;
-  const GridMeta& g = env.grid;
-  if (g.dims[0] == 0) return true;  // no points: every query returns +inf
-  // bounding box of the live lanes' positions
-  const int blx = __reduce_min_sync(kFull, live ? ford(p.x) : 0x7FFFFFFF);
-  const int bly = __reduce_min_sync(kFull, live ? ford(p.y) : 0x7FFFFFFF);
-  const int blz = __reduce_min_sync(kFull, live ? ford(p.z) : 0x7FFFFFFF);
-  const int bhx = __reduce_max_sync(kFull, live ? ford(p.x) : static_cast<int>(0x80000000));
-  const int bhy = __reduce_max_sync(kFull, live ? ford(p.y) : static_cast<int>(0x80000000));
-  const int bhz = __reduce_max_sync(kFull, live ? ford(p.z) : static_cast<int>(0x80000000));
-  const float lox = iford(blx), loy = iford(bly), loz = iford(blz);
-  const float hix = iford(bhx), hiy = iford(bhy), hiz = iford(bhz);
-  // a point belongs to the list when its squared gap to the box is below the
-  // query reach (with a relative margin far above FP32 rounding: extra points
-  // never change a minimum)
-  const float lim2m = env.reach2 * 1.0001f;
-  const float reach = sqrt_approx(lim2m) * 1.001f + 1e-3f * g.h_f;
-  auto cell_lo = [&](float v, int a) {
-    return max(0, __float2int_rd((v - reach - g.origin_f[a]) * g.inv_h_f));
-  };
-  auto cell_hi = [&](float v, int a) {
-    return min(g.dims[a] - 1, __float2int_rd((v + reach - g.origin_f[a]) * g.inv_h_f));
-  };
-  const int cx0 = cell_lo(lox, 0), cx1 = cell_hi(hix, 0);
-  const int cy0 = cell_lo(loy, 1), cy1 = cell_hi(hiy, 1);
-  const int cz0 = cell_lo(loz, 2), cz1 = cell_hi(hiz, 2);
-  if (cx0 > cx1 || cy0 > cy1 || cz0 > cz1) return true;  // the region misses the grid
-  const int ny = cy1 - cy0 + 1, nz = cz1 - cz0 + 1;
-  const int ncells = (cx1 - cx0 + 1) * ny * nz;
-  const int p1 = g.dims[1] + 2, p2 = g.dims[2] + 2;
-  int n = 0;  // warp-uniform list length
-  for (int c0 = 0; c0 < ncells; c0 += 32) {
-    const int c = c0 + lane;
-    bool occ = false;
-    int cell = 0;
-    if (c < ncells) {
-      const int cz = cz0 + c % nz, cy = cy0 + (c / nz) % ny, cx = cx0 + c / (nz * ny);
-      occ = (__ldg(env.gnbr + ((cx + 1) * p1 + (cy + 1)) * p2 + (cz + 1)) & kNbrCenter) != 0u;
-      cell = (cx * g.dims[1] + cy) * g.dims[2] + cz;
-    }
-    unsigned m = __ballot_sync(kFull, occ);
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const int cc = __shfl_sync(kFull, cell, src);
-      const uint32_t r0 = __ldg(&env.grec[2 * cc].x);
-      const uint32_t k0 = r0 & 0xFFFFu, k1 = k0 + (r0 >> 16);
-      const uint32_t bmax = (k1 - 1) / kPointBlock;
-      for (uint32_t b0 = k0 / kPointBlock; b0 <= bmax; b0 += 32) {
-        const uint32_t b = b0 + lane;
-        float4 X = make_float4(0.f, 0.f, 0.f, 0.f), Y = X, Z = X;
-        if (b <= bmax) {
-          X = __ldg(env.gpts + 3 * b);
-          Y = __ldg(env.gpts + 3 * b + 1);
-          Z = __ldg(env.gpts + 3 * b + 2);
-        }
-        const float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w}, zs[4] = {Z.x, Z.y, Z.z, Z.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const uint32_t idx = kPointBlock * b + t;
-          bool in = b <= bmax && idx >= k0 && idx < k1;
-          if (in) {
-            const float gx = fmaxf(fmaxf(lox - xs[t], xs[t] - hix), 0.f);
-            const float gy = fmaxf(fmaxf(loy - ys[t], ys[t] - hiy), 0.f);
-            const float gz = fmaxf(fmaxf(loz - zs[t], zs[t] - hiz), 0.f);
-            in = sq3f(gx, gy, gz) < lim2m;
-          }
-          const unsigned bal = __ballot_sync(kFull, in);
-          const int pos = n + __popc(bal & ((1u << lane) - 1u));
-          if (in && pos < kListCap) {
-            lx[pos] = xs[t];
-            ly[pos] = ys[t];
-            lz[pos] = zs[t];
-          }
-          n += __popc(bal);
-        }
-      }
-    }
-  }
-  AMPPI_STAT(75, lane == 0 ? 1 : 0);
-  AMPPI_STAT(76, lane == 0 ? n : 0);
-  if (n > kListCap) {
-    AMPPI_STAT(77, lane == 0 ? 1 : 0);
-    __syncwarp();
-    return false;
-  }
-  if (lane == 0 && (n & 1)) lx[n] = ly[n] = lz[n] = kInf;  // pad to whole pairs
-  __syncwarp();
-  if (live) {
-    const float2 npx = make_float2(-p.x, -p.x), npy = make_float2(-p.y, -p.y), npz = make_float2(-p.z, -p.z);
-    float best = kInf;
-    for (int i = 0; i < n; i += 2) {
-      const float2 dx = __fadd2_rn(*reinterpret_cast<const float2*>(lx + i), npx);
-      const float2 dy = __fadd2_rn(*reinterpret_cast<const float2*>(ly + i), npy);
-      const float2 dz = __fadd2_rn(*reinterpret_cast<const float2*>(lz + i), npz);
-      const float2 dd = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-      best = fminf(best, fminf(dd.x, dd.y));
-      if (best < stop2) break;
-    }
-    d2 = best;
-  }
-  __syncwarp();  // the list is rewritten by the next step's gather
-  return true;
-}
 
 // Main screening pass with lane compaction: samples [k1, K) of one instance
 // per CTA, stepped in lockstep; every kCompact steps the live samples (not
@@ -514,9 +374,6 @@ constexpr int kScreenThreads = 128;
 #define AMPPI_MAIN_COMPACT 10
 #endif
 constexpr int kMainThreads = AMPPI_MAIN_THREADS, kMainMinBlocks = AMPPI_MAIN_MINBLOCKS;
-#ifndef AMPPI_REPACK_KEY
-#define AMPPI_REPACK_KEY 0  // 0: grid-cell hash of the position, 1: nearest point block of the last query
-#endif
 #ifndef AMPPI_MAIN_GROUPS
 #define AMPPI_MAIN_GROUPS 1
 #endif
@@ -532,15 +389,6 @@ constexpr int kBoundLarge = AMPPI_BOUND_LARGE;  // bound-sample cap when K >= 20
 static_assert(kBoundLarge % 32 == 0, "whole warps of bound samples");
 static_assert(32 % kBoundSamples == 0, "bound samples divide a warp");
 constexpr int kMainCompact = AMPPI_MAIN_COMPACT;
-// Bound pass as a cascade: samples [0, 8) in full (4 instances per warp),
-// then samples [8, 32) aborted against those 8 (one warp per instance).  The
-// 32-sample minimum U the main pass aborts against is unchanged: a cascade
-// sample stops only once its partial cost passes U8 + window >= U8, so its
-// final cost could not have lowered the minimum.
-#ifndef AMPPI_BOUND_CASCADE
-#define AMPPI_BOUND_CASCADE 0
-#endif
-constexpr int kCascadeFirst = 8;
 constexpr int kStateWords = 22;  // p(3) q(4) v(3) trk vn mag rate goal col up(4) hint amb
 
 // Samples [k_lo + kb0, k_lo + kend) of every instance, aborted against the
@@ -558,9 +406,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   __shared__ int s_k[kT];
   __shared__ int s_wcount[2][kT / 32];
   __shared__ uint32_t s_bcnt[64], s_boff[64];  // cell-order buckets of the repack
-#if AMPPI_WARP_LIST
-  __shared__ __align__(16) float s_list[kT / 32][3][kListStride];  // per-warp neighbourhood lists (x | y | z)
-#endif
   if (threadIdx.x < 64) s_bcnt[threadIdx.x] = 0u;
   const int k_n = kend - kb0;
   const int tiles = (k_n + kT - 1) / kT;
@@ -654,43 +499,12 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     env.d2_x0 = s_d2;
     env.hint = s_hint;
   }
-#if AMPPI_REPACK_KEY == 3
-  float last_d2 = env.d2_x0;
-#endif
   int round = 0;
   for (int j0 = 0; j0 < N; j0 += kCompact, ++round) {
     const int j1 = min(j0 + kCompact, N);
-#if AMPPI_WARP_LIST
-    // warp-synchronous steps: every lane runs the loop (dead lanes idle) so
-    // the warp can gather one neighbourhood list per step for its live lanes
-    float* wl = &s_list[warp][0][0];
-    for (int j = j0; j < j1; ++j) {
-      if (!__any_sync(0xffffffffu, live)) break;
-      StepCtl c;
-      if (live && screen_pre(x, cs, up, j, env, pr, c)) {
-        out[k] = 3.4028234663852886e38f;
-        live = false;
-      }
-      float d2 = env.d2_x0;  // step 0 is x0 for every sample: answered once per CTA
-      if (j > 0 && !warp_list_query(env, live, x.p, c.stop2, wl, wl + kListStride, wl + 2 * kListStride, d2) &&
-          live)
-        d2 = nearest_sq_fast(env.grid, env.grec, env.gnbr, env.gleaf, env.gpts, x.p, env.reach2, c.stop2, &env.hint);
-      if (live) {
-        const int st = screen_post(x, cs, c, d2, env);
-        if (st) {
-          out[k] = st == 1 ? 3.4028234663852886e38f : __int_as_float(0x7f800000);
-          live = false;
-        }
-      }
-    }
-#else
     if (live) {
       for (int j = j0; j < j1; ++j) {
-#if AMPPI_REPACK_KEY == 3
-        const int st = screen_step(x, cs, up, j, env, pr, &last_d2);
-#else
         const int st = screen_step(x, cs, up, j, env, pr);
-#endif
         if (st) {
           out[k] = st == 1 ? 3.4028234663852886e38f : __int_as_float(0x7f800000);
           live = false;
@@ -698,7 +512,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         }
       }
     }
-#endif
     if (j1 >= N) break;
     const unsigned bal = __ballot_sync(0xffffffffu, live);
     int* wc = s_wcount[round & 1];
@@ -725,34 +538,11 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         int bkt = 0;
         uint32_t rank = 0;
         if (live) {
-#if AMPPI_REPACK_KEY == 1
-          // by the previous step's nearest point block: samples near the same
-          // obstacle patch share a warp and walk the same leaves
-          bkt = env.hint == kNoHint ? 0 : 1 + static_cast<int>((env.hint >> 2) % 63u);
-#elif AMPPI_REPACK_KEY == 3
-          // samples whose last query found a point within reach first (their
-          // next queries are likely hits, the expensive kind), each half by
-          // grid cell
-          const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
-          const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);
-          const int cz = __float2int_rd((x.p.z - env.grid.origin_f[2]) * env.grid.inv_h_f);
-          bkt = (last_d2 < env.reach2 ? 0 : 32) +
-                static_cast<int>((static_cast<uint32_t>(cx) * 73856093u ^ static_cast<uint32_t>(cy) * 19349663u ^
-                                  static_cast<uint32_t>(cz) * 83492791u) >> 27);
-#elif AMPPI_REPACK_KEY == 2
-          // by the number of non-empty cells around the sample (most first):
-          // lanes of a warp then run collision queries of similar cost
-          const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
-          const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);
-          const int cz = __float2int_rd((x.p.z - env.grid.origin_f[2]) * env.grid.inv_h_f);
-          bkt = 27 - __popc(nbr_mask(env.grid, env.gnbr, cx, cy, cz));
-#else
           const int cx = __float2int_rd((x.p.x - env.grid.origin_f[0]) * env.grid.inv_h_f);
           const int cy = __float2int_rd((x.p.y - env.grid.origin_f[1]) * env.grid.inv_h_f);
           const int cz = __float2int_rd((x.p.z - env.grid.origin_f[2]) * env.grid.inv_h_f);
           bkt = static_cast<int>((static_cast<uint32_t>(cx) * 73856093u ^ static_cast<uint32_t>(cy) * 19349663u ^
                                   static_cast<uint32_t>(cz) * 83492791u) >> 26);
-#endif
           rank = atomicAdd(&s_bcnt[bkt], 1u);
         }
         __syncthreads();
@@ -1123,12 +913,7 @@ cudaError_t launch_stage1_f32(const BatchIn& in, const Perception& P, const Plan
                                                                    : kBoundSamples);
   {
     TimedRegion t(timer, "k_stage1_f32_bound", st);
-    if (AMPPI_BOUND_CASCADE && !in.injected && kBoundSamples == 32) {
-      constexpr int G = 32 / kCascadeFirst;
-      k_stage1_bound<G><<<static_cast<unsigned>((SM + G - 1) / G), 32, 0, st>>>(in, P, pl, cfg, sc, iter);
-      k_stage1_f32c<32, kMainCompact, 32><<<static_cast<unsigned>(SM), 32, 0, st>>>(in, P, pl, cfg, sc, iter,
-                                                                                   kCascadeFirst, 32, kCascadeFirst);
-    } else if (in.injected || kBoundSamples == 32) {
+    if (in.injected || kBoundSamples == 32) {
       kern<<<static_cast<unsigned>(SM * (k1 / 32)), 32, 0, st>>>(in, P, pl, cfg, sc, iter, 1, k1);
     } else {
       constexpr int G = 32 / kBoundSamples;

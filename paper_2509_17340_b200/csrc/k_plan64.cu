@@ -1173,11 +1173,6 @@ __global__ void __launch_bounds__(256) k_col_classify(Perception P, Plan pl, Dev
     pl.col_terms[i] = 0.0;  // no point within d_max: collision_term(+inf) = 0
 }
 
-#ifndef AMPPI_COL_GROUP
-#define AMPPI_COL_GROUP 1  // lanes per deferred FP64 query (1: one thread per query)
-#endif
-constexpr int kColGroup = AMPPI_COL_GROUP;
-
 // Bucketed work list (AMPPI_COL_BUCKETS): a query's cost grows with the
 // number of non-empty cells around it, and a warp of the query pass runs as
 // long as its slowest lane, so the list is ordered by that count (most cells
@@ -1274,28 +1269,6 @@ __global__ void __launch_bounds__(128) k_col_query(Perception P, Plan pl, DevCon
                                                    const uint32_t* __restrict__ work,
                                                    const unsigned int* __restrict__ count) {
   const unsigned int n = *count;
-  if constexpr (kColGroup > 1) {
-    // L lanes per query (nearest_sq_exact_group): the whole group iterates
-    // together, so the grid-stride loop is group-uniform
-    const int r = threadIdx.x % kColGroup;
-    const unsigned gmask = ((1u << kColGroup) - 1u) << ((threadIdx.x & 31) & ~(kColGroup - 1));
-    const unsigned int groups = gridDim.x * blockDim.x / kColGroup;
-    for (unsigned int q = (blockIdx.x * blockDim.x + threadIdx.x) / kColGroup; q < n; q += groups) {
-      const uint32_t i = work[q];
-      const int64_t w = i / cfg.N;
-      const int64_t smi = J.pairs ? static_cast<int64_t>(J.pairs[w].x) : w;
-      const int s = static_cast<int>(smi / cfg.M);
-      const double* pp = pl.pos64 + 4 * static_cast<int64_t>(i);
-      const double d2 = nearest_sq_exact_group<kColGroup>(
-          P.grid[s], P.grid_rec + static_cast<int64_t>(s) * kGridCells * 2,
-          P.grid_nbr + static_cast<int64_t>(s) * kPadCells, P.grid_leaf + static_cast<int64_t>(s) * kCells * 2,
-          P.grid_pts64 + static_cast<int64_t>(s) * kCells * 3, P.grid_pts32 + static_cast<int64_t>(s) * kCells,
-          V3<double>{pp[0], pp[1], pp[2]}, cfg.col_d_max * cfg.col_d_max, cfg.col_d_min * cfg.col_d_min, gmask, r);
-      if (r == 0)
-        pl.col_terms[i] = collision_term(sqrt(d2), cfg.col_scale, cfg.col_slope, cfg.col_d_min, cfg.col_d_max);
-    }
-    return;
-  }
   for (unsigned int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     const uint32_t i = work[q];
     const int64_t w = i / cfg.N;
@@ -1367,7 +1340,7 @@ void launch_col_queries(const Perception& P, const Plan& pl, const DevConfig& cf
 #else
   k_col_classify<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
 #endif
-  const int64_t b = std::min<int64_t>((q * kColGroup + 127) / 128, static_cast<int64_t>(device_sms()) * 16);
+  const int64_t b = std::min<int64_t>((q + 127) / 128, static_cast<int64_t>(device_sms()) * 16);
   k_col_query<<<static_cast<unsigned>(b), 128, 0, st>>>(P, pl, cfg, J, pl.col_work, pl.col_count);
 }
 

@@ -29,8 +29,7 @@ for kind in (1, 2, 3):
         "hit_queries": st[5] / q, "scanned_miss_queries": st[6] / q,
         "points_per_hit_query": (st[4] - st[7]) / max(st[5], 1), "points_per_miss_query": st[7] / max(st[6], 1),
         "d_max_band_steps_per_query": st[72] / q,
-        "warp_list_gathers": st[75], "warp_list_mean_points": st[76] / max(st[75], 1),
-        "warp_list_overflow_frac": st[77] / max(st[75], 1), "main_pass_flagged_of_completed": st[73] / max(st[74], 1),
+        "main_pass_flagged_of_completed": st[73] / max(st[74], 1),
         "main_pass_live_fraction_by_step": [round(st[8 + j] / max(st[8], 1), 3) for j in range(cfg.mppi.horizon)]}
     p.close()
 print(json.dumps(out, indent=1))
