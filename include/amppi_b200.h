@@ -244,8 +244,9 @@ int amppi_cycle_batch_device(amppi_ctx* ctx, const amppi_batch_input* in_device,
 
 /* Streaming form of amppi_cycle_batch: submit queues one batch (uploads on the
  * copy engine, planning on the compute streams) and returns a ticket; wait
- * returns that batch's results.  Two batches may be in flight, so the next
- * batch's upload overlaps the current batch's planning.  The caller's xyz
+ * returns that batch's results.  Up to three batches may be in flight, so the
+ * next batch's upload overlaps the current batch's planning and is queued
+ * before the previous batch is collected.  The caller's xyz
  * buffer (pinned memory for an asynchronous copy) must stay valid until the
  * batch is waited for; the per-scene arrays are copied at submit.  Tickets
  * are waited for in submit order. */

@@ -174,8 +174,9 @@ struct amppi_ctx {
   unsigned char* d_gather{nullptr};
   unsigned char* h_gather{nullptr};  // pinned mirror of d_gather (per-chunk result copies)
   std::vector<cudaEvent_t> chunk_done;
-  // streaming batches (amppi_cycle_batch_submit / _wait): two input slots, so
-  // batch t+1's upload overlaps batch t's planning
+  // streaming batches (amppi_cycle_batch_submit / _wait): three input slots,
+  // so batch t+1's upload overlaps batch t's planning and can be queued
+  // before batch t-1 is collected (no host round trip between them)
   struct StreamSlot {
     float* d_xyz{nullptr};
     int64_t xyz_cap{0};
@@ -188,7 +189,8 @@ struct amppi_ctx {
     int S{0};
     int64_t ticket{-1};
   };
-  StreamSlot slots[2];
+  static constexpr int kStreamSlots = 3;
+  StreamSlot slots[kStreamSlots];
   int64_t next_ticket{0};
   uint32_t* h_flags{nullptr};  // mapped device error word (Perception::flags)
   // single-scene plan captured as a CUDA graph (the plan kernels of one
@@ -1552,11 +1554,13 @@ static int batch_outputs_gather(amppi_ctx* ctx, int S, amppi_batch_output* out, 
 
 // ---------------------------------------------------------------------------
 // Streaming batches: submit returns once the batch is queued; wait returns its
-// results.  Inputs go through one of two device slots, so with two batches in
+// results.  Inputs go through one of three device slots: with two batches in
 // flight the next batch's point upload (copy engine) runs under the current
 // batch's planning (SMs) -- the steady state is max(upload, planning) instead
-// of their sum.  Planning arrays are shared: batches plan one after another on
-// the context's streams.
+// of their sum; a third lets the caller queue batch t+1 before collecting
+// batch t-1, so the upload starts the moment the copy engine is free rather
+// than after a host round trip.  Planning arrays are shared: batches plan one
+// after another on the context's streams.
 // ---------------------------------------------------------------------------
 static size_t gather_bytes(const amppi_ctx* ctx) {
   const size_t Sc = static_cast<size_t>(ctx->S_cap);
@@ -1581,8 +1585,8 @@ extern "C" int amppi_cycle_batch_submit(amppi_ctx* ctx, const amppi_batch_input*
     max_scene = std::max(max_scene, n);
   }
   const int64_t total = in->point_offsets[S];
-  amppi_ctx::StreamSlot& sl = ctx->slots[ctx->next_ticket & 1];
-  if (sl.busy) return ctx->fail(AMPPI_INVALID_ARGUMENT, "two batches already in flight: wait for one first");
+  amppi_ctx::StreamSlot& sl = ctx->slots[ctx->next_ticket % amppi_ctx::kStreamSlots];
+  if (sl.busy) return ctx->fail(AMPPI_INVALID_ARGUMENT, "three batches already in flight: wait for one first");
   if (total > ctx->P_cap) {  // the candidate log and point tables are sized by P_cap
     CK(cudaDeviceSynchronize());
     if (int rc = alloc_points(ctx, total); rc != AMPPI_OK) return rc;
@@ -1664,7 +1668,8 @@ extern "C" int amppi_cycle_batch_submit(amppi_ctx* ctx, const amppi_batch_input*
 extern "C" int amppi_cycle_batch_wait(amppi_ctx* ctx, int64_t ticket, amppi_batch_output* out) {
   NvtxRange nvtx_range("amppi_cycle_batch_wait");
   if (!ctx) return AMPPI_INVALID_ARGUMENT;
-  amppi_ctx::StreamSlot& sl = ctx->slots[ticket & 1];
+  if (ticket < 0) return ctx->fail(AMPPI_INVALID_ARGUMENT, "unknown ticket");
+  amppi_ctx::StreamSlot& sl = ctx->slots[ticket % amppi_ctx::kStreamSlots];
   if (!sl.busy || sl.ticket != ticket) return ctx->fail(AMPPI_INVALID_ARGUMENT, "unknown or already collected ticket");
   CK(cudaEventSynchronize(sl.done));
   sl.busy = false;

@@ -555,7 +555,7 @@ class Planner:
                            goals: np.ndarray, last_applied: np.ndarray, cycles: np.ndarray, seeds: np.ndarray,
                            previous: np.ndarray | None = None, r_max: float = 10.0) -> int:
         """Streaming form (amppi_cycle_batch_submit): queue the batch and return
-        a ticket; up to two batches in flight, so the next batch's upload
+        a ticket; up to three batches in flight, so the next batch's upload
         overlaps this one's planning.  xyz should be pinned memory (e.g. a
         torch pin_memory() tensor's numpy view) for the copy to be asynchronous."""
         bi, arrs, out, bo = self._batch_structs(offsets, xyz, poses, states, goals, last_applied, cycles, seeds,

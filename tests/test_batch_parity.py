@@ -154,9 +154,9 @@ def test_device_entry_point_equals_host(batch):
 
 
 def test_streaming_batches_equal_blocking(big_batch):
-    """amppi_cycle_batch_submit / _wait with two batches in flight (the next
-    batch's upload overlapping the current one's planning) return exactly what
-    the blocking call returns for each batch."""
+    """amppi_cycle_batch_submit / _wait with two and three batches in flight
+    (the next batch's upload overlapping the current one's planning) return
+    exactly what the blocking call returns for each batch."""
     import torch
 
     cfg, data, planner = big_batch
@@ -174,3 +174,11 @@ def test_streaming_batches_equal_blocking(big_batch):
         for k in r:
             assert np.array_equal(got[k], r[k]), k
     assert not np.array_equal(ref[0]["control"], ref[1]["control"])  # the batches really differ
+    # three in flight (the bench's e2e pattern), then a fourth refused until one is collected
+    ts = [planner.cycle_batch_submit(*args, c, data["seeds"]) for c in cyc]
+    with pytest.raises(ValueError, match="in flight"):
+        planner.cycle_batch_submit(*args, cyc[0], data["seeds"])
+    for t, r in zip(ts, ref):
+        got = planner.cycle_batch_wait(t)
+        for k in r:
+            assert np.array_equal(got[k], r[k]), k
