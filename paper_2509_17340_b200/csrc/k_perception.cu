@@ -290,6 +290,9 @@ constexpr int kFinalizeThreads = AMPPI_SNAP_THREADS;  // fused per-scene CTAs (t
 constexpr int kFinalizeThreadsFew = 1024;  // k_finalize_scene for a handful of scenes (latency)
 constexpr int kMaxWarps = kFinalizeThreadsFew / 32;
 constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
+#ifndef AMPPI_SORT_REGS
+#define AMPPI_SORT_REGS 1  // grid-build sort: in-window stages in registers (0: every stage in shared memory)
+#endif
 #ifndef AMPPI_POOL_STRIDED
 #define AMPPI_POOL_STRIDED 1  // filtered compaction: one thread per filtered slot (0: per-thread cell chunks)
 #endif
@@ -578,6 +581,87 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
       }
     }
   };
+#if AMPPI_SORT_REGS
+  // Stages that stay inside a 64-key window (every stage of sizes <= 64, and
+  // the strides 32..1 that end every larger merge) run in registers: each
+  // warp loads a window as two 64-bit (key << 16 | value) words per lane
+  // (positions l and l + 32), exchanges them with shuffles and stores once.
+  // The comparisons are on the key alone with the shared-memory stages' tie
+  // rule (swap only when the lower position holds the larger key).
+  {
+    const int lane = tid & 31, nw = static_cast<int>(blockDim.x >> 5);
+    const uint32_t nwin = (n_pts + 63) / 64;
+    auto kof = [](uint64_t x) { return static_cast<uint32_t>(x >> 16); };
+    auto ce_lane = [&](uint64_t& x, int partner, bool lower) {
+      const uint64_t y = __shfl_sync(0xffffffffu, x, partner);
+      if (lower ? kof(x) > kof(y) : kof(y) > kof(x)) x = y;
+    };
+    auto ce_slot = [&](uint64_t& a, uint64_t& b) {  // positions l (a) and l + 32 (b)
+      if (kof(a) > kof(b)) {
+        const uint64_t t = a;
+        a = b;
+        b = t;
+      }
+    };
+    auto halves = [&](uint64_t& a, uint64_t& b, int from) {  // half-cleaners, strides from..1 (<= 16)
+      for (int st = from; st > 0; st >>= 1) {
+        ce_lane(a, lane ^ st, !(lane & st));
+        ce_lane(b, lane ^ st, !(lane & st));
+      }
+    };
+    auto window = [&](bool first) {
+      for (uint32_t w = tid >> 5; w < nwin; w += nw) {
+        const uint32_t i0 = 64 * w + lane, i1 = i0 + 32;
+        uint64_t a = i0 < n_pts ? (static_cast<uint64_t>(keys[i0]) << 16) | vals[i0] : ~0ull;
+        uint64_t b = i1 < n_pts ? (static_cast<uint64_t>(keys[i1]) << 16) | vals[i1] : ~0ull;
+        if (first) {  // sizes 2..32 in each half, then size 64 across the halves
+          for (int size = 2; size <= 32; size <<= 1) {
+            ce_lane(a, lane ^ (size - 1), !(lane & (size >> 1)));  // flip
+            ce_lane(b, lane ^ (size - 1), !(lane & (size >> 1)));
+            halves(a, b, size >> 2);
+          }
+          const uint64_t am = __shfl_sync(0xffffffffu, a, lane ^ 31), bm = __shfl_sync(0xffffffffu, b, lane ^ 31);
+          if (kof(a) > kof(bm)) a = bm;  // flip of 64: l (lower) <-> 63 - l
+          if (kof(am) > kof(b)) b = am;
+          halves(a, b, 16);
+        } else {  // the end of a larger merge: strides 32..1
+          ce_slot(a, b);
+          halves(a, b, 16);
+        }
+        if (i0 < n_pts) {
+          keys[i0] = kof(a);
+          vals[i0] = static_cast<uint16_t>(a & 0xFFFFu);
+        }
+        if (i1 < n_pts) {
+          keys[i1] = kof(b);
+          vals[i1] = static_cast<uint16_t>(b & 0xFFFFu);
+        }
+      }
+    };
+    window(true);
+    __syncthreads();
+    for (uint32_t size = 128; size <= n2; size <<= 1) {
+      const uint32_t half = size >> 1;
+      const uint32_t tf = min(n2 >> 1, (n_pts + size) >> 1);
+      for (uint32_t t = tid; t < tf; t += blockDim.x) {  // flip: i <-> mirror in its block
+        const uint32_t o = t & (half - 1);
+        const uint32_t i = 2 * t - o;
+        cx(i, i + size - 1 - 2 * o);
+      }
+      __syncthreads();
+      for (uint32_t stride = half >> 1; stride >= 64; stride >>= 1) {
+        const uint32_t th = min(n2 >> 1, (n_pts + stride) >> 1);
+        for (uint32_t t = tid; t < th; t += blockDim.x) {
+          const uint32_t i = 2 * t - (t & (stride - 1));
+          cx(i, i + stride);
+        }
+        __syncthreads();
+      }
+      window(false);
+      __syncthreads();
+    }
+  }
+#else
   for (uint32_t size = 2; size <= n2; size <<= 1) {
     const uint32_t half = size >> 1;
     const uint32_t tf = min(n2 >> 1, (n_pts + size) >> 1);
@@ -598,6 +682,7 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
     }
   }
   __syncthreads();
+#endif
   SNAP_PHASE(5);  // sort keys + bitonic sort
   // scatter into sorted order and flag leaf starts: every cell's points form
   // leaves of kLeafSize consecutive (Morton-ordered) points
