@@ -766,26 +766,32 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   const uint32_t wstride = 2 * (blockDim.x >> 5);
   for (uint32_t l0 = 2 * warp; l0 < n_leaves; l0 += wstride) {
     const uint32_t l = l0 + (lane >> 4);
-    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    // each point's local coordinate rounded down / up to float, then a float
+    // min / max: rounding is monotone, so this is the outward-rounded box of
+    // the FP64 minimum and maximum, in half the shuffles
+    float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     static_assert(kLeafSize <= 16, "one lane per leaf point");
     if (l < n_leaves) {
       const uint32_t t = (lstart[l] & 0x7FFFFFFFu) + sub;
       if (t < (lstart[l + 1] & 0x7FFFFFFFu))
 #pragma unroll
-        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = gp64[3 * t + a] - meta.org[a];  // local frame, as gp32
+        for (int a = 0; a < 3; ++a) {
+          const double v = gp64[3 * t + a] - meta.org[a];  // local frame, as gp32
+          lo[a] = __double2float_rd(v);
+          hi[a] = __double2float_ru(v);
+        }
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-        hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+        hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
       }
     if (sub == 0 && l < n_leaves) {
-      gleaf[2 * l] = make_uint4(__float_as_uint(__double2float_rd(lo[0])), __float_as_uint(__double2float_ru(hi[0])),
-                                __float_as_uint(__double2float_rd(lo[1])), __float_as_uint(__double2float_ru(hi[1])));
-      gleaf[2 * l + 1] =
-          make_uint4(__float_as_uint(__double2float_rd(lo[2])), __float_as_uint(__double2float_ru(hi[2])), 0u, 0u);
+      gleaf[2 * l] = make_uint4(__float_as_uint(lo[0]), __float_as_uint(hi[0]), __float_as_uint(lo[1]),
+                                __float_as_uint(hi[1]));
+      gleaf[2 * l + 1] = make_uint4(__float_as_uint(lo[2]), __float_as_uint(hi[2]), 0u, 0u);
     }
   }
   __syncthreads();
