@@ -744,20 +744,30 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   // leaf ids = prefix count of leaf starts (contiguous 16-point chunks per thread)
   const uint32_t kPerThread = kCellsPow2 / blockDim.x;  // blockDim.x divides 8192
   const uint32_t i0 = tid * kPerThread;
-  uint32_t n_leaf_starts = 0;
-  for (uint32_t i = i0; i < i0 + kPerThread; ++i) n_leaf_starts += lflag[i];
-  const uint32_t leaf0 = block_exclusive_scan(n_leaf_starts, sm.warp_sums, &sm.total);
-  const uint32_t n_leaves = sm.total;
-  // leaf start table (sm.idx is dead by now): point index, bit 31 = starts a cell
+  // (and the cells' first leaves: leaf starts in the low 16 bits of the
+  // scanned count, cell starts in the high 16; both <= 8192)
+  auto cell_start = [&](uint32_t i) { return i == 0 || (keys[i - 1] >> 9) != (keys[i] >> 9); };
+  uint32_t counts = 0;
+  for (uint32_t i = i0; i < i0 + kPerThread; ++i)
+    if (lflag[i]) counts += 1u + (i < n_pts && cell_start(i) ? 0x10000u : 0u);
+  const uint32_t first = block_exclusive_scan(counts, sm.warp_sums, &sm.total);
+  const uint32_t n_leaves = sm.total & 0xFFFFu, n_cells = sm.total >> 16;
+  // leaf start table (sm.idx is dead by now): point index, bit 31 = starts a
+  // cell; and the cells' first leaves in cell order (u16, in the dead vals)
   uint32_t* lstart = sm.idx;
+  uint16_t* cleaf = vals;  // [n_cells + 1]
   {
-    uint32_t leaf = leaf0;
+    uint32_t leaf = first & 0xFFFFu, cell = first >> 16;
     for (uint32_t i = i0; i < i0 + kPerThread && i < n_pts; ++i) {
       if (!lflag[i]) continue;
-      const bool cell_start = i == 0 || (keys[i - 1] >> 9) != (keys[i] >> 9);
-      lstart[leaf++] = i | (cell_start ? 0x80000000u : 0u);
+      const bool cs = cell_start(i);
+      if (cs) cleaf[cell++] = static_cast<uint16_t>(leaf);
+      lstart[leaf++] = i | (cs ? 0x80000000u : 0u);
     }
-    if (tid == 0) lstart[n_leaves] = n_pts | 0x80000000u;  // sentinel
+    if (tid == 0) {
+      lstart[n_leaves] = n_pts | 0x80000000u;  // sentinel
+      cleaf[n_cells] = static_cast<uint16_t>(n_leaves);
+    }
   }
   __syncthreads();
   // leaf boxes: 16 lanes per leaf (2 leaves per warp, warp-uniform loop),
@@ -796,24 +806,12 @@ __device__ void finalize_body(FinalizeSmem& sm, const BatchIn& in, const Percept
   }
   __syncthreads();
   SNAP_PHASE(7);  // leaf boxes
-  // cell records: 16 lanes per cell-starting leaf; the cell's leaves are the
-  // leaves up to the next cell start (the sentinel ends the scan); box = union
-  // of their boxes
-  for (uint32_t l0 = 2 * warp; l0 < n_leaves; l0 += wstride) {
-    const uint32_t l = l0 + (lane >> 4);
-    const bool act = l < n_leaves && (lstart[l] & 0x80000000u);
-    uint32_t nl = 0;
-    bool done = !act;
-    for (uint32_t off = 1;; off += 16) {
-      const uint32_t q = l + off + sub;
-      const bool cs = !done && q <= n_leaves && (lstart[q] & 0x80000000u);
-      const unsigned m = (__ballot_sync(0xffffffffu, cs) >> (lane & 16)) & 0xFFFFu;
-      if (!done && m) {
-        nl = off + __ffs(m) - 1;
-        done = true;
-      }
-      if (__all_sync(0xffffffffu, done)) break;
-    }
+  // cell records: 16 lanes per non-empty cell (its leaves run from its first
+  // leaf to the next cell's, cleaf); box = union of the leaf boxes
+  for (uint32_t c0 = 2 * warp; c0 < n_cells; c0 += wstride) {  // one non-empty cell per 16 lanes
+    const uint32_t ci = c0 + (lane >> 4);
+    const bool act = ci < n_cells;
+    const uint32_t l = act ? cleaf[ci] : 0u, nl = act ? cleaf[ci + 1] - l : 0u;
     float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (uint32_t k = sub; k < nl; k += 16) {
       const uint4 la = gleaf[2 * (l + k)], lb = gleaf[2 * (l + k) + 1];
