@@ -306,9 +306,15 @@ constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 #define AMPPI_LOCAL_FRAME 1  // FP32 grid data and screening relative to the snapshot pose (0: world frame)
 #endif
 
+// The rng..idx region (86 KB) is reused phase by phase: keying's u64 range
+// bits (rng) and argmin indices (idx); pooling's ranges; the compaction map
+// (comp_k / comp_f in rng); the grid build's byte layout from rng:
+// keys u32[8192] @0, vals u16[8192] @32K (then the cells' first leaves),
+// leaf flags u8[8192] @48K, cell-start bitmap u32[256] @56K, and the leaf
+// start table u32[] in idx.
 struct FinalizeSmem {
-  double rng[kCells];  // also the u64 range-bits table during fused keying, and
-  uint32_t idx[kCells + 1];  // (rng..idx, 86 KB) the sort keys / values of the grid build; then leaf starts
+  double rng[kCells];
+  uint32_t idx[kCells + 1];
   uint32_t rows[kGridAxis * kGridAxis];  // non-empty grid cells: bit z of row (x, y)
   uint32_t warp_sums[kMaxWarps];
   double bbox_lo[kMaxWarps][3];
