@@ -92,8 +92,11 @@ def full(path):
         if fl == fl and hz == hz:
             print(f"| executed FP32 flops (2 FFMA + FADD + FMUL) | {fl:.0f} /cycle = {fl * hz / 1e12:.2f} TFLOP/s "
                   f"= {100 * fl / peak:.1f}% of the {peak:.0f}/cycle FFMA peak |")
-        dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
-        print(f"| DRAM traffic read+write | {dram:.1f} {units[col['dram__bytes_read.sum']]} |")
+        scale = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12}
+        def nbytes(m):  # ncu picks a unit per column
+            return num(m) * scale.get(units[col[m]].lower(), float("nan")) if m in col else float("nan")
+        dram = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
+        print(f"| DRAM traffic read+write | {dram / 1e6:.1f} Mbyte |")
         print()
 
 
