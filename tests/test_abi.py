@@ -112,3 +112,24 @@ def test_invalid_config_rejected(product_lib):
     c.horizon = 0
     h = ctypes.c_void_p()
     assert product_lib.amppi_create(ctypes.byref(c), None, ctypes.byref(h)) == _abi.AMPPI_INVALID_ARGUMENT
+
+
+def test_plan_result_records_are_built_on_access():
+    """PlanResult.per_instance / anchors (planner._Records): a read-only
+    sequence that builds each record once, on first access."""
+    from paper_2509_17340_b200.planner import _Records
+
+    made = []
+
+    def make(i):
+        made.append(i)
+        return {"m": i}
+
+    r = _Records(4, make)
+    assert len(r) == 4 and made == []
+    assert r[2] == {"m": 2} and r[-1] == {"m": 3} and made == [2, 3]
+    assert r[2] is r[2] and made == [2, 3]  # cached
+    assert [x["m"] for x in r] == [0, 1, 2, 3]
+    assert [x["m"] for x in r[1:3]] == [1, 2]
+    with pytest.raises(IndexError):
+        r[4]
