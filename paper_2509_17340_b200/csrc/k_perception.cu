@@ -172,6 +172,26 @@ __device__ __forceinline__ bool key_point(const PoseFrame& pose, V3<double> w, d
   return true;
 }
 
+// key_point without the FP64 / correctly rounded fallbacks: 0 = out of range,
+// 1 = keyed, 2 = inside a guard band (the caller defers it to key_point, so
+// a warp does not idle behind the one lane on the slow path)
+__device__ __forceinline__ int key_point_fast(const PoseFrame& pose, V3<double> w, double r_max, int& f,
+                                              uint64_t& bits) {
+  const V3<double> p = to_body(pose, w);
+  const double r = sqrt(sqnorm(p));
+  if (!(r > kMinPointRange) || r > r_max) return 0;
+  constexpr float kInvStepF = static_cast<float>(1.0 / 0x1.acee9f37bebd5p-5);
+  const float xf = static_cast<float>(p.x), yf = static_cast<float>(p.y);
+  int i = fast_cell(yf, xf, 3.14159265358979f, kInvStepF);
+  const int j = fast_cell(static_cast<float>(p.z), sqrtf(xf * xf + yf * yf), 1.57079632679490f, kInvStepF);
+  if (i < 0 || j < 0) return 2;
+  if (i >= kAz) i -= kAz;  // as cell_key
+  i = i > kAz - 1 ? kAz - 1 : i;
+  f = i * kEl + (j > kEl - 1 ? kEl - 1 : j);
+  bits = static_cast<uint64_t>(__double_as_longlong(r));
+  return 1;
+}
+
 // ---------------------------------------------------------------------------
 // global schedule (large scenes)
 // ---------------------------------------------------------------------------
@@ -296,6 +316,9 @@ constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 #ifndef AMPPI_POOL_STRIDED
 #define AMPPI_POOL_STRIDED 1  // filtered compaction: one thread per filtered slot (0: per-thread cell chunks)
 #endif
+#ifndef AMPPI_KEY_DEFER
+#define AMPPI_KEY_DEFER 512  // fused pass A: guard-band points deferred per scene (then keyed by full warps)
+#endif
 #ifndef AMPPI_LOG_BITS
 #define AMPPI_LOG_BITS 1  // fused pass A logs (cell, index, range bits); 0: (cell, index), pass B re-keys
 #endif
@@ -312,6 +335,8 @@ constexpr uint32_t kCellsPow2 = 8192;  // sort capacity >= kCells
 // keys u32[8192] @0, vals u16[8192] @32K (then the cells' first leaves),
 // leaf flags u8[8192] @48K, cell-start bitmap u32[256] @56K, and the leaf
 // start table u32[] in idx.
+constexpr uint32_t kKeyDeferCap = AMPPI_KEY_DEFER;  // (0 keeps the slow path inline)
+
 struct FinalizeSmem {
   double rng[kCells];
   uint32_t idx[kCells + 1];
@@ -323,6 +348,8 @@ struct FinalizeSmem {
   PoseFrame pose;
   uint32_t total;
   uint32_t n_cand;
+  uint32_t n_defer;
+  uint32_t defer[kKeyDeferCap];  // fused pass A: points whose fast key hit a guard band
 };
 
 // Block-wide exclusive scan of one value per thread; returns the prefix and
@@ -923,11 +950,31 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
   uint32_t* __restrict__ log = reinterpret_cast<uint32_t*>(P.cand) + b;  // [points of this scene]
   const bool rekey = e - b > 0x10000 || e > 4 * P.cand_cap;
 #endif
-  if (tid == 0) sm.n_cand = 0u;
+  if (tid == 0) {
+    sm.n_cand = 0u;
+    sm.n_defer = 0u;
+  }
   __syncthreads();
   // the log holds the scene's candidates at [b, e) of the context's candidate
   // buffer; a scene past 2^16 points or past that buffer re-keys in pass B
   const int lane = tid & 31;
+  // a warp's new candidates appended to the log (one shared atomic per warp)
+  auto log_cand = [&](bool cand, int f, int64_t g, uint64_t bits) {
+    const unsigned want = __ballot_sync(0xffffffffu, cand);
+    if (want) {
+      uint32_t base = 0;
+      if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
+      base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
+      if (cand && !rekey) {
+#if AMPPI_LOG_BITS
+        log[base + __popc(want & ((1u << lane) - 1u))] =
+            Candidate{static_cast<uint32_t>(f), static_cast<uint32_t>(g - b), bits};
+#else
+        log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
+#endif
+      }
+    }
+  };
   constexpr int kUnroll = 4;  // points per thread per iteration
   // software pipeline: the next iteration's points are loaded before this
   // iteration's keys are computed, so the HBM latency overlaps the keying
@@ -960,24 +1007,44 @@ __global__ void __launch_bounds__(kFinalizeThreads, AMPPI_SNAP_MINB) k_snapshot_
       uint64_t bits = 0;
       bool cand = false;
       bool skip = g >= e;
-      if (!skip && key_point(pose, w[u], r_max, f, bits)) cand = atomicMin(cell_bits + f, bits) >= bits;
-      const unsigned want = __ballot_sync(0xffffffffu, cand);
-      if (want) {
-        uint32_t base = 0;
-        if (lane == __ffs(want) - 1) base = atomicAdd(&sm.n_cand, static_cast<uint32_t>(__popc(want)));
-        base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
-        if (cand && !rekey) {
-#if AMPPI_LOG_BITS
-          log[base + __popc(want & ((1u << lane) - 1u))] =
-              Candidate{static_cast<uint32_t>(f), static_cast<uint32_t>(g - b), bits};
-#else
-          log[base + __popc(want & ((1u << lane) - 1u))] = (static_cast<uint32_t>(f) << 16) | static_cast<uint32_t>(g - b);
-#endif
+      if (!skip) {
+        int kr;
+        if constexpr (kKeyDeferCap > 0) {
+          kr = key_point_fast(pose, w[u], r_max, f, bits);
+          if (kr == 2) {
+            const uint32_t slot = atomicAdd(&sm.n_defer, 1u);
+            if (slot < kKeyDeferCap) {
+              sm.defer[slot] = static_cast<uint32_t>(g - b);
+              kr = 0;
+            } else {
+              kr = key_point(pose, w[u], r_max, f, bits) ? 1 : 0;  // (queue full: inline)
+            }
+          }
+        } else {
+          kr = key_point(pose, w[u], r_max, f, bits) ? 1 : 0;
         }
+        if (kr == 1) cand = atomicMin(cell_bits + f, bits) >= bits;
       }
+      log_cand(cand, f, g, bits);
     }
   }
   __syncthreads();
+  if constexpr (kKeyDeferCap > 0) {
+    // the deferred guard-band points, keyed with the FP64 / correctly rounded
+    // fallbacks by full warps (any arrival order gives the same minima, and a
+    // point tied with its cell's final minimum is logged whenever it arrives)
+    const uint32_t n_def = min(sm.n_defer, kKeyDeferCap);
+    for (uint32_t q0 = 0; q0 < n_def; q0 += blockDim.x) {
+      const uint32_t q = q0 + tid;
+      int f = 0;
+      uint64_t bits = 0;
+      bool cand = false;
+      const int64_t g = b + (q < n_def ? sm.defer[q] : 0u);
+      if (q < n_def && key_point(pose, load_point(in, g), r_max, f, bits)) cand = atomicMin(cell_bits + f, bits) >= bits;
+      log_cand(cand, f, g, bits);
+    }
+    __syncthreads();
+  }
   SNAP_PHASE(1);  // pass A keying
   // pass B: lowest point index among the logged points at the minimum
   // ("strict <, first point wins", perception.cpp:80-86).  The log packs the
