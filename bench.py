@@ -54,7 +54,7 @@ BYTES_PER_POINT = 12  # FP32 xyz read once by the keying pass
 # ncu --set full of the FP32 screening kernels (bound + main pass) on the C5
 # batch as one chunk: DRAM read+write per step and the main pass's issue-slot
 # use (profiles/r02_c5_full.md)
-TRAFFIC_BYTES_PER_LAUNCH = 198.2e6
+TRAFFIC_BYTES_PER_LAUNCH = 195.4e6
 TRAFFIC_SOURCE = "profiles/r02_c5_full.md"
 ISSUE_ACTIVE_FRAC = 0.7225
 # FP32 flops the two screening kernels executed in one C5 launch, counted by ncu on the SASS page
