@@ -233,6 +233,9 @@ __global__ void __launch_bounds__(256) k_key_points(BatchIn in, Perception P) {
 // the global minimum.
 __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total);
 
+#ifndef AMPPI_KEY_PPT
+#define AMPPI_KEY_PPT 8  // cluster keying: target points per thread (sets the clusters per scene)
+#endif
 constexpr int kKeyCluster = 8;
 constexpr int kKeyCellsPerRank = kCells / kKeyCluster;  // 900
 constexpr int kKeyThreads = 512;
@@ -1122,7 +1125,8 @@ cudaError_t launch_snapshot(const BatchIn& in, const Perception& P, const DevCon
   if (err != cudaSuccess) return err;
   {
     // clusters per scene: ~8 points per thread, at most ~2 waves of clusters
-    int64_t cps = (max_points_per_scene + 8 * kKeyCluster * kKeyThreads - 1) / (8 * kKeyCluster * kKeyThreads);
+    constexpr int64_t kPer = AMPPI_KEY_PPT;  // target points per thread
+    int64_t cps = (max_points_per_scene + kPer * kKeyCluster * kKeyThreads - 1) / (kPer * kKeyCluster * kKeyThreads);
     cps = cps < 1 ? 1 : (cps > 64 ? 64 : cps);
     TimedRegion t(timer, "k_key_points", st);
     k_key_points_cluster<<<dim3(static_cast<unsigned>(cps * kKeyCluster), in.S), kKeyThreads,
