@@ -76,6 +76,21 @@ def test_batch_warm_start_matches_oracle(oracle, batch):
     assert _check_against_oracle(oracle, cfg, data, out, previous=first["winner_nominal"], cycle_shift=1) > S // 2
 
 
+def test_batch_two_iterations_paper_grid(oracle):
+    """The paper's default ensemble (5x3 anchors x 256 samples x 25 steps)
+    with two MPPI iterations per cycle, on the throughput schedules: the
+    nominal update between iterations, the second iteration's perturbation
+    stream and its bound / main passes, scene by scene against the oracle."""
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.workloads import plan_config, scenes
+
+    cfg = plan_config(m_h=5, m_v=3, K=256, N=25, iterations=2)
+    data = scenes(S, points=20000, frames=20, first=3000)
+    with Planner(cfg, precision=32, max_scenes=S, max_points=int(data["offsets"][-1])) as planner:
+        out = _host_call(planner, data)
+    assert _check_against_oracle(oracle, cfg, data, out) > S // 2
+
+
 @pytest.fixture(scope="module")
 def big_batch():
     from paper_2509_17340_b200 import Planner
