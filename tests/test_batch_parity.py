@@ -91,6 +91,19 @@ def test_batch_two_iterations_paper_grid(oracle):
     assert _check_against_oracle(oracle, cfg, data, out) > S // 2
 
 
+def test_batch_precision64_matches_oracle(oracle):
+    """The FP64 screening (precision 64: every sample rolled out in FP64,
+    k_stage1_f64) on the batch path, scene by scene against the oracle."""
+    from paper_2509_17340_b200 import Planner
+    from paper_2509_17340_b200.workloads import plan_config, scenes
+
+    cfg = plan_config()
+    data = scenes(S, points=20000, frames=20, first=4000)
+    with Planner(cfg, precision=64, max_scenes=S, max_points=int(data["offsets"][-1])) as planner:
+        out = _host_call(planner, data)
+    assert _check_against_oracle(oracle, cfg, data, out) > S // 2
+
+
 @pytest.fixture(scope="module")
 def big_batch():
     from paper_2509_17340_b200 import Planner
