@@ -41,3 +41,4 @@ if __name__ == "__main__":
     stride = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     run("C5 4096-scene batch (forest / verticals / inclines), 4x2 x 256 x 30", plan_config(), n, 0, stride)
     run("C4-sized instances, 8x8 x 8192 x 50 (every 4th sample)", plan_config(8, 8, K=8192, N=50), 8, 4096, 4)
+    run("the paper's default ensemble, 5x3 x 256 x 25, 1024 scenes", plan_config(5, 3, K=256, N=25), 1024, 8192, 1)
